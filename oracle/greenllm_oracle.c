@@ -1,0 +1,341 @@
+/*
+ * greenllm_oracle.c -- plain, slow, single-threaded CPU oracle for the
+ * batched SLO / carbon evaluation of GreenLLM (arXiv 2412.20322).
+ *
+ * TEST INFRASTRUCTURE.  Only tests/, __graft_entry__.smoke() and bench.py's
+ * cpu_baseline / --impl reference legs may load this library.  It shares no
+ * code, header, table or constant generator with the CUDA path
+ * (paper_2412_20322_b200/csrc), and neither side includes the other.
+ *
+ * What it computes, literally and in the
+ * paper's order:
+ *   stage 1  prefill FCFS on the new GPU: c_i = max(c_{i-1}, a_i) + t1[p_i]
+ *            (§2.1; TTFT_i = c_i - a_i)
+ *   stage 2  FIFO KV link (DPD) or prompt handoff + draft
+ *            prefill (DSD): r_i = max(r_{i-1}, c_i) + t2[p_i]
+ *   decode   continuous batching stepped ONE ITERATION AT A TIME (no event
+ *            jumping, no precomputed demand): every member advances each
+ *            iteration; DPD by one token, DSD by 1 + #accepted draft tokens
+ *            drawn per member-step from Philox4x32-10 against the acceptance
+ *            thresholds floor(alpha^c * 2^32) (rejection rule P:111-114
+ *            collapsed to a marginal rate alpha, R22)
+ *   SLO      TTFT <= SLO_ttft and (o = 1 or finish - c <= SLO_tpot (o-1))
+ *            (Table 2; per-request mean TPOT, R25)
+ *   carbon   Eqs. 1-3 with the fixed expression of R34
+ *   Alg. 1   feasible set, argmin, fallback
+ * Every rule R1-R40 it follows is listed in DESIGN.md §2.
+ *
+ * Pins (tests/test_oracle_pins.py): Philox known-answer vectors; the E[acc]
+ * closed form (1-alpha^(g+1))/(1-alpha); hand-worked queueing examples
+ * (SURVEY Appendix A.1-A.5); an independent 1-us tick brute force on <=10
+ * requests and exhaustive tiny enumerations; the max-plus longest-path form of
+ * stages 1-2; the cap=1 Lindley recursion; the isolated-request and D/D/1
+ * closed forms; carbon closed forms S:55-74; Alg. 1 against brute force.
+ *
+ * Build: gcc -O2 -std=c11 -ffp-contract=off -shared -fPIC (no threads, no SIMD
+ * intrinsics).
+ */
+#include <math.h>
+#include <stdint.h>
+#include <stdlib.h>
+#include <string.h>
+
+#define OR_ST_UNSORTED 1u
+#define OR_ST_PROMPT_RANGE 2u
+#define OR_ST_OUTPUT_ZERO 4u
+#define OR_ST_OVERFLOW 8u
+#define OR_ST_NEG_ARRIVAL 16u
+
+#define OR_ACCEPT_STREAM 0x41434350u /* "ACCP": third Philox counter word */
+
+typedef struct {
+    int32_t mode; /* 0 = DPD, 1 = DSD */
+    int32_t cap;
+    int32_t gamma;
+    int32_t max_prompt;
+    double alpha;
+    uint64_t seed;
+    const int32_t *t1_us;
+    const int64_t *e1_new_uj;
+    const int32_t *t2_us;
+    const int32_t *b2_old_us;
+    const int64_t *e2_old_uj;
+    const int32_t *step_us;
+    const int32_t *step_busy_new_us;
+    const int32_t *step_busy_old_us;
+    const int64_t *step_e_new_uj;
+    const int64_t *step_e_old_uj;
+    int64_t ttft_slo_us;
+    int64_t tpot_slo_us;
+} or_chain;
+
+typedef struct {
+    int64_t n, slo_ok, tokens, busy_new_us, busy_old_us, e_new_uj, e_old_uj, makespan_us;
+    uint64_t req_hash;
+    uint32_t status, capacity_ok;
+} or_stats;
+
+/* ---------------- Philox4x32-10 (Salmon et al.; own implementation) ------- */
+static void or_philox(uint32_t ctr[4], uint32_t k0, uint32_t k1)
+{
+    for (int round = 0; round < 10; ++round) {
+        if (round > 0) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        uint64_t p0 = (uint64_t)0xD2511F53u * ctr[0];
+        uint64_t p1 = (uint64_t)0xCD9E8D57u * ctr[2];
+        uint32_t n0 = (uint32_t)(p1 >> 32) ^ ctr[1] ^ k0;
+        uint32_t n1 = (uint32_t)p1;
+        uint32_t n2 = (uint32_t)(p0 >> 32) ^ ctr[3] ^ k1;
+        uint32_t n3 = (uint32_t)p0;
+        ctr[0] = n0;
+        ctr[1] = n1;
+        ctr[2] = n2;
+        ctr[3] = n3;
+    }
+}
+
+void oracle_philox4x32_10(const uint32_t in_ctr[4], uint32_t k0, uint32_t k1, uint32_t out[4])
+{
+    uint32_t c[4] = {in_ctr[0], in_ctr[1], in_ctr[2], in_ctr[3]};
+    or_philox(c, k0, k1);
+    memcpy(out, c, sizeof c);
+}
+
+/* The acceptance draw of request j at its own step s (R22): word (s mod 4) of
+ * Philox(counter = (s/4, j, ACCEPT_STREAM, 0), key = seed). */
+static uint32_t or_accept_word(uint64_t seed, uint32_t j, uint32_t s)
+{
+    uint32_t c[4] = {s / 4u, j, OR_ACCEPT_STREAM, 0u};
+    or_philox(c, (uint32_t)seed, (uint32_t)(seed >> 32));
+    return c[s % 4u];
+}
+
+/* thr_c = floor(alpha^c * 2^32), alpha^c by left-to-right repeated products */
+void oracle_thresholds(double alpha, int32_t gamma, uint64_t *thr)
+{
+    double x = 1.0;
+    for (int c = 1; c <= gamma; ++c) {
+        x = x * alpha;
+        thr[c - 1] = (uint64_t)floor(x * 4294967296.0);
+    }
+}
+
+/* accepted tokens of one speculative step: 1 (target's own token) + the
+ * number of thresholds the uniform word falls under (R22) */
+int32_t oracle_accept_count(uint32_t u, const uint64_t *thr, int32_t gamma)
+{
+    int32_t acc = 1;
+    for (int c = 1; c <= gamma; ++c)
+        if ((uint64_t)u < thr[c - 1]) acc += 1;
+    return acc;
+}
+
+static uint64_t or_rotl(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
+/* SplitMix64 finaliser of j ^ rotl(ttft,21) ^ rotl(finish,42) */
+uint64_t oracle_mix64(uint64_t j, int64_t ttft, int64_t finish)
+{
+    uint64_t z = j ^ or_rotl((uint64_t)ttft, 21) ^ or_rotl((uint64_t)finish, 42);
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+static int64_t or_max(int64_t x, int64_t y) { return x > y ? x : y; }
+
+typedef struct {
+    int64_t j;
+    int64_t rem;
+    uint32_t s;
+} or_member;
+
+/*
+ * Simulate one timing chain.  ttft_out / finish_out / ready_out (stage-2
+ * completion r_i) may be NULL.  Returns the status bits (0 = valid input).
+ */
+uint32_t oracle_simulate_chain(const int64_t *a, const uint32_t *p, const uint32_t *o, int64_t n,
+                               const or_chain *ch, or_stats *st, int64_t *ttft_out,
+                               int64_t *finish_out, int64_t *ready_out)
+{
+    memset(st, 0, sizeof *st);
+    st->n = n;
+    uint32_t status = 0;
+    for (int64_t i = 0; i < n; ++i) {
+        if (a[i] < 0) status |= OR_ST_NEG_ARRIVAL;
+        if (i > 0 && a[i] < a[i - 1]) status |= OR_ST_UNSORTED;
+        if (p[i] < 1 || (int64_t)p[i] > ch->max_prompt) status |= OR_ST_PROMPT_RANGE;
+        if (o[i] < 1) status |= OR_ST_OUTPUT_ZERO;
+    }
+    st->status = status;
+    if (status || n <= 0) return status;
+
+    int64_t *c = malloc(sizeof(int64_t) * n);
+    int64_t *r = malloc(sizeof(int64_t) * n);
+    int64_t *fin = malloc(sizeof(int64_t) * n);
+    or_member *A = malloc(sizeof(or_member) * (ch->cap > 0 ? ch->cap : 1));
+    uint64_t thr[64];
+    if (ch->mode == 1) oracle_thresholds(ch->alpha, ch->gamma, thr);
+
+    /* stage 1: prefill FCFS on the new GPU */
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t start = (i == 0) ? a[i] : or_max(c[i - 1], a[i]);
+        c[i] = start + ch->t1_us[p[i]];
+        st->busy_new_us += ch->t1_us[p[i]];
+        st->e_new_uj += ch->e1_new_uj[p[i]];
+    }
+    /* stage 2: KV link (DPD) / handoff + draft prefill (DSD); o = 1 skips it */
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t s2 = (o[i] > 1) ? ch->t2_us[p[i]] : 0;
+        int64_t start = (i == 0) ? c[i] : or_max(r[i - 1], c[i]);
+        r[i] = start + s2;
+        if (o[i] > 1) {
+            st->busy_old_us += ch->b2_old_us[p[i]];
+            st->e_old_uj += ch->e2_old_uj[p[i]];
+        }
+    }
+    /* requests with a single output token finish at prefill completion */
+    for (int64_t i = 0; i < n; ++i) fin[i] = c[i];
+
+    /* decode: continuous batching, one iteration per loop pass */
+    int64_t T = 0;
+    int32_t size = 0;
+    int64_t nxt = 0;
+    while (nxt < n && o[nxt] <= 1) ++nxt;
+    while (nxt < n || size > 0) {
+        /* admit FCFS ready requests (r <= T) while there is room */
+        while (nxt < n && size < ch->cap && r[nxt] <= T) {
+            A[size].j = nxt;
+            A[size].rem = (int64_t)o[nxt] - 1;
+            A[size].s = 0;
+            ++size;
+            ++nxt;
+            while (nxt < n && o[nxt] <= 1) ++nxt;
+        }
+        if (size == 0) { /* idle until the next request is ready */
+            T = r[nxt];
+            continue;
+        }
+        /* one iteration at batch size b */
+        int32_t b = size;
+        T += ch->step_us[b];
+        st->busy_new_us += ch->step_busy_new_us[b];
+        st->busy_old_us += ch->step_busy_old_us[b];
+        st->e_new_uj += ch->step_e_new_uj[b];
+        st->e_old_uj += ch->step_e_old_uj[b];
+        for (int32_t m = 0; m < size;) {
+            if (ch->mode == 0) {
+                A[m].rem -= 1;
+            } else {
+                uint32_t u = or_accept_word(ch->seed, (uint32_t)A[m].j, A[m].s);
+                A[m].rem -= oracle_accept_count(u, thr, ch->gamma);
+                A[m].s += 1;
+            }
+            if (A[m].rem <= 0) {
+                fin[A[m].j] = T;
+                A[m] = A[size - 1];
+                --size;
+            } else {
+                ++m;
+            }
+        }
+    }
+
+    /* per-request SLO and chain statistics */
+    for (int64_t i = 0; i < n; ++i) {
+        int64_t ttft = c[i] - a[i];
+        int ok = (ttft <= ch->ttft_slo_us) &&
+                 (o[i] == 1 || fin[i] - c[i] <= ch->tpot_slo_us * (int64_t)(o[i] - 1));
+        st->slo_ok += ok;
+        st->tokens += o[i];
+        if (fin[i] > st->makespan_us) st->makespan_us = fin[i];
+        st->req_hash += oracle_mix64((uint64_t)i, ttft, fin[i]);
+        if (ttft_out) ttft_out[i] = ttft;
+        if (finish_out) finish_out[i] = fin[i];
+        if (ready_out) ready_out[i] = r[i];
+    }
+    free(c);
+    free(r);
+    free(fin);
+    free(A);
+    return 0;
+}
+
+/* Eqs. 1-3 with the fixed expression of R34 (no contraction: -ffp-contract=off) */
+void oracle_carbon(const or_stats *st, double ce_new_g, double ce_old_g, double ci,
+                   double lt_new_s, double lt_old_s, double out[3])
+{
+    double kwh_new = (double)st->e_new_uj / 3.6e12;
+    double kwh_old = (double)st->e_old_uj / 3.6e12;
+    double op = (kwh_new + kwh_old) * ci;
+    double emb = ((double)st->busy_new_us / 1e6) / lt_new_s * ce_new_g +
+                 ((double)st->busy_old_us / 1e6) / lt_old_s * ce_old_g;
+    out[0] = op;
+    out[1] = emb;
+    out[2] = op + emb;
+}
+
+/* attainment comparison by cross-multiplication: sign(ok1/n1 - ok2/n2) */
+static int or_cmp_att(int64_t ok1, int64_t n1, int64_t ok2, int64_t n2)
+{
+    __int128 l = (__int128)ok1 * n2, rr = (__int128)ok2 * n1;
+    return (l > rr) - (l < rr);
+}
+
+/*
+ * Alg. 1 over a rows x cols grid.  present[i] = 0 marks an absent
+ * cell.  cap_ok = 0 cells are infeasible and count as ok = 0, total = +inf in
+ * the fallback (R37).
+ */
+void oracle_alg1(int32_t rows, int32_t cols, const uint8_t *present, const double *total,
+                 const int64_t *ok, const int64_t *n, const uint8_t *cap_ok, int32_t slo_num,
+                 int32_t slo_den, int32_t priority, int32_t default_col, int32_t *choice,
+                 uint8_t *via_fallback)
+{
+    for (int32_t row = 0; row < rows; ++row) {
+        int32_t best = -1;
+        for (int32_t col = 0; col < cols; ++col) {
+            int64_t k = (int64_t)row * cols + col;
+            if (!present[k] || !cap_ok[k]) continue;
+            if ((__int128)slo_den * ok[k] < (__int128)slo_num * n[k]) continue; /* SLO_att < target */
+            if (best < 0) {
+                best = col;
+                continue;
+            }
+            int64_t kb = (int64_t)row * cols + best;
+            if (total[k] < total[kb] ||
+                (total[k] == total[kb] && or_cmp_att(ok[k], n[k], ok[kb], n[kb]) > 0))
+                best = col;
+        }
+        if (best >= 0) {
+            choice[row] = best;
+            via_fallback[row] = 0;
+            continue;
+        }
+        via_fallback[row] = 1;
+        if (priority != 0) {
+            choice[row] = default_col;
+            continue;
+        }
+        /* FallbackStrategy, priority = SLO: argmax attainment, then lower total */
+        for (int32_t col = 0; col < cols; ++col) {
+            int64_t k = (int64_t)row * cols + col;
+            if (!present[k]) continue;
+            int64_t okk = cap_ok[k] ? ok[k] : 0;
+            double tk = cap_ok[k] ? total[k] : INFINITY;
+            if (best < 0) {
+                best = col;
+                continue;
+            }
+            int64_t kb = (int64_t)row * cols + best;
+            int64_t okb = cap_ok[kb] ? ok[kb] : 0;
+            double tb = cap_ok[kb] ? total[kb] : INFINITY;
+            int cmp = or_cmp_att(okk, n[k], okb, n[kb]);
+            if (cmp > 0 || (cmp == 0 && tk < tb)) best = col;
+        }
+        choice[row] = best;
+    }
+}
+
+int32_t oracle_version(void) { return 1; }

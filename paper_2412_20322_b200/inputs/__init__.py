@@ -1,0 +1,15 @@
+"""Seeded synthetic inputs shared by the CUDA path and the oracle.
+
+Holds none of the method's arithmetic (queueing, carbon, Alg. 1): only the
+Philox-seeded traces, the integer latency/energy tables that stand in for the
+paper's profiling database, and the grid layouts of BASELINE.json's configs.
+"""
+from .grids import (MODE_DPD, MODE_DSD, PRIORITY_DEFAULT, PRIORITY_SLO, ChainSpec,
+                    GridSpec, build_config, custom_trace, subset_chains)
+from .tables import ChainTables, dpd_tables, dsd_tables
+from .workload import BASE_SEED, RATES8, WORKLOADS, Trace, make_trace
+
+__all__ = ["MODE_DPD", "MODE_DSD", "PRIORITY_DEFAULT", "PRIORITY_SLO", "ChainSpec",
+           "GridSpec", "build_config", "custom_trace", "subset_chains", "ChainTables",
+           "dpd_tables", "dsd_tables", "BASE_SEED", "RATES8", "WORKLOADS", "Trace",
+           "make_trace"]
