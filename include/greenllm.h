@@ -1,0 +1,213 @@
+/*
+ * greenllm.h -- C ABI of libgreenllm.so, the B200-native (sm_100a) batched
+ * SLO / carbon grid evaluator for GreenLLM (arXiv 2412.20322).
+ *
+ * The problem statement this ABI follows is Alg. 1 (§4.3):
+ *   input  a profiling database D, workloads W = {(req_size, qps)},
+ *          SLO_target and a fallback priority;
+ *   output the Optimal configuration per workload.
+ * gl_eval_grid replaces D by exact simulation of every candidate configuration
+ * on a request trace; gl_argmin_feasible IS Alg. 1 with
+ * the carbon matrix C computed from Eqs. 1-3.  gl_evaluate_host runs
+ * both end to end from host buffers.
+ *
+ * Conventions
+ *  - Times are integer microseconds (int64 absolute, int32 table entries),
+ *    energies integer microjoules, carbon grams (fp64), lifetimes seconds
+ *    (365-day years), carbon intensity gCO2/kWh.  DESIGN.md §2 lists every
+ *    rule (R1-R40) the simulation implements; the CPU oracle under oracle/
+ *    implements the same rules independently.
+ *  - "device" = CUDA device memory of the current device; "host" = CPU memory.
+ *  - The caller owns every buffer.  The library keeps no global state besides
+ *    a cached device-capability check, allocates only stream-ordered scratch
+ *    (cudaMallocAsync / cudaFreeAsync on `stream`) and never synchronises
+ *    except in gl_evaluate_host.
+ *  - Calls are asynchronous and stream-ordered (except gl_evaluate_host):
+ *    device buffers must stay valid until `stream` has passed the call; host
+ *    descriptor arrays are consumed before the call returns.
+ *  - Outputs are deterministic: bit-identical for identical inputs, for any
+ *    launch geometry, chain order or sharding.
+ *  - `stream` is a cudaStream_t passed as void* (NULL = legacy default stream).
+ *  - Errors: invalid host-visible arguments return a gl_status synchronously
+ *    and launch nothing.  Data-dependent violations found on the device are
+ *    reported per chain in gl_chain_stats.status (GL_ST_* bits); the chain's
+ *    other statistics are then unspecified.
+ */
+#ifndef GREENLLM_H
+#define GREENLLM_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define GL_VERSION 1
+#define GL_MAX_CAP 256        /* batch cap: 8 active-set slots per lane x 32 lanes */
+#define GL_MAX_GAMMA 16       /* DSD draft length */
+#define GL_MAX_PROMPT 16384   /* prompt-indexed tables live in shared memory */
+
+typedef int32_t gl_status;
+enum {
+    GL_OK = 0,
+    GL_E_INVALID = -1,     /* null pointer, n <= 0, cap/gamma/max_prompt out of range, misaligned */
+    GL_E_DOMAIN = -2,      /* alpha not in [0,1], negative SLO, CI < 0, LT <= 0, Ce <= 0, non-finite */
+    GL_E_LOOKUP = -3,      /* trace_idx, row_scenario, cell_chain or default_col out of range */
+    GL_E_CUDA = -4,        /* a CUDA runtime call or launch failed */
+    GL_E_UNSUPPORTED = -5  /* current device is not sm_100 (B200) */
+};
+
+enum { GL_MODE_DPD = 0, GL_MODE_DSD = 1 };           /* Disg-Pref-Decode / Disg-Spec-Decode */
+enum { GL_PRIORITY_SLO = 0, GL_PRIORITY_DEFAULT = 1 }; /* Alg. 1 FallbackStrategy */
+
+/* per-chain status bits, set on the device */
+enum {
+    GL_ST_UNSORTED = 1u,      /* arrival_us decreases somewhere */
+    GL_ST_PROMPT_RANGE = 2u,  /* prompt_len outside [1, max_prompt] */
+    GL_ST_OUTPUT_ZERO = 4u,   /* output_len == 0 */
+    GL_ST_OVERFLOW = 8u,      /* output_len >= 2^30 */
+    GL_ST_NEG_ARRIVAL = 16u,  /* arrival_us < 0 */
+    GL_ST_TABLE = 32u         /* t1/t2 < 0, or step_us[b] < 1 for some b in [1, batch_cap] */
+};
+
+/* One request trace, structure of arrays, sorted by arrival (R6).
+ * Device pointers for gl_eval_grid, host pointers for gl_evaluate_host
+ * (pinned memory recommended).  Each array must be 16-byte aligned. */
+typedef struct {
+    const int64_t *arrival_us;   /* [n] non-decreasing, >= 0 */
+    const uint32_t *prompt_len;  /* [n] in [1, max_prompt of every chain using the trace] */
+    const uint32_t *output_len;  /* [n] >= 1; counts prefill's first token (R7) */
+    int64_t n;                   /* 1 <= n < 2^31 */
+} gl_trace;
+
+/* One timing chain = one candidate configuration's timing: (trace, GPU pair,
+ * mode, gamma, alpha, batch cap, link).  Table pointers are DEVICE memory and
+ * stand in for the profiling database D.  Prompt-indexed tables have
+ * max_prompt+1 entries, batch-indexed ones batch_cap+1 entries (index 0 unused).
+ *   t1_us[p]      prefill latency of a p-token prompt on the new GPU (stage 1)
+ *   e1_new_uj[p]  its energy
+ *   t2_us[p]      stage-2 service: DPD KV transfer of p+1 tokens over the link
+ *                 (P:50-52); DSD prompt handoff + draft prefill (R12)
+ *   b2_old_us[p]  stage-2 busy time of the old GPU; e2_old_uj[p] its energy
+ *   step_us[b]    decode iteration (DPD) / speculative step (DSD, Fig. 7) latency
+ *                 at batch size b; step_busy_{new,old}_us[b], step_e_{new,old}_uj[b]
+ *                 the per-GPU busy time and energy of that iteration
+ * DSD acceptance: thr_c = floor(alpha^c * 2^32) (alpha^c by repeated products),
+ * accepted tokens per member-step = 1 + #{c in 1..gamma : u < thr_c}, u = word
+ * (s mod 4) of Philox4x32-10(counter (s/4, j, 0x41434350, 0), key = seed) for
+ * request j's own step s (R22; rejection rule P:111-114 as a marginal rate). */
+typedef struct {
+    int32_t mode;          /* GL_MODE_DPD or GL_MODE_DSD */
+    int32_t trace_idx;     /* index into the traces array */
+    int32_t batch_cap;     /* [1, GL_MAX_CAP] */
+    int32_t gamma;         /* DSD: [1, GL_MAX_GAMMA]; ignored for DPD */
+    int32_t max_prompt;    /* [1, GL_MAX_PROMPT] */
+    int32_t capacity_ok;   /* 0 => excluded from Alg. 1's feasible set (R38), still simulated */
+    double alpha;          /* DSD marginal acceptance rate in [0, 1] */
+    uint64_t seed;         /* DSD Philox key */
+    const int32_t *t1_us;
+    const int64_t *e1_new_uj;
+    const int32_t *t2_us;
+    const int32_t *b2_old_us;
+    const int64_t *e2_old_uj;
+    const int32_t *step_us;
+    const int32_t *step_busy_new_us;
+    const int32_t *step_busy_old_us;
+    const int64_t *step_e_new_uj;
+    const int64_t *step_e_old_uj;
+    int64_t ttft_slo_us;   /* Table 2 TTFT SLO, >= 0 */
+    int64_t tpot_slo_us;   /* Table 2 TPOT SLO, >= 0 */
+    double ce_new_g;       /* Table 1 embodied carbon of the new GPU, grams (> 0) */
+    double ce_old_g;       /* ... of the old GPU */
+} gl_chain;
+
+/* Sufficient statistics of one simulated chain (integers => bit-exact). 80 B. */
+typedef struct {
+    int64_t n;             /* requests */
+    int64_t slo_ok;        /* requests meeting TTFT and TPOT SLOs (R27) */
+    int64_t tokens;        /* sum of output_len */
+    int64_t busy_new_us;   /* new-GPU busy time (Eq. 1's t, R31) */
+    int64_t busy_old_us;
+    int64_t e_new_uj;      /* new-GPU energy (Eq. 2's E, R32) */
+    int64_t e_old_uj;
+    int64_t makespan_us;   /* max finish time */
+    uint64_t req_hash;     /* sum_j mix64(j, ttft_j, finish_j) mod 2^64 */
+    uint32_t status;       /* GL_ST_* bits */
+    uint32_t capacity_ok;  /* copied from the chain */
+} gl_chain_stats;
+
+/* One carbon scenario (a row's CI and lifetimes; changes only carbon). */
+typedef struct {
+    double ci_g_per_kwh;   /* >= 0, finite */
+    double lt_new_s;       /* > 0 */
+    double lt_old_s;       /* > 0 */
+} gl_scenario;
+
+/* Alg. 1 matrices (Fig. 8): rows = workloads/scenarios, cols =
+ * candidate configurations.  HOST arrays. */
+typedef struct {
+    int32_t rows, cols;           /* >= 1 */
+    const int32_t *row_scenario;  /* [rows] index into the scenarios */
+    const int32_t *cell_chain;    /* [rows*cols] chain scored in that cell, -1 = absent */
+} gl_grid;
+
+/*
+ * Simulate every timing chain on its trace (stages 1-2 as max-plus scans,
+ * continuous-batching decode as a per-warp event loop) and write one
+ * gl_chain_stats per chain.
+ *   traces, chains   HOST descriptor arrays; their data pointers are DEVICE
+ *   stats_out        DEVICE [n_chains]
+ *   per_request_out  DEVICE int64 [sum over chains of n(trace)][2] = (ttft_us,
+ *                    finish_us), chain-major in chain order; NULL to skip
+ */
+gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
+                       int32_t n_chains, gl_chain_stats *stats_out, int64_t *per_request_out,
+                       void *stream);
+
+/*
+ * Alg. 1 on the carbon matrix of Eqs. 1-3:
+ *   total = ((e_new/3.6e12) + (e_old/3.6e12)) * CI
+ *         + ((busy_new/1e6)/LT_new)*Ce_new + ((busy_old/1e6)/LT_old)*Ce_old
+ * (fixed order, no contraction: R34).  A cell is feasible iff capacity_ok and
+ * slo_den*slo_ok >= slo_num*n (SLO_att >= SLO_target).  Per row: argmin
+ * total over feasible cells, ties -> higher attainment -> lower column; if none
+ * is feasible via_fallback = 1 and: priority SLO -> argmax attainment (capacity-
+ * infeasible cells count as 0 and +inf), ties -> lower total -> lower column,
+ * -1 if the row has no present cell; priority DEFAULT -> default_col.
+ *   stats            DEVICE [n_chains] (all chains, e.g. after an allgather)
+ *   chains           HOST [n_chains] (ce_new_g, ce_old_g, capacity_ok are read)
+ *   scen             HOST [n_scen];  grid: HOST arrays
+ *   carbon_out       DEVICE double [rows*cols] (absent cells: NaN) or NULL
+ *   choice_out       DEVICE int32 [rows];  via_fallback_out DEVICE uint8 [rows]
+ */
+gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains,
+                             const gl_chain *chains, const gl_scenario *scen, int32_t n_scen,
+                             const gl_grid *grid, int32_t slo_num, int32_t slo_den,
+                             int32_t priority, int32_t default_col, double *carbon_out,
+                             int32_t *choice_out, uint8_t *via_fallback_out, void *stream);
+
+/*
+ * End to end from host buffers: copies the traces host->device, runs
+ * gl_eval_grid and gl_argmin_feasible, copies the results device->host and
+ * synchronises `stream` before returning.
+ *   host_traces      HOST descriptors with HOST data pointers
+ *   chains           as for gl_eval_grid (tables stay in DEVICE memory)
+ *   stats_host       HOST [n_chains];  carbon_host HOST [rows*cols] or NULL
+ *   choice_host      HOST [rows];      via_fallback_host HOST [rows]
+ */
+gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces,
+                           const gl_chain *chains, int32_t n_chains, const gl_scenario *scen,
+                           int32_t n_scen, const gl_grid *grid, int32_t slo_num,
+                           int32_t slo_den, int32_t priority, int32_t default_col,
+                           gl_chain_stats *stats_host, double *carbon_host,
+                           int32_t *choice_host, uint8_t *via_fallback_host, void *stream);
+
+/* Number of CUDA kernels the last successful call on this thread enqueued. */
+int32_t gl_last_launch_count(void);
+const char *gl_strerror(gl_status status);
+int32_t gl_version(void);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GREENLLM_H */

@@ -1,0 +1,171 @@
+"""Public Python API: resident device grids, gl_eval_grid / gl_argmin_feasible /
+gl_evaluate_host through the C ABI.  PyTorch provides device memory and
+streams only; every step of the path runs in libgreenllm.so's kernels.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import native as N
+from .inputs.grids import GridSpec
+
+
+def _dev_tensor(x: np.ndarray, device) -> torch.Tensor:
+    x = np.ascontiguousarray(x)
+    if x.dtype == np.uint32:
+        x = x.view(np.int32)  # same bits; the kernels read uint32
+    return torch.from_numpy(x).to(device)
+
+
+def _pinned(x: np.ndarray) -> torch.Tensor:
+    x = np.ascontiguousarray(x)
+    if x.dtype == np.uint32:
+        x = x.view(np.int32)
+    return torch.from_numpy(x).pin_memory()
+
+
+class DeviceGrid:
+    """A GridSpec resident in device memory: traces (SoA) and integer tables,
+    plus the host descriptor arrays the C ABI consumes."""
+
+    def __init__(self, grid: GridSpec, device="cuda", chain_ids=None):
+        self.grid = grid
+        self.device = torch.device(device)
+        self._keep = []
+        arr_cache = {}
+
+        def up(x):
+            k = id(x)
+            if k not in arr_cache:
+                arr_cache[k] = _dev_tensor(x, self.device)
+                self._keep.append(x)  # keep id() stable
+            return arr_cache[k]
+
+        self.trace_tensors = []
+        self.gl_traces = []
+        for tr in grid.traces:
+            a, p, o = up(tr.arrival_us), up(tr.prompt_len), up(tr.output_len)
+            self.trace_tensors.append((a, p, o))
+            self.gl_traces.append(N.GlTrace(a.data_ptr(), p.data_ptr(), o.data_ptr(), tr.n))
+        self.gl_chains = []
+        for ch in grid.chains:
+            t = ch.tables
+            tabs = [up(getattr(t, f)) for f in ("t1_us", "e1_new_uj", "t2_us", "b2_old_us",
+                                                 "e2_old_uj", "step_us", "step_busy_new_us",
+                                                 "step_busy_old_us", "step_e_new_uj",
+                                                 "step_e_old_uj")]
+            self.gl_chains.append(N.GlChain(
+                ch.mode, ch.trace_idx, ch.cap, ch.gamma if ch.mode == N.GL_MODE_DSD else 0,
+                t.max_prompt, int(ch.capacity_ok), float(ch.alpha), int(ch.seed) & (2**64 - 1),
+                *[x.data_ptr() for x in tabs], int(ch.ttft_slo_us), int(ch.tpot_slo_us),
+                float(ch.ce_new_g), float(ch.ce_old_g)))
+        self.n_chains = len(self.gl_chains)
+        self.chain_n = np.array([grid.traces[c.trace_idx].n for c in grid.chains], np.int64)
+        self.last_launches = 0
+
+    # ------------------------------------------------------------ host copies
+    def pinned_traces(self):
+        """Pinned host copies of the traces (inputs of the end-to-end path)."""
+        out = []
+        cache = {}
+        for tr in self.grid.traces:
+            arrs = []
+            for x in (tr.arrival_us, tr.prompt_len, tr.output_len):
+                if id(x) not in cache:
+                    cache[id(x)] = _pinned(x)
+                arrs.append(cache[id(x)])
+            out.append(tuple(arrs))
+        return out
+
+
+def _stream_ptr(stream) -> int:
+    if stream is None:
+        stream = torch.cuda.current_stream()
+    return stream.cuda_stream
+
+
+def eval_grid(dg: DeviceGrid, chain_lo: int = 0, chain_hi: int | None = None, stats=None,
+              per_request: bool = False, stream=None):
+    """Simulate chains [chain_lo, chain_hi) -> (stats uint8 tensor [k, 80], per-request
+    int64 tensor [sum n, 2] or None).  ``stats`` may be a preallocated view."""
+    hi = dg.n_chains if chain_hi is None else chain_hi
+    chains = dg.gl_chains[chain_lo:hi]
+    k = len(chains)
+    if stats is None:
+        stats = torch.empty((k, N.STATS_DTYPE.itemsize), dtype=torch.uint8, device=dg.device)
+    pr = None
+    if per_request:
+        tot = int(dg.chain_n[chain_lo:hi].sum())
+        pr = torch.empty((tot, 2), dtype=torch.int64, device=dg.device)
+    dg.last_launches = N.eval_grid(dg.gl_traces, chains, stats.data_ptr(),
+                                   pr.data_ptr() if pr is not None else None, _stream_ptr(stream))
+    return stats, pr
+
+
+def argmin_feasible(dg: DeviceGrid, stats: torch.Tensor, want_carbon: bool = True, stream=None):
+    """Alg. 1 over the grid -> (carbon f64 [rows, cols] or None, choice int32 [rows],
+    via_fallback uint8 [rows]) as device tensors."""
+    g = dg.grid
+    carbon = torch.empty((g.rows, g.cols), dtype=torch.float64, device=dg.device) \
+        if want_carbon else None
+    choice = torch.empty(g.rows, dtype=torch.int32, device=dg.device)
+    fb = torch.empty(g.rows, dtype=torch.uint8, device=dg.device)
+    dg.last_launches = N.argmin_feasible(
+        stats.data_ptr(), dg.gl_chains, g.scenarios, g.rows, g.cols, g.row_scenario,
+        g.cell_chain, g.slo_num, g.slo_den, g.priority, g.default_col,
+        carbon.data_ptr() if carbon is not None else None, choice.data_ptr(), fb.data_ptr(),
+        _stream_ptr(stream))
+    return carbon, choice, fb
+
+
+@dataclass
+class HostResult:
+    stats: np.ndarray
+    carbon: np.ndarray | None
+    choice: np.ndarray
+    via_fallback: np.ndarray
+    launches: int
+    h2d_bytes: int
+    d2h_bytes: int
+
+
+def evaluate_host(dg: DeviceGrid, host_traces, want_carbon: bool = False, stream=None,
+                  out: HostResult | None = None) -> HostResult:
+    """End to end through gl_evaluate_host: pinned host traces in, host results out."""
+    g = dg.grid
+    gl_tr = [N.GlTrace(a.data_ptr(), p.data_ptr(), o.data_ptr(), a.shape[0])
+             for (a, p, o) in host_traces]
+    if out is None:
+        out = HostResult(np.zeros(dg.n_chains, N.STATS_DTYPE),
+                         np.zeros((g.rows, g.cols)) if want_carbon else None,
+                         np.zeros(g.rows, np.int32), np.zeros(g.rows, np.uint8), 0, 0, 0)
+    out.launches = N.evaluate_host(gl_tr, dg.gl_chains, g.scenarios, g.rows, g.cols,
+                                   g.row_scenario, g.cell_chain, g.slo_num, g.slo_den, g.priority,
+                                   g.default_col, out.stats, out.carbon, out.choice,
+                                   out.via_fallback, _stream_ptr(stream))
+    seen = set()
+    h2d = 0
+    for arrs in host_traces:
+        for x in arrs:
+            if x.data_ptr() not in seen:
+                seen.add(x.data_ptr())
+            h2d += x.numel() * x.element_size()  # the ABI copies every trace's arrays
+    out.h2d_bytes = h2d
+    out.d2h_bytes = out.stats.nbytes + (out.carbon.nbytes if out.carbon is not None else 0) + \
+        out.choice.nbytes + out.via_fallback.nbytes
+    return out
+
+
+def stats_numpy(stats: torch.Tensor) -> np.ndarray:
+    """Device stats tensor -> numpy structured array (gl_chain_stats fields)."""
+    return stats.detach().cpu().numpy().view(N.STATS_DTYPE).reshape(-1)
+
+
+def check_status(stats_np: np.ndarray):
+    bad = np.nonzero(stats_np["status"])[0]
+    if bad.size:
+        raise N.GreenLLMError(N.GL_E_INVALID, f"device status bits {stats_np['status'][bad]} "
+                                              f"on chains {bad.tolist()}")

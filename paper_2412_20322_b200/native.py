@@ -1,0 +1,144 @@
+"""ctypes binding of libgreenllm.so (include/greenllm.h) -- marshalling only.
+
+Every step of the evaluated path runs in the CUDA kernels behind these entry
+points.  There is no CPU fallback: if the shared library is missing or the
+device is not sm_100 the calls raise.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(HERE, "libgreenllm.so")
+
+GL_OK, GL_E_INVALID, GL_E_DOMAIN, GL_E_LOOKUP, GL_E_CUDA, GL_E_UNSUPPORTED = 0, -1, -2, -3, -4, -5
+GL_MODE_DPD, GL_MODE_DSD = 0, 1
+GL_PRIORITY_SLO, GL_PRIORITY_DEFAULT = 0, 1
+GL_MAX_CAP, GL_MAX_GAMMA, GL_MAX_PROMPT = 256, 16, 16384
+ST_UNSORTED, ST_PROMPT_RANGE, ST_OUTPUT_ZERO, ST_OVERFLOW, ST_NEG_ARRIVAL, ST_TABLE = \
+    1, 2, 4, 8, 16, 32
+
+
+class GlTrace(C.Structure):
+    _fields_ = [("arrival_us", C.c_void_p), ("prompt_len", C.c_void_p),
+                ("output_len", C.c_void_p), ("n", C.c_int64)]
+
+
+class GlChain(C.Structure):
+    _fields_ = [("mode", C.c_int32), ("trace_idx", C.c_int32), ("batch_cap", C.c_int32),
+                ("gamma", C.c_int32), ("max_prompt", C.c_int32), ("capacity_ok", C.c_int32),
+                ("alpha", C.c_double), ("seed", C.c_uint64),
+                ("t1_us", C.c_void_p), ("e1_new_uj", C.c_void_p), ("t2_us", C.c_void_p),
+                ("b2_old_us", C.c_void_p), ("e2_old_uj", C.c_void_p), ("step_us", C.c_void_p),
+                ("step_busy_new_us", C.c_void_p), ("step_busy_old_us", C.c_void_p),
+                ("step_e_new_uj", C.c_void_p), ("step_e_old_uj", C.c_void_p),
+                ("ttft_slo_us", C.c_int64), ("tpot_slo_us", C.c_int64),
+                ("ce_new_g", C.c_double), ("ce_old_g", C.c_double)]
+
+
+class GlScenario(C.Structure):
+    _fields_ = [("ci_g_per_kwh", C.c_double), ("lt_new_s", C.c_double), ("lt_old_s", C.c_double)]
+
+
+class GlGrid(C.Structure):
+    _fields_ = [("rows", C.c_int32), ("cols", C.c_int32), ("row_scenario", C.c_void_p),
+                ("cell_chain", C.c_void_p)]
+
+
+# gl_chain_stats (80 B) as a numpy structured dtype
+STATS_DTYPE = np.dtype([("n", "<i8"), ("slo_ok", "<i8"), ("tokens", "<i8"),
+                        ("busy_new_us", "<i8"), ("busy_old_us", "<i8"), ("e_new_uj", "<i8"),
+                        ("e_old_uj", "<i8"), ("makespan_us", "<i8"), ("req_hash", "<u8"),
+                        ("status", "<u4"), ("capacity_ok", "<u4")])
+assert STATS_DTYPE.itemsize == 80
+SCEN_DTYPE = np.dtype([("ci", "<f8"), ("lt_new", "<f8"), ("lt_old", "<f8")])
+
+EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_last_launch_count",
+           "gl_strerror", "gl_version")
+
+_lib = None
+
+
+class GreenLLMError(RuntimeError):
+    def __init__(self, status: int, where: str):
+        msg = lib().gl_strerror(status).decode() if _lib is not None else str(status)
+        super().__init__(f"{where}: {msg} (status {status})")
+        self.status = status
+
+
+def lib():
+    """Load libgreenllm.so (built in-tree by __graft_entry__.build()); raise if absent."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise RuntimeError(f"CUDA extension missing: {LIB_PATH} (run __graft_entry__.build())")
+        L = C.CDLL(LIB_PATH)
+        vp, i32 = C.c_void_p, C.c_int32
+        L.gl_eval_grid.restype = i32
+        L.gl_eval_grid.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32, vp, vp, vp]
+        L.gl_argmin_feasible.restype = i32
+        L.gl_argmin_feasible.argtypes = [vp, i32, C.POINTER(GlChain), C.POINTER(GlScenario), i32,
+                                         C.POINTER(GlGrid), i32, i32, i32, i32, vp, vp, vp, vp]
+        L.gl_evaluate_host.restype = i32
+        L.gl_evaluate_host.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
+                                       C.POINTER(GlScenario), i32, C.POINTER(GlGrid), i32, i32,
+                                       i32, i32, vp, vp, vp, vp, vp]
+        L.gl_last_launch_count.restype = i32
+        L.gl_last_launch_count.argtypes = []
+        L.gl_strerror.restype = C.c_char_p
+        L.gl_strerror.argtypes = [i32]
+        L.gl_version.restype = i32
+        L.gl_version.argtypes = []
+        _lib = L
+    return _lib
+
+
+def check(status: int, where: str):
+    if status != GL_OK:
+        raise GreenLLMError(status, where)
+
+
+def eval_grid(traces, chains, stats_ptr: int, per_request_ptr: int | None, stream: int):
+    t_arr = (GlTrace * len(traces))(*traces)
+    c_arr = (GlChain * len(chains))(*chains)
+    check(lib().gl_eval_grid(t_arr, len(traces), c_arr, len(chains), stats_ptr,
+                             per_request_ptr or None, stream or None), "gl_eval_grid")
+    return lib().gl_last_launch_count()
+
+
+def argmin_feasible(stats_ptr: int, chains, scen: np.ndarray, rows: int, cols: int,
+                    row_scenario: np.ndarray, cell_chain: np.ndarray, slo_num: int, slo_den: int,
+                    priority: int, default_col: int, carbon_ptr: int | None, choice_ptr: int,
+                    fb_ptr: int, stream: int):
+    c_arr = (GlChain * len(chains))(*chains)
+    s = np.ascontiguousarray(scen, dtype=np.float64).reshape(-1, 3)
+    s_arr = (GlScenario * len(s))(*[GlScenario(*map(float, x)) for x in s])
+    rs = np.ascontiguousarray(row_scenario, dtype=np.int32)
+    cc = np.ascontiguousarray(cell_chain, dtype=np.int32)
+    g = GlGrid(rows, cols, rs.ctypes.data, cc.ctypes.data)
+    check(lib().gl_argmin_feasible(stats_ptr, len(chains), c_arr, s_arr, len(s), C.byref(g),
+                                   slo_num, slo_den, priority, default_col, carbon_ptr or None,
+                                   choice_ptr, fb_ptr, stream or None), "gl_argmin_feasible")
+    return lib().gl_last_launch_count()
+
+
+def evaluate_host(host_traces, chains, scen, rows, cols, row_scenario, cell_chain, slo_num,
+                  slo_den, priority, default_col, stats_out: np.ndarray, carbon_out,
+                  choice_out: np.ndarray, fb_out: np.ndarray, stream: int):
+    t_arr = (GlTrace * len(host_traces))(*host_traces)
+    c_arr = (GlChain * len(chains))(*chains)
+    s = np.ascontiguousarray(scen, dtype=np.float64).reshape(-1, 3)
+    s_arr = (GlScenario * len(s))(*[GlScenario(*map(float, x)) for x in s])
+    rs = np.ascontiguousarray(row_scenario, dtype=np.int32)
+    cc = np.ascontiguousarray(cell_chain, dtype=np.int32)
+    g = GlGrid(rows, cols, rs.ctypes.data, cc.ctypes.data)
+    check(lib().gl_evaluate_host(t_arr, len(host_traces), c_arr, len(chains), s_arr, len(s),
+                                 C.byref(g), slo_num, slo_den, priority, default_col,
+                                 stats_out.ctypes.data,
+                                 None if carbon_out is None else carbon_out.ctypes.data,
+                                 choice_out.ctypes.data, fb_out.ctypes.data, stream or None),
+          "gl_evaluate_host")
+    return lib().gl_last_launch_count()

@@ -1,0 +1,303 @@
+"""CUDA path (through the C ABI) vs the CPU oracle, element by element.
+
+Integer results (per-request TTFT / finish, every chain statistic, Alg. 1
+choice) must be bit-exact; fp64 carbon must be within 1e-9 relative (it is
+bit-identical by construction: same expression order, no contraction).
+"""
+import dataclasses
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2412_20322_b200 import api
+from paper_2412_20322_b200 import native as N
+from paper_2412_20322_b200.inputs import (MODE_DPD, MODE_DSD, GridSpec, build_config,
+                                          custom_trace)
+from tests.helpers import make_chain, make_tables, random_case
+
+pytestmark = pytest.mark.gpu
+
+INT_FIELDS = ("n", "slo_ok", "tokens", "busy_new_us", "busy_old_us", "e_new_uj", "e_old_uj",
+              "makespan_us", "req_hash", "status", "capacity_ok")
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _gpu():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a CUDA device")
+    N.lib()
+
+
+def grid_of(pairs, name="cases"):
+    """GridSpec with one trace and one chain per (trace, chain) pair, one row per chain."""
+    traces, chains = [], []
+    for i, (tr, ch) in enumerate(pairs):
+        traces.append(tr)
+        chains.append(dataclasses.replace(ch, trace_idx=i))
+    k = len(chains)
+    lt = 7 * 365 * 24 * 3600.0
+    return GridSpec(name, traces, chains, np.array([[261.0, lt, lt]]), np.zeros(k, np.int32),
+                    np.arange(k, dtype=np.int32), k, 1)
+
+
+def run_gpu(g, per_request=True):
+    dg = api.DeviceGrid(g)
+    stats, pr = api.eval_grid(dg, per_request=per_request)
+    carbon, choice, fb = api.argmin_feasible(dg, stats)
+    torch.cuda.synchronize()
+    return (api.stats_numpy(stats), None if pr is None else pr.cpu().numpy(),
+            carbon.cpu().numpy(), choice.cpu().numpy(), fb.cpu().numpy())
+
+
+def assert_parity(g, chain_ids=None, per_request=True, check_grid=True):
+    st, pr, carbon, choice, fb = run_gpu(g, per_request)
+    ids = range(len(g.chains)) if chain_ids is None else chain_ids
+    ref = O.evaluate_grid(g, chain_ids=ids, per_request=per_request)
+    offs = np.concatenate([[0], np.cumsum([g.traces[c.trace_idx].n for c in g.chains])])
+    for ci in ids:
+        want = ref["stats"][ci]
+        for f in INT_FIELDS:
+            assert int(st[ci][f]) == int(want[f]), (g.name, ci, f, int(st[ci][f]), int(want[f]))
+        if per_request and want["status"] == 0:
+            got = pr[offs[ci]:offs[ci + 1]]
+            ttft, fin = ref["per_request"][ci]
+            bad = np.nonzero((got[:, 0] != ttft) | (got[:, 1] != fin))[0]
+            assert bad.size == 0, (g.name, ci, bad[:5], got[bad[:5]], ttft[bad[:5]], fin[bad[:5]])
+    if check_grid and chain_ids is None:
+        m = ref["present"].astype(bool)
+        assert np.array_equal(carbon[m], ref["carbon"][m])  # bit-identical (R34)
+        np.testing.assert_allclose(carbon[m], ref["carbon"][m], rtol=1e-9)
+        assert np.array_equal(choice, ref["choice"])
+        assert np.array_equal(fb, ref["via_fallback"])
+    return st
+
+
+# ----------------------------------------------------------- random tiny cases
+def test_random_tiny_cases_vs_oracle():
+    rng = np.random.default_rng(20322)
+    pairs = [random_case(rng) for _ in range(400)]
+    assert_parity(grid_of(pairs), check_grid=True)
+
+
+@pytest.mark.parametrize("cap", [1, 2, 3, 16, 31, 32, 33, 64, 100, 128, 200, 256])
+def test_caps_and_slot_layouts(cap):
+    """SPL = 1/2/4/8 slots per lane, caps at and across the 32-lane boundaries."""
+    rng = np.random.default_rng(cap)
+    pairs = []
+    for mode in (MODE_DPD, MODE_DSD):
+        for n in (1, 7, 129, 1000):
+            tr, ch = random_case(rng, n=n, mode=mode, cap=cap)
+            a = np.sort(rng.integers(0, 40 * n, n))  # dense enough to fill big batches
+            pairs.append((custom_trace(a, tr.prompt_len, tr.output_len), ch))
+    assert_parity(grid_of(pairs))
+
+
+def test_medium_random_traces():
+    """Several chunks, ring wrap-around, ragged tails, mixed o = 1."""
+    rng = np.random.default_rng(5)
+    pairs = []
+    for n in (127, 128, 129, 255, 256, 257, 1000, 4099, 20000):
+        for mode in (MODE_DPD, MODE_DSD):
+            tr, ch = random_case(rng, n=n, mode=mode, cap=int(rng.integers(1, 40)))
+            a = np.sort(rng.integers(0, int(rng.integers(1, 200)) * n, n))
+            pairs.append((custom_trace(a, tr.prompt_len, tr.output_len), ch))
+    assert_parity(grid_of(pairs))
+
+
+# ------------------------------------------------------------------ edge cases
+def _edge_chain(cap=4, mode=MODE_DPD, gamma=0, alpha=0.0, t2zero=False, max_prompt=8, **kw):
+    tab = make_tables(max_prompt, cap, lambda p: 10 * p, (lambda p: 0) if t2zero else (lambda p: 3 * p),
+                      [0] + [20 + b for b in range(1, cap + 1)], e1=lambda p: 7 * p,
+                      b2=lambda p: p, e2=lambda p: 2 * p, sbn=[0] + [5] * cap,
+                      sbo=[0] + [20 + b for b in range(1, cap + 1)], sen=[0] + [9] * cap,
+                      seo=[0] + [11 * b for b in range(1, cap + 1)])
+    return make_chain(tab, mode, cap, gamma, alpha, ttft_slo=300, tpot_slo=40, **kw)
+
+
+def test_edge_cases():
+    pairs = []
+    # one request; o = 1 everywhere; equal arrivals; cap = 1; cap >= N
+    pairs.append((custom_trace([5], [3], [4]), _edge_chain()))
+    pairs.append((custom_trace([0, 0, 0, 0, 9], [1, 2, 3, 4, 5], [1, 1, 1, 1, 1]), _edge_chain()))
+    pairs.append((custom_trace([0] * 300, [2] * 300, [5] * 300), _edge_chain(cap=1)))
+    pairs.append((custom_trace(np.arange(50), [1] * 50, [3] * 50), _edge_chain(cap=256)))
+    # all-zero stage-2 table; r == boundary ties
+    pairs.append((custom_trace(np.arange(0, 2000, 21), [1] * 96, [4] * 96), _edge_chain(t2zero=True)))
+    # DSD alpha 0 / 1, gamma 1 / 16
+    for g, a in ((1, 0.0), (1, 1.0), (16, 1.0), (16, 0.5), (4, 0.8)):
+        pairs.append((custom_trace(np.arange(0, 3000, 13), [2] * 231, [1 + (i % 40) for i in range(231)]),
+                      _edge_chain(mode=MODE_DSD, gamma=g, alpha=a)))
+    # int64-large timestamps
+    big = 2**52 + np.arange(0, 500 * 37, 37)
+    pairs.append((custom_trace(big, [3] * 500, [6] * 500), _edge_chain(cap=8)))
+    # large prompt tables (GL_MAX_PROMPT) and a 1-entry table
+    pairs.append((custom_trace(np.arange(300) * 50, np.arange(1, 301) * 50, [3] * 300),
+                  _edge_chain(max_prompt=16384)))
+    pairs.append((custom_trace([0, 1, 2], [1, 1, 1], [2, 3, 4]), _edge_chain(max_prompt=1)))
+    assert_parity(grid_of(pairs))
+
+
+def test_status_bits_match_oracle():
+    pairs = [(custom_trace([5, 3, 7], [1, 1, 1], [2, 2, 2]), _edge_chain()),
+             (custom_trace([0, 3], [0, 99], [2, 2]), _edge_chain()),
+             (custom_trace([0, 3], [1, 1], [0, 2]), _edge_chain()),
+             (custom_trace([-4, 3], [1, 1], [1, 2]), _edge_chain())]
+    st, *_ = run_gpu(grid_of(pairs), per_request=False)
+    for i, (tr, ch) in enumerate(pairs):
+        want, _, _ = O.simulate_chain(tr, ch, per_request=False)
+        assert st[i]["status"] == want["status"] != 0
+    # table errors are device-only (GL_ST_TABLE)
+    bad = make_tables(4, 2, lambda p: 1, lambda p: 1, [0, 0, 3])
+    st, *_ = run_gpu(grid_of([(custom_trace([0], [1], [3]), make_chain(bad))]), per_request=False)
+    assert st[0]["status"] & N.ST_TABLE
+
+
+# ------------------------------------------------------------ BASELINE configs
+@pytest.mark.parametrize("mode,rate", [("dist", 1.0), ("fixed", 1.0), ("dist", 0.5), ("fixed", 0.5)])
+def test_config1(mode, rate):
+    assert_parity(build_config(1, mode=mode, rate=rate))
+
+
+def test_config2_full():
+    assert_parity(build_config(2))
+
+
+def test_config3_reduced_all_chains():
+    assert_parity(build_config(3, n=5000))
+
+
+def test_config4_reduced_all_chains():
+    assert_parity(build_config(4, n=5000))
+
+
+def test_config4_full_size_all_chains():
+    """The bench workload at full size (64 chains x 100k requests), every chain."""
+    assert_parity(build_config(4), per_request=False)
+
+
+def test_config5_full_size_sampled_chains():
+    """1M-request LongBench traces: every chain simulated on the GPU, sampled
+    chains (lowest/highest rate, gamma 1 and 8) checked against the oracle."""
+    g = build_config(5)
+    st, *_ = run_gpu(g, per_request=False)
+    assert np.all(st["status"] == 0)
+    for ci in (0, 7, 39 * 8 + 0, 319):
+        want, _, _ = O.simulate_chain(g.traces[g.chains[ci].trace_idx], g.chains[ci], False)
+        for f in INT_FIELDS:
+            assert int(st[ci][f]) == int(want[f]), (ci, f)
+
+
+# ------------------------------------------------------------ determinism
+def test_determinism_and_chain_order_invariance():
+    g = build_config(4, n=3000)
+    a, *_ = run_gpu(g, per_request=False)
+    b, *_ = run_gpu(g, per_request=False)
+    assert a.tobytes() == b.tobytes()
+    perm = np.random.default_rng(1).permutation(len(g.chains))
+    gp = dataclasses.replace(g, chains=[g.chains[i] for i in perm],
+                             cell_chain=np.array([np.nonzero(perm == c)[0][0] for c in g.cell_chain],
+                                                 np.int32))
+    c, *_ = run_gpu(gp, per_request=False)
+    assert c[np.argsort(perm)].tobytes() == a.tobytes()
+    # shard boundaries do not matter
+    dg = api.DeviceGrid(g)
+    full = torch.empty((len(g.chains), 80), dtype=torch.uint8, device="cuda")
+    for lo, hi in ((0, 5), (5, 6), (6, 40), (40, 64)):
+        api.eval_grid(dg, lo, hi, stats=full[lo:hi])
+    torch.cuda.synchronize()
+    assert api.stats_numpy(full).tobytes() == a.tobytes()
+
+
+# ------------------------------------------------------------------- Alg. 1
+def test_argmin_random_stats_vs_oracle():
+    """GPU Alg. 1 on synthetic stats (ties, absents, capacity, both priorities)."""
+    rng = np.random.default_rng(11)
+    base = build_config(2, n=200)
+    for it in range(30):
+        k = 24
+        st = np.zeros(k, N.STATS_DTYPE)
+        st["n"] = rng.integers(5, 20, k)
+        st["slo_ok"] = np.minimum(st["n"], rng.integers(0, 21, k))
+        st["busy_new_us"] = rng.choice([10**6, 2 * 10**6, 3 * 10**6], k)
+        st["busy_old_us"] = rng.choice([0, 10**6], k)
+        st["e_new_uj"] = rng.choice([0, 10**9, 2 * 10**9], k)
+        st["e_old_uj"] = rng.choice([0, 10**9], k)
+        chains = [dataclasses.replace(base.chains[0], capacity_ok=int(rng.random() > 0.2),
+                                      ce_new_g=float(rng.choice([26340.0, 20000.0])))
+                  for _ in range(k)]
+        rows, cols = 37, 40
+        cells = rng.integers(-1, k, rows * cols).astype(np.int32)
+        scen = np.array([[rng.choice([0.0, 17.0, 261.0]), 7 * 3.15e7, rng.choice([5, 10]) * 3.15e7]
+                         for _ in range(3)])
+        rs = rng.integers(0, 3, rows).astype(np.int32)
+        prio = int(it % 3 == 2)
+        g = GridSpec("argmin", base.traces, chains, scen, rs, cells, rows, cols, 9, 10, prio,
+                     int(rng.integers(-1, cols)))
+        dg = api.DeviceGrid(g)
+        stats = torch.from_numpy(st.view(np.uint8).reshape(k, 80).copy()).cuda()
+        carbon, choice, fb = api.argmin_feasible(dg, stats)
+        torch.cuda.synchronize()
+        total = np.zeros((rows, cols))
+        ok = np.zeros((rows, cols), np.int64)
+        n = np.ones((rows, cols), np.int64)
+        present = cells.reshape(rows, cols) >= 0
+        cap = np.zeros((rows, cols), np.uint8)
+        for r in range(rows):
+            for c in range(cols):
+                kk = cells[r * cols + c]
+                if kk < 0:
+                    continue
+                d = {f: int(st[kk][f]) for f in INT_FIELDS}
+                sc = scen[rs[r]]
+                total[r, c] = O.carbon(d, chains[kk].ce_new_g, chains[kk].ce_old_g, *sc)[2]
+                ok[r, c], n[r, c], cap[r, c] = d["slo_ok"], d["n"], chains[kk].capacity_ok
+        want_c, want_f = O.alg1(total, ok, n, present, cap, 9, 10, prio, g.default_col)
+        assert np.array_equal(choice.cpu().numpy(), want_c), it
+        assert np.array_equal(fb.cpu().numpy(), want_f), it
+        got = carbon.cpu().numpy()
+        assert np.array_equal(got[present], total[present])
+        assert np.all(np.isnan(got[~present]))
+
+
+# --------------------------------------------------------- end-to-end host path
+def test_evaluate_host_matches_device_path():
+    g = build_config(4, n=4000)
+    dg = api.DeviceGrid(g)
+    stats, _ = api.eval_grid(dg)
+    carbon, choice, fb = api.argmin_feasible(dg, stats)
+    torch.cuda.synchronize()
+    res = api.evaluate_host(dg, dg.pinned_traces(), want_carbon=True)
+    assert res.stats.tobytes() == api.stats_numpy(stats).tobytes()
+    assert np.array_equal(res.choice, choice.cpu().numpy())
+    assert np.array_equal(res.via_fallback, fb.cpu().numpy())
+    assert np.array_equal(res.carbon, carbon.cpu().numpy())
+    assert res.launches == 3 and res.h2d_bytes > 0
+
+
+def test_abi_errors():
+    g = build_config(1)
+    dg = api.DeviceGrid(g)
+    ch = dg.gl_chains[0]
+    bad = N.GlChain.from_buffer_copy(ch)
+    bad.batch_cap = 0
+    stats = torch.empty((1, 80), dtype=torch.uint8, device="cuda")
+    with pytest.raises(N.GreenLLMError) as e:
+        N.eval_grid(dg.gl_traces, [bad], stats.data_ptr(), None, 0)
+    assert e.value.status == N.GL_E_INVALID
+    bad = N.GlChain.from_buffer_copy(ch)
+    bad.trace_idx = 5
+    with pytest.raises(N.GreenLLMError) as e:
+        N.eval_grid(dg.gl_traces, [bad], stats.data_ptr(), None, 0)
+    assert e.value.status == N.GL_E_LOOKUP
+    bad = N.GlChain.from_buffer_copy(ch)
+    bad.mode, bad.gamma, bad.alpha = 1, 4, 1.5
+    with pytest.raises(N.GreenLLMError) as e:
+        N.eval_grid(dg.gl_traces, [bad], stats.data_ptr(), None, 0)
+    assert e.value.status == N.GL_E_DOMAIN
+    with pytest.raises(N.GreenLLMError) as e:
+        N.argmin_feasible(stats.data_ptr(), [ch], np.array([[-1.0, 1.0, 1.0]]), 1, 1,
+                          np.zeros(1), np.zeros(1), 9, 10, 0, -1, None,
+                          stats.data_ptr(), stats.data_ptr(), 0)
+    assert e.value.status == N.GL_E_DOMAIN
