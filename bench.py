@@ -1,0 +1,412 @@
+"""Benchmark: the full config-4 grid (BASELINE.json configs[3]) per step.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = the whole hot path over the grid: gl_eval_grid on this rank's
+shard of timing chains (k_dsd_demand + k_chain), one NCCL all_gather of the
+80-byte chain statistics (N > 1), gl_argmin_feasible (k_argmin) over all
+8,192 rows x 8 columns.  Inputs are resident in HBM; L2 is flushed (512 MiB
+write) between timed steps, outside the timed events.  Rank 0 prints one JSON
+line.  ``--impl reference`` times the CPU oracle (oracle/) on a bounded
+sample of the same workload instead (the reference arm of this tier).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "config×request evals/sec at 1/2/4/8 B200; % HBM roofline; speedup vs CPU oracle"
+UNIT = "config×request evals/s"
+WORKLOAD = ("cfg4: full grid, Llama-7B DPD + DSD(1B draft, gamma 4, alpha 0.8) x 4 GPU pairs "
+            "x 8 rates (0.5-8 req/s) x 64 CI x 16 lifetimes, 100k chat requests per trace")
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--n", type=int, default=100_000, help="requests per trace")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-budget-s", type=float, default=15.0)
+    return ap.parse_args()
+
+
+def dist_env():
+    rank = int(os.environ.get("RANK", 0))
+    world = int(os.environ.get("WORLD_SIZE", 1))
+    local = int(os.environ.get("LOCAL_RANK", 0))
+    return rank, world, local
+
+
+def algorithmic_bytes(grid, lo, hi):
+    """16 B per (chain, request) (a i64 + p u32 + o u32) read by
+    k_chain, +4 B for the DSD demand K_j it also reads; tables amortise to ~0."""
+    tot = 0
+    for ch in grid.chains[lo:hi]:
+        n = grid.traces[ch.trace_idx].n
+        tot += n * (20 if ch.mode == 1 else 16)
+    return tot
+
+
+def shard_bounds(n_chains, world):
+    from paper_2412_20322_b200.dist import shard_bounds as sb
+    return sb(n_chains, world)
+
+
+# --------------------------------------------------------------- clocks sampler
+class ClockSampler:
+    FIELDS = ("clocks.sm,clocks.max.sm,power.draw,utilization.gpu,"
+              "clocks_event_reasons.sw_power_cap,clocks_event_reasons.hw_slowdown,"
+              "clocks_event_reasons.hw_thermal_slowdown,clocks_event_reasons.sw_thermal_slowdown")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.FIELDS}",
+                 "--format=csv,noheader,nounits", "-lms", "50"],
+                stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.th = threading.Thread(target=self._read, daemon=True)
+            self.th.start()
+        except OSError:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append((time.time(), line.strip()))
+
+    def stop(self):
+        if self.proc is not None:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self, t0, t1):
+        rows = []
+        for ts, line in self.lines:
+            parts = [p.strip() for p in line.split(",")]
+            if len(parts) < 8:
+                continue
+            try:
+                sm, smax = float(parts[0]), float(parts[1])
+            except ValueError:
+                continue
+            rows.append((ts, sm, smax, parts[3], parts[4:8]))
+        inside = [r for r in rows if t0 <= r[0] <= t1] or rows
+        if not inside:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        names = ["sw_power_cap", "hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown"]
+        reasons = sorted({names[i] for r in inside for i, v in enumerate(r[4]) if v == "Active"})
+        return {"sm_mhz": statistics.median(r[1] for r in inside),
+                "sm_max_mhz": max(r[2] for r in inside), "reasons": reasons,
+                "samples": len(inside)}
+
+
+# ------------------------------------------------------------------ CPU oracle
+def cpu_baseline(grid, budget_s, chain_order=None):
+    """Time the oracle as it stands (single thread) on a bounded sample of the
+    workload: whole chains (simulation + carbon + Alg. 1 over their cells)."""
+    from oracle import oracle as O
+    O.lib()
+    order = chain_order if chain_order is not None else list(range(len(grid.chains)))
+    # size the sample to the budget from one probe chain of each mode
+    t0 = time.perf_counter()
+    for ci in order[:2]:
+        O.simulate_chain(grid.traces[grid.chains[ci].trace_idx], grid.chains[ci], False)
+    per_chain = (time.perf_counter() - t0) / 2
+    k = int(max(2, min(len(order), budget_s / max(per_chain, 1e-6))))
+    step = max(1, len(order) // k)
+    done = order[::step][:k]
+    sub = _subset(grid, done)
+    t1 = time.perf_counter()
+    O.evaluate_grid(sub)  # simulation + carbon + Alg. 1 over the sample's cells
+    t_all = time.perf_counter() - t1
+    cells = int(np.isin(grid.cell_chain, done).sum())
+    reqs = grid.traces[0].n
+    evals = cells * reqs
+    return dict(value=evals / t_all, cells=cells, chains=len(done), seconds=t_all,
+                chain_request_sims_per_s=len(done) * reqs / t_all)
+
+
+def _subset(grid, chain_ids):
+    from paper_2412_20322_b200.inputs import subset_chains
+    return subset_chains(grid, chain_ids)
+
+
+def run_reference(args):
+    rank, world, _ = dist_env()
+    if rank != 0:
+        return 0
+    from oracle import oracle as O
+    from paper_2412_20322_b200.inputs import build_config
+    O.lib()
+    grid = build_config(4, n=args.n)
+    per_step_chains = 2
+    times, evals = [], []
+    for step in range(args.warmup + args.steps):
+        ids = [(step * per_step_chains + k) % len(grid.chains) for k in range(per_step_chains)]
+        t0 = time.perf_counter()
+        sub = _subset(grid, ids)
+        ref = O.evaluate_grid(sub)
+        dt = time.perf_counter() - t0
+        if step >= args.warmup:
+            times.append(dt)
+            evals.append(int(ref["present"].sum()) * grid.traces[0].n)
+    value = sum(evals) / sum(times)
+    out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
+           "steps": args.steps, "warmup": args.warmup,
+           "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
+           "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+           "config": {"workload": WORKLOAD, "sample": f"{per_step_chains} timing chains "
+                      "(each 100k requests, all 1,024 of its grid cells) per step, rotating"},
+           "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
+                            "sample": f"{per_step_chains} of 64 chains per step"},
+           "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(out))
+    return 0
+
+
+# --------------------------------------------------------------------- ours
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_20322_b200 import api
+    from paper_2412_20322_b200 import native as N
+    from paper_2412_20322_b200.dist import all_gather_stats
+    from paper_2412_20322_b200.inputs import build_config
+
+    rank, world, local = dist_env()
+    if world > 1:
+        torch.cuda.set_device(local)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+    else:
+        torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    grid = build_config(4, n=args.n)
+    dg = api.DeviceGrid(grid, dev)
+    bounds = shard_bounds(dg.n_chains, world)
+    lo, hi = bounds[rank]
+    max_shard = max(h - l for l, h in bounds)
+    local_stats = torch.zeros((max_shard, 80), dtype=torch.uint8, device=dev)
+    gathered = torch.empty((world * max_shard, 80), dtype=torch.uint8, device=dev)
+    flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+    stream = torch.cuda.current_stream()
+
+    def step():
+        launches = 0
+        if hi > lo:
+            api.eval_grid(dg, lo, hi, stats=local_stats[: hi - lo])
+            launches += dg.last_launches
+        if world > 1:
+            full = all_gather_stats(local_stats, gathered, bounds, dg.n_chains)
+        else:
+            full = local_stats
+        api.argmin_feasible(dg, full, want_carbon=True)
+        launches += dg.last_launches
+        return launches
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    st = api.stats_numpy(local_stats[: hi - lo]) if hi > lo else None
+    if st is not None:
+        api.check_status(st)
+
+    sampler = ClockSampler(local)
+    sampler.start()
+    time.sleep(0.3)
+    N.profile_enable(True)
+    N.kernel_times()
+    evs = [(torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True))
+           for _ in range(args.steps)]
+    launches = 0
+    kt = {}
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_wall0 = time.time()
+    for i in range(args.steps):
+        flush.fill_(i & 0xFF)
+        evs[i][0].record(stream)
+        launches += step()
+        evs[i][1].record(stream)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    t_wall1 = time.time()
+    for name, ms in N.kernel_times():
+        kt.setdefault(name, []).append(ms)
+    N.profile_enable(False)
+    sampler.stop()
+    step_ms = [a.elapsed_time(b) for a, b in evs]
+    total_ms = torch.tensor([sum(step_ms)], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(total_ms, op=dist.ReduceOp.MAX)
+    ms_per_step = float(total_ms.item()) / args.steps
+
+    # end to end: pinned host traces -> gl_evaluate_host (H2D, kernels, D2H)
+    e2e = None
+    if world == 1:
+        host = dg.pinned_traces()
+        res = api.evaluate_host(dg, host)
+        for _ in range(2):
+            api.evaluate_host(dg, host, out=res)
+        e_ms = []
+        for i in range(max(3, args.steps // 2)):
+            flush.fill_(i & 0xFF)
+            torch.cuda.synchronize()
+            e0 = torch.cuda.Event(enable_timing=True)
+            e1 = torch.cuda.Event(enable_timing=True)
+            e0.record(stream)
+            api.evaluate_host(dg, host, out=res)
+            e1.record(stream)
+            torch.cuda.synchronize()
+            e_ms.append(e0.elapsed_time(e1))
+        e2e_ms = sum(e_ms) / len(e_ms)
+        e2e = {"value": grid.grid_points * grid.traces[0].n / (e2e_ms / 1e3), "unit": UNIT,
+               "ms_per_step": e2e_ms, "h2d_bytes_per_step": res.h2d_bytes,
+               "d2h_bytes_per_step": res.d2h_bytes,
+               "path": "gl_evaluate_host (pinned host traces, cudaMemcpyAsync in, results out)"}
+    else:
+        e2e = e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush, dev)
+
+    if rank != 0:
+        if world > 1:
+            dist.destroy_process_group()
+        return 0
+
+    reqs = grid.traces[0].n
+    evals = grid.grid_points * reqs
+    value = evals / (ms_per_step / 1e3)
+    chain_req = dg.chain_n.sum() / (ms_per_step / 1e3)
+    kchain = kt.get("k_chain", [])
+    kchain_ms = sum(kchain) / max(1, len(kchain))
+    peaks = {}
+    try:
+        peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
+    except OSError:
+        pass
+    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    alg_bytes = algorithmic_bytes(grid, lo, hi)
+    achieved = alg_bytes / (kchain_ms / 1e3) / 1e9 if kchain_ms > 0 else 0.0
+    traffic = None
+    prof_path = os.path.join(ROOT, "profiles", "k_chain_dram_bytes.json")
+    if os.path.exists(prof_path):
+        try:
+            traffic = json.load(open(prof_path)).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+    step_total = {k: sum(v) / max(1, len(v)) for k, v in kt.items()}
+    cpu = None
+    if not args.no_cpu_baseline:
+        cb = cpu_baseline(grid, args.cpu_budget_s)
+        cpu = {"value": cb["value"], "unit": UNIT, "cores": 1, "kind": "oracle",
+               "sample": f"{cb['chains']} of {len(grid.chains)} timing chains x {reqs} requests "
+                         f"(all {cb['cells']} of their grid cells), single-threaded, "
+                         f"{cb['seconds']:.1f} s",
+               "chain_request_sims_per_s": cb["chain_request_sims_per_s"]}
+    clocks = sampler.summary(t_wall0, t_wall1)
+    out = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+        "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+        "config": {"workload": WORKLOAD, "grid_points": grid.grid_points,
+                   "timing_chains": len(grid.chains), "requests_per_trace": reqs,
+                   "l2": "flushed between timed steps (512 MiB device write, outside the events)",
+                   "parallelism": f"chains sharded over {world} GPU(s), one NCCL all_gather of "
+                                  "80-B chain stats" if world > 1 else "1 GPU",
+                   "grid_point_factorisation": "each timing chain is simulated once and scores "
+                                               "its 1,024 CI x lifetime cells (SURVEY F2)"},
+        "chain_request_sims_per_s": chain_req,
+        "kernel_ms_per_step": step_total,
+        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic,
+                     "kernel": "k_chain", "algorithmic_bytes_per_launch": alg_bytes,
+                     "kernel_ms": kchain_ms,
+                     "note": "k_chain is bound by the dependent latency of each chain's serial "
+                             "decode event loop, not by HBM (DESIGN.md §5)"},
+        "cpu_baseline": cpu,
+        "e2e": e2e,
+        "gpu_launches": launches,
+        "clocks": clocks,
+    }
+    print(json.dumps(out))
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush, dev):
+    """N > 1: each rank copies its shard's traces from pinned host memory, runs
+    its chains, all_gathers stats, runs Alg. 1 and reads the choices back."""
+    import torch
+    import torch.distributed as dist
+
+    from paper_2412_20322_b200 import api
+    from paper_2412_20322_b200.dist import all_gather_stats
+    host = dg.pinned_traces()
+    needed = sorted({grid.chains[c].trace_idx for c in range(lo, hi)})
+    dev_tr = {t: tuple(torch.empty_like(x, device=dev) for x in host[t]) for t in needed}
+    stream = torch.cuda.current_stream()
+    times = []
+    h2d = sum(x.numel() * x.element_size() for t in needed for x in host[t])
+    d2h = 0
+    for i in range(args.warmup + max(3, args.steps // 2)):
+        flush.fill_(i & 0xFF)
+        dist.barrier()
+        torch.cuda.synchronize()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        for t in needed:
+            for d, h in zip(dev_tr[t], host[t]):
+                d.copy_(h, non_blocking=True)
+        if hi > lo:
+            api.eval_grid(dg, lo, hi, stats=local_stats[: hi - lo])
+        full = all_gather_stats(local_stats, gathered, bounds, dg.n_chains)
+        _, choice, fb = api.argmin_feasible(dg, full, want_carbon=False)
+        c_h, f_h = choice.cpu(), fb.cpu()
+        e1.record(stream)
+        torch.cuda.synchronize()
+        d2h = c_h.numel() * 4 + f_h.numel()
+        if i >= args.warmup:
+            times.append(e0.elapsed_time(e1))
+    t = torch.tensor([sum(times) / len(times)], dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    ms = float(t.item())
+    return {"value": grid.grid_points * grid.traces[0].n / (ms / 1e3), "unit": UNIT,
+            "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "path": "per rank: pinned H2D of its shard's traces, gl_eval_grid, NCCL all_gather, "
+                    "gl_argmin_feasible, D2H of choices"}
+
+
+def main():
+    args = parse()
+    if args.warmup < 3:
+        args.warmup = 3
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -204,6 +204,15 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces,
 
 /* Number of CUDA kernels the last successful call on this thread enqueued. */
 int32_t gl_last_launch_count(void);
+
+/* Benchmark instrumentation (per calling thread).  When enabled (on != 0),
+ * gl_eval_grid and gl_argmin_feasible record CUDA events on `stream` around
+ * every kernel they enqueue.  After the stream is synchronised,
+ * gl_kernel_times writes up to `max` (name, milliseconds) pairs of the
+ * kernels enqueued since the previous gl_kernel_times call and returns how
+ * many it wrote (names are static strings).  Disabled by default. */
+gl_status gl_profile_enable(int32_t on);
+int32_t gl_kernel_times(const char **names_out, float *ms_out, int32_t max);
 const char *gl_strerror(gl_status status);
 int32_t gl_version(void);
 

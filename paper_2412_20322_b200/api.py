@@ -35,7 +35,7 @@ class DeviceGrid:
         self.grid = grid
         self.device = torch.device(device)
         self._keep = []
-        arr_cache = {}
+        arr_cache = self._dev_cache = {}  # device tensors must outlive every ABI call
 
         def up(x):
             k = id(x)

@@ -717,6 +717,36 @@ __global__ void __launch_bounds__(256)
 // ================================================================ host side
 thread_local int32_t g_last_launches = 0;
 
+// benchmark instrumentation: CUDA events around each kernel (gl_profile_enable)
+constexpr int PROF_MAX = 256;
+struct ProfState {
+    bool on = false;
+    int used = 0;
+    std::vector<cudaEvent_t> ev;
+    const char *names[PROF_MAX];
+};
+thread_local ProfState g_prof;
+
+void prof_begin(const char *name, cudaStream_t s)
+{
+    if (!g_prof.on || g_prof.used >= PROF_MAX) return;
+    while ((int)g_prof.ev.size() < 2 * (g_prof.used + 1)) {
+        cudaEvent_t e;
+        if (cudaEventCreate(&e) != cudaSuccess) return;
+        g_prof.ev.push_back(e);
+    }
+    g_prof.names[g_prof.used] = name;
+    cudaEventRecord(g_prof.ev[2 * g_prof.used], s);
+}
+
+void prof_end(cudaStream_t s)
+{
+    if (!g_prof.on || g_prof.used >= PROF_MAX || (int)g_prof.ev.size() < 2 * (g_prof.used + 1))
+        return;
+    cudaEventRecord(g_prof.ev[2 * g_prof.used + 1], s);
+    ++g_prof.used;
+}
+
 gl_status device_check()
 {
     static int cached = -1;  // 1 = ok, 0 = unsupported
@@ -890,8 +920,10 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
         int64_t maxn = 0;
         for (auto &g : groups) maxn = std::max(maxn, g.n);
         dim3 grid((unsigned)((maxn + 255) / 256), (unsigned)groups.size());
+        prof_begin("k_dsd_demand", stream);
         k_dsd_demand<<<grid, 256, 0, stream>>>(reinterpret_cast<const DGroup *>(scratch + off_groups));
         e = cudaGetLastError();
+        prof_end(stream);
         ++launches;
     }
     if (e == cudaSuccess) {
@@ -900,8 +932,11 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
             if (r != cudaSuccess) return r;
+            prof_begin("k_chain", stream);
             kern<<<n_chains, 32, smem, stream>>>(dc, stats_out, per_request_out);
-            return cudaGetLastError();
+            r = cudaGetLastError();
+            prof_end(stream);
+            return r;
         };
         if (max_cap <= 32)
             e = launch(k_chain<1>);
@@ -978,6 +1013,7 @@ gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains, cons
     if (e == cudaSuccess) {
         const int warps = 8;
         const unsigned blocks = (unsigned)((rows + warps - 1) / warps);
+        prof_begin("k_argmin", stream);
         k_argmin<<<blocks, 32 * warps, 0, stream>>>(
             stats, reinterpret_cast<const DCarbon *>(scratch),
             reinterpret_cast<const gl_scenario *>(scratch + o_scen),
@@ -985,6 +1021,7 @@ gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains, cons
             reinterpret_cast<const int32_t *>(scratch + o_cells), (int32_t)rows, (int32_t)cols,
             slo_num, slo_den, priority, default_col, carbon_out, choice_out, via_fallback_out);
         e = cudaGetLastError();
+        prof_end(stream);
     }
     cudaError_t ef = cudaFreeAsync(scratch, stream);
     if (e == cudaSuccess) e = ef;
@@ -1082,6 +1119,28 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
 }
 
 int32_t gl_last_launch_count(void) { return g_last_launches; }
+
+gl_status gl_profile_enable(int32_t on)
+{
+    g_prof.on = on != 0;
+    g_prof.used = 0;
+    return GL_OK;
+}
+
+int32_t gl_kernel_times(const char **names_out, float *ms_out, int32_t max)
+{
+    int32_t k = 0;
+    for (int i = 0; i < g_prof.used && k < max; ++i) {
+        float ms = 0.f;
+        if (cudaEventElapsedTime(&ms, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]) != cudaSuccess)
+            ms = -1.f;
+        if (names_out) names_out[k] = g_prof.names[i];
+        if (ms_out) ms_out[k] = ms;
+        ++k;
+    }
+    g_prof.used = 0;
+    return k;
+}
 
 const char *gl_strerror(gl_status s)
 {

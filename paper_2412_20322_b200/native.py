@@ -57,7 +57,7 @@ assert STATS_DTYPE.itemsize == 80
 SCEN_DTYPE = np.dtype([("ci", "<f8"), ("lt_new", "<f8"), ("lt_old", "<f8")])
 
 EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_last_launch_count",
-           "gl_strerror", "gl_version")
+           "gl_profile_enable", "gl_kernel_times", "gl_strerror", "gl_version")
 
 _lib = None
 
@@ -88,6 +88,10 @@ def lib():
                                        i32, i32, vp, vp, vp, vp, vp]
         L.gl_last_launch_count.restype = i32
         L.gl_last_launch_count.argtypes = []
+        L.gl_profile_enable.restype = i32
+        L.gl_profile_enable.argtypes = [i32]
+        L.gl_kernel_times.restype = i32
+        L.gl_kernel_times.argtypes = [C.POINTER(C.c_char_p), C.POINTER(C.c_float), i32]
         L.gl_strerror.restype = C.c_char_p
         L.gl_strerror.argtypes = [i32]
         L.gl_version.restype = i32
@@ -142,3 +146,15 @@ def evaluate_host(host_traces, chains, scen, rows, cols, row_scenario, cell_chai
                                  choice_out.ctypes.data, fb_out.ctypes.data, stream or None),
           "gl_evaluate_host")
     return lib().gl_last_launch_count()
+
+
+def profile_enable(on: bool):
+    check(lib().gl_profile_enable(1 if on else 0), "gl_profile_enable")
+
+
+def kernel_times(max_n: int = 256):
+    """[(kernel name, ms)] recorded since the last read (stream must be synchronised)."""
+    names = (C.c_char_p * max_n)()
+    ms = (C.c_float * max_n)()
+    k = lib().gl_kernel_times(names, ms, max_n)
+    return [(names[i].decode(), float(ms[i])) for i in range(k)]
