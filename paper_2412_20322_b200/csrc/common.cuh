@@ -1,0 +1,140 @@
+// common.cuh -- device descriptors and warp / PTX helpers shared by the kernels
+// of libgreenllm.so (sm_100a).  Part of the CUDA path only.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+
+#include "greenllm.h"
+
+namespace gl {
+
+constexpr int RING = 256;       // decode-request ring per chain (shared memory)
+constexpr int RING_MASK = RING - 1;
+constexpr int CHUNK = 128;      // requests per produce step: 4 per lane, 128-bit loads
+constexpr int LOOKAHEAD = 64;   // decode candidates kept staged ahead of the ring head
+constexpr uint32_t ACCEPT_STREAM = 0x41434350u;  // "ACCP": third Philox counter word (R22)
+constexpr int64_t NEG_INF = INT64_MIN / 4;
+constexpr uint32_t F_EMPTY = 0xFFFFFFFFu;
+constexpr unsigned FULL = 0xFFFFFFFFu;
+constexpr uint32_t O_LIMIT = 1u << 30;
+
+// one timing chain as the kernels see it (built by the host from gl_chain + gl_trace)
+struct DChain {
+    const int64_t *a;
+    const uint32_t *p;
+    const uint32_t *o;
+    const uint32_t *K;  // DSD: speculative steps per request (k_dsd_demand); DPD: null
+    const int32_t *t1, *t2, *b2;
+    const int64_t *e1, *e2;
+    const int32_t *step, *sbn, *sbo;
+    const int64_t *sen, *seo;
+    int64_t n;
+    int64_t ttft_slo, tpot_slo;
+    int64_t out_off;  // first row of this chain in the per-request (ttft, finish) array
+    int32_t mode, cap, max_prompt, capacity_ok;
+};
+
+// one DSD demand group: requests sharing (output lengths, gamma, alpha, seed)
+struct DGroup {
+    const uint32_t *o;
+    uint32_t *K;
+    int64_t n;
+    uint64_t seed;
+    int32_t gamma, pad;
+    uint64_t thr[GL_MAX_GAMMA];
+};
+
+struct DCarbon {
+    double ce_new, ce_old;
+    int32_t cap_ok, pad;
+};
+
+// Philox4x32-10 (Salmon et al. 2011), the CUDA path's own implementation
+__device__ __forceinline__ uint4 philox4x32_10(uint4 c, uint32_t k0, uint32_t k1)
+{
+#pragma unroll
+    for (int r = 0; r < 10; ++r) {
+        if (r) {
+            k0 += 0x9E3779B9u;
+            k1 += 0xBB67AE85u;
+        }
+        const uint32_t hi0 = __umulhi(0xD2511F53u, c.x), lo0 = 0xD2511F53u * c.x;
+        const uint32_t hi1 = __umulhi(0xCD9E8D57u, c.z), lo1 = 0xCD9E8D57u * c.z;
+        c = make_uint4(hi1 ^ c.y ^ k0, lo1, hi0 ^ c.w ^ k1, lo0);
+    }
+    return c;
+}
+
+__device__ __forceinline__ uint64_t rotl64(uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
+// SplitMix64 finaliser; the per-request hash is mix(j ^ rotl(ttft,21) ^ rotl(finish,42))
+__device__ __forceinline__ uint64_t splitmix_fin(uint64_t z)
+{
+    z = (z ^ (z >> 30)) * 0xbf58476d1ce4e5b9ull;
+    z = (z ^ (z >> 27)) * 0x94d049bb133111ebull;
+    return z ^ (z >> 31);
+}
+
+__device__ __forceinline__ int64_t shfl_i64(int64_t v, int src) { return __shfl_sync(FULL, v, src); }
+__device__ __forceinline__ int64_t shfl_up_i64(int64_t v, int d) { return __shfl_up_sync(FULL, v, d); }
+
+__device__ __forceinline__ int64_t warp_sum_i64(int64_t v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v += __shfl_xor_sync(FULL, v, o);
+    return v;
+}
+
+__device__ __forceinline__ int64_t warp_max_i64(int64_t v)
+{
+#pragma unroll
+    for (int o = 16; o; o >>= 1) v = max(v, (int64_t)__shfl_xor_sync(FULL, v, o));
+    return v;
+}
+
+__device__ __forceinline__ uint32_t smem_u32(const void *p)
+{
+    return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t *bar, uint32_t count)
+{
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
+__device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t bytes)
+{
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+
+__device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
+{
+    uint32_t done = 0;
+    while (!done) {
+        asm volatile(
+            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
+            " selp.u32 %0, 1, 0, p;\n}\n"
+            : "=r"(done)
+            : "r"(smem_u32(bar)), "r"(phase)
+            : "memory");
+    }
+}
+
+// TMA bulk copy global -> shared; completion is signalled on the mbarrier's tx count
+__device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_t bytes, uint64_t *bar)
+{
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar))
+        : "memory");
+}
+
+__host__ __device__ __forceinline__ int round_up4(int x) { return (x + 3) & ~3; }
+
+}  // namespace gl
