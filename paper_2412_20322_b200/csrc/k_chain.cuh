@@ -29,7 +29,7 @@ namespace gl {
 
 struct SmemLayout {
     int p1pad, cappad;
-    size_t off_t1, off_t2, off_step, off_r, off_dj, off_bar, total;
+    size_t off_t1, off_t2, off_step, off_magic, off_r, off_dj, off_bar, total;
     __host__ __device__ SmemLayout(int max_prompt, int cap)
     {
         p1pad = round_up4(max_prompt + 1);
@@ -37,12 +37,23 @@ struct SmemLayout {
         off_t1 = 0;
         off_t2 = off_t1 + 4 * (size_t)p1pad;
         off_step = off_t2 + 4 * (size_t)p1pad;
-        off_r = (off_step + 4 * (size_t)cappad + 15) & ~(size_t)15;
+        off_magic = (off_step + 4 * (size_t)cappad + 15) & ~(size_t)15;
+        off_r = off_magic + 8 * (size_t)cappad;
         off_dj = off_r + 8 * RING;
         off_bar = off_dj + 8 * RING;
         total = off_bar + 16;
     }
 };
+
+// ceil(gap / st) for 0 < gap < 2^31, 1 <= st < 2^31 without a division:
+// Lemire, Kaser & Kurz (2019): with M = floor((2^64 - 1) / d) + 1, floor(x / d) =
+// mulhi64(M, x) for every 32-bit x.  (d = 1 is stored as M = 0 and handled apart.)
+__device__ __forceinline__ uint32_t ceil_div_magic(uint32_t gap, uint32_t st, uint64_t M)
+{
+    const uint32_t x = gap + st - 1u;
+    const uint64_t hi = (uint64_t)(uint32_t)(M >> 32) * x + __umulhi((uint32_t)M, x);
+    return st == 1u ? gap : (uint32_t)(hi >> 32);
+}
 
 // Stage a [count] int32 table into shared memory: the 16-B aligned bulk by TMA
 // (lane 0 issues), the ragged tail by plain loads.  Returns the TMA byte count.
@@ -86,19 +97,31 @@ __global__ void __launch_bounds__(32, 1)
     __syncwarp();
 
     uint32_t status = 0;
+    uint64_t *magic = reinterpret_cast<uint64_t *>(smem + L.off_magic);
     {
         bool bad = false;
         for (int i = 1 + lane; i <= P; i += 32) bad |= (t1s[i] < 0) | (t2s[i] < 0);
-        for (int b = 1 + lane; b <= cap; b += 32) bad |= steps[b] < 1;
+        for (int b = 1 + lane; b <= cap; b += 32) {
+            const int32_t s = steps[b];
+            bad |= s < 1;
+            magic[b] = s > 1 ? 0xFFFFFFFFFFFFFFFFull / (uint64_t)s + 1ull : 0ull;
+        }
         if (__any_sync(FULL, bad)) status |= GL_ST_TABLE;
+        __syncwarp();
     }
 
     // lane-local accumulators
     int64_t acc_busy_new = 0, acc_busy_old = 0, acc_e_new = 0, acc_e_old = 0, acc_tokens = 0;
     int64_t acc_mk = 0;
-    uint64_t iters[SPL + 1];  // iterations run at batch size b: lane b & 31, row b >> 5
+    // iterations run at batch size b, held by lane b & 31 in row b >> 5: 32-bit
+    // counters (flushed into 64-bit totals whenever the iteration counter rebases)
+    uint64_t iters[SPL + 1];
+    uint32_t cnt[SPL + 1];
 #pragma unroll
-    for (int s = 0; s <= SPL; ++s) iters[s] = 0;
+    for (int s = 0; s <= SPL; ++s) {
+        iters[s] = 0;
+        cnt[s] = 0;
+    }
 
     const int32_t n = (int32_t)ch.n;
     const bool dsd = ch.mode == GL_MODE_DSD;
@@ -286,107 +309,198 @@ __global__ void __launch_bounds__(32, 1)
         const int lo = s * 32;
         free_m[s] = cap >= lo + 32 ? FULL : (cap > lo ? ((1u << (cap - lo)) - 1u) : 0u);
     }
-    int64_t hr = 0;
-    uint32_t hd = 0, hj = 0;
-    auto load_head = [&]() {
-        if (nxt < produced) {  // broadcast shared-memory loads
-            const int e = nxt & RING_MASK;
-            hr = ring_r[e];
-            const uint2 dj = ring_dj[e];
-            hd = dj.x;
-            hj = dj.y;
-        }
+    // Ring head (hr, hd, hj) and the request after it (nr, nd, nj), prefetched so
+    // that a join never waits on shared memory.  hr = INT64_MAX: no head.
+    int64_t hr = INT64_MAX, nr = INT64_MAX;
+    uint32_t hd = 0, hj = 0, nd = 0, nj = 0;
+    auto load_pair = [&]() {  // broadcast shared-memory loads
+        hr = nxt < produced ? ring_r[nxt & RING_MASK] : INT64_MAX;
+        const uint2 dh = ring_dj[nxt & RING_MASK];
+        hd = dh.x;
+        hj = dh.y;
+        nr = nxt + 1 < produced ? ring_r[(nxt + 1) & RING_MASK] : INT64_MAX;
+        const uint2 dn = ring_dj[(nxt + 1) & RING_MASK];
+        nd = dn.x;
+        nj = dn.y;
     };
-    auto refill = [&]() {
+    auto advance_head = [&]() {
+        ++nxt;
+        hr = nr;
+        hd = nd;
+        hj = nj;
         if (chunk_next < n && produced - nxt < LOOKAHEAD) {
-            const bool was_empty = nxt >= produced;
             do produce();
             while (chunk_next < n && produced - nxt < LOOKAHEAD);
-            if (was_empty) load_head();
+            load_pair();
+        } else {
+            const int e = (nxt + 1) & RING_MASK;
+            nr = nxt + 1 < produced ? ring_r[e] : INT64_MAX;
+            const uint2 dn = ring_dj[e];
+            nd = dn.x;
+            nj = dn.y;
         }
     };
-    refill();
-    load_head();
-    for (;;) {
-        // FCFS joins at boundary T (r <= T) while the batch has room (R16, R18)
-        while (b < cap && nxt < produced && hr <= T) {
-            int s_sel = SPL;
-            unsigned bit = 0;
-#pragma unroll
-            for (int s = SPL - 1; s >= 0; --s)
-                if (free_m[s]) {
-                    s_sel = s;
-                    bit = free_m[s] & (0u - free_m[s]);
+    while (chunk_next < n && produced - nxt < LOOKAHEAD) produce();
+    load_pair();
+    const unsigned lane_bit = 1u << lane;
+    if constexpr (SPL == 1) {
+        // cap <= 32: one member per lane.  fmin (the smallest finish iteration)
+        // is kept warp-uniform: a join only lowers it (scalar min), so the REDUX
+        // runs only after leaves.
+        uint32_t Fm = F_EMPTY, jm = 0, fmin = F_EMPTY;
+        unsigned fr = free_m[0];
+        uint32_t c_lo = 0, c_hi = 0;  // iterations at b (lane b & 31; b = 32 -> c_hi of lane 0)
+        for (;;) {
+            while (b < cap && hr <= T) {  // FCFS joins at T (R16, R18)
+                if (I >= 0x80000000u) {   // rebase the 32-bit iteration counter
+                    if (Fm != F_EMPTY) Fm -= I;
+                    if (fmin != F_EMPTY) fmin -= I;
+                    iters[0] += c_lo;
+                    iters[1] += c_hi;
+                    c_lo = c_hi = 0;
+                    I = 0;
                 }
-            const bool me = (lane == __ffs(bit) - 1);
+                const unsigned bit = fr & (0u - fr);
+                fr ^= bit;
+                const uint32_t fnew = I + hd;
+                if (lane_bit == bit) {
+                    Fm = fnew;
+                    jm = hj;
+                }
+                fmin = min(fmin, fnew);
+                ++b;
+                advance_head();
+            }
+            if (b == 0) {  // idle until the next decode request is ready (R17)
+                if (hr == INT64_MAX) break;
+                T = hr;
+                continue;
+            }
+            const int64_t st = steps[b];
+            const uint32_t kL = fmin - I;
+            const int64_t gap = hr - T;  // > 0 whenever b < cap
+            uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, magic[b]);
+            if (gap >= 0x80000000ll) kJ = 0xFFFFFFFFu;
+            if (b < cap && kJ < kL) {
+                if (gap >= 0x80000000ll && hr != INT64_MAX)  // rare: very long gap
+                    kJ = (uint32_t)min((gap + st - 1) / st, (int64_t)kL);
+                if (kJ < kL) {  // join event: no member leaves before the head joins
+                    T += (int64_t)kJ * st;
+                    I += kJ;
+                    const uint32_t kk = (lane == (b & 31)) ? kJ : 0u;
+                    if (b < 32) c_lo += kk; else c_hi += kk;
+                    continue;
+                }
+            }
+            // leave event at iteration fmin (R16): finish = boundary time
+            T += (int64_t)kL * st;
+            I = fmin;
+            {
+                const uint32_t kk = (lane == (b & 31)) ? kL : 0u;
+                if (b < 32) c_lo += kk; else c_hi += kk;
+            }
+            const bool lv = Fm == I;
+            const unsigned lm = __ballot_sync(FULL, lv);
+            if (lv) {
+                out[2 * (int64_t)jm + 1] = T;
+                Fm = F_EMPTY;
+            }
+            fr |= lm;
+            b -= __popc(lm);
+            mk_dec = T;
+            fmin = __reduce_min_sync(FULL, Fm);
+        }
+        iters[0] += c_lo;
+        iters[1] += c_hi;
+    } else for (;;) {
+        // FCFS joins at boundary T (r <= T) while the batch has room (R16, R18)
+        while (b < cap && hr <= T) {
+            if (I >= 0x80000000u) {  // rebase the 32-bit iteration counter (F = I + d fits)
 #pragma unroll
-            for (int s = 0; s < SPL; ++s) {
-                if (s == s_sel) {
-                    free_m[s] &= ~bit;
-                    if (me) {
-                        F[s] = I + hd;
-                        jl[s] = hj;
+                for (int s = 0; s < SPL; ++s)
+                    if (F[s] != F_EMPTY) F[s] -= I;
+#pragma unroll
+                for (int s = 0; s <= SPL; ++s) {
+                    iters[s] += cnt[s];
+                    cnt[s] = 0;
+                }
+                I = 0;
+            }
+            if (SPL == 1) {  // lowest free lane takes the head
+                const unsigned bit = free_m[0] & (0u - free_m[0]);
+                free_m[0] ^= bit;
+                if (lane_bit == bit) {
+                    F[0] = I + hd;
+                    jl[0] = hj;
+                }
+            } else {
+                int s_sel = SPL;
+                unsigned bit = 0;
+#pragma unroll
+                for (int s = SPL - 1; s >= 0; --s)
+                    if (free_m[s]) {
+                        s_sel = s;
+                        bit = free_m[s] & (0u - free_m[s]);
+                    }
+#pragma unroll
+                for (int s = 0; s < SPL; ++s) {
+                    if (s == s_sel) {
+                        free_m[s] ^= bit;
+                        if (lane_bit == bit) {
+                            F[s] = I + hd;
+                            jl[s] = hj;
+                        }
                     }
                 }
             }
             ++b;
-            ++nxt;
-            refill();
-            load_head();
+            advance_head();
         }
         if (b == 0) {  // idle until the next decode request is ready (R17)
-            if (nxt >= produced) break;
+            if (hr == INT64_MAX) break;
             T = hr;
             continue;
         }
-        // next event: the first member leave, or the boundary at which the head joins
+        // Next event: the first member leave (kL iterations away, REDUX min) or the
+        // boundary at which the head joins (kJ = ceil(gap / step)); kJ does not
+        // depend on kL, so the reciprocal multiply overlaps the REDUX latency.
         const int64_t st = steps[b];
+        const int64_t gap = hr - T;  // > 0 whenever b < cap: the head was not admitted at T
+        uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, magic[b]);
+        if (b >= cap) kJ = 0xFFFFFFFFu;
+        if (gap >= 0x80000000ll && b < cap)  // rare: very long gaps, or no head (INT64_MAX)
+            kJ = hr == INT64_MAX ? 0xFFFFFFFFu
+                                 : (uint32_t)min((gap + st - 1) / st, (int64_t)0xFFFFFFFF);
         uint32_t fmin = F[0];
 #pragma unroll
         for (int s = 1; s < SPL; ++s) fmin = min(fmin, F[s]);
         fmin = __reduce_min_sync(FULL, fmin);
         const uint32_t kL = fmin - I;
-        uint32_t k = kL;
-        if (b < cap && nxt < produced) {
-            const int64_t gap = hr - T;  // > 0: the head was not admitted at T
-            if (gap <= (int64_t)(kL - 1) * st) {
-                if (gap < 0x80000000ll)
-                    k = ((uint32_t)gap + (uint32_t)st - 1u) / (uint32_t)st;
-                else
-                    k = (uint32_t)((gap + st - 1) / st);
-            }
-        }
+        const uint32_t k = min(kL, kJ);
         T += (int64_t)k * st;
         I += k;
         {
-            const bool mine = lane == (b & 31);
+            const uint32_t kk = (lane == (b & 31)) ? k : 0u;
             const int row = b >> 5;
 #pragma unroll
-            for (int s = 0; s <= SPL; ++s) iters[s] += (mine && s == row) ? (uint64_t)k : 0ull;
+            for (int s = 0; s <= SPL; ++s) cnt[s] += (s == row) ? kk : 0u;
         }
-        if (k == kL) {  // leaves at boundary T (R16): finish = T
-            int nl = 0;
+        // leaves at boundary T (R16): finish = T.  No branch: when k < kL no
+        // member has F == I.
+        int nl = 0;
 #pragma unroll
-            for (int s = 0; s < SPL; ++s) {
-                const bool lv = F[s] == I;
-                const unsigned lm = __ballot_sync(FULL, lv);
-                if (lv) {
-                    out[2 * (int64_t)jl[s] + 1] = T;
-                    F[s] = F_EMPTY;
-                }
-                free_m[s] |= lm;
-                nl += __popc(lm);
-            }
-            b -= nl;
-            mk_dec = T;
+        for (int s = 0; s < SPL; ++s) {
+            const bool lv = F[s] == I;
+            free_m[s] |= __ballot_sync(FULL, lv);
+            nl += (int)__reduce_add_sync(FULL, lv ? 1u : 0u);
+            if (lv) out[2 * (int64_t)jl[s] + 1] = T;
+            F[s] = lv ? F_EMPTY : F[s];
         }
-        if (I >= 0x80000000u) {  // rebase the 32-bit iteration counter
-#pragma unroll
-            for (int s = 0; s < SPL; ++s)
-                if (F[s] != F_EMPTY) F[s] -= I;
-            I = 0;
-        }
+        b -= nl;
+        mk_dec = nl ? T : mk_dec;
     }
+#pragma unroll
+    for (int s = 0; s <= SPL; ++s) iters[s] += cnt[s];
 
     // ---- S7: chain reductions (SLO counts and the hash: k_finalize) ------------
 #pragma unroll
