@@ -273,7 +273,7 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
             prof_end(stream);
             return r;
         };
-        if (max_cap <= 32)
+        if (max_cap <= 31)  // the one-row fast path needs b < 32
             e = launch(gl::k_chain<1>);
         else if (max_cap <= 64)
             e = launch(gl::k_chain<2>);

@@ -344,65 +344,79 @@ __global__ void __launch_bounds__(32, 1)
     load_pair();
     const unsigned lane_bit = 1u << lane;
     if constexpr (SPL == 1) {
-        // cap <= 32: one member per lane.  fmin (the smallest finish iteration)
-        // is kept warp-uniform: a join only lowers it (scalar min), so the REDUX
-        // runs only after leaves.
+        // cap <= 31: one member per lane, b < 32.  fmin (the smallest finish
+        // iteration) is kept warp-uniform: a join only lowers it (scalar min), so
+        // the REDUX runs only after leaves.  The ring head and the request after
+        // it are held in registers (h_*, n_*) so a join never waits on shared memory.
         uint32_t Fm = F_EMPTY, jm = 0, fmin = F_EMPTY;
         unsigned fr = free_m[0];
-        uint32_t c_lo = 0, c_hi = 0;  // iterations at b (lane b & 31; b = 32 -> c_hi of lane 0)
+        uint32_t c_b = 0;  // iterations run at batch size b == lane
+        int64_t *fin_col = out + 1;
+        int64_t h_r = hr, n_r = nr;
+        uint2 h_dj = make_uint2(hd, hj), n_dj = make_uint2(nd, nj);
         for (;;) {
-            while (b < cap && hr <= T) {  // FCFS joins at T (R16, R18)
-                if (I >= 0x80000000u) {   // rebase the 32-bit iteration counter
+            while (b < cap && h_r <= T) {  // FCFS joins at T (R16, R18)
+                if (I >= 0x80000000u) {    // rebase the 32-bit iteration counter
                     if (Fm != F_EMPTY) Fm -= I;
                     if (fmin != F_EMPTY) fmin -= I;
-                    iters[0] += c_lo;
-                    iters[1] += c_hi;
-                    c_lo = c_hi = 0;
+                    iters[0] += c_b;
+                    c_b = 0;
                     I = 0;
                 }
                 const unsigned bit = fr & (0u - fr);
                 fr ^= bit;
-                const uint32_t fnew = I + hd;
+                const uint32_t fnew = I + h_dj.x;
                 if (lane_bit == bit) {
                     Fm = fnew;
-                    jm = hj;
+                    jm = h_dj.y;
                 }
                 fmin = min(fmin, fnew);
                 ++b;
-                advance_head();
+                ++nxt;
+                h_r = n_r;
+                h_dj = n_dj;
+                if (chunk_next < n && produced - nxt < LOOKAHEAD) {
+                    do produce();
+                    while (chunk_next < n && produced - nxt < LOOKAHEAD);
+                    const int e = nxt & RING_MASK;
+                    h_r = nxt < produced ? ring_r[e] : INT64_MAX;
+                    h_dj = ring_dj[e];
+                }
+                const int e1 = (nxt + 1) & RING_MASK;
+                n_r = nxt + 1 < produced ? ring_r[e1] : INT64_MAX;
+                n_dj = ring_dj[e1];
             }
             if (b == 0) {  // idle until the next decode request is ready (R17)
-                if (hr == INT64_MAX) break;
-                T = hr;
+                if (h_r == INT64_MAX) break;
+                T = h_r;
                 continue;
             }
             const int64_t st = steps[b];
             const uint32_t kL = fmin - I;
-            const int64_t gap = hr - T;  // > 0 whenever b < cap
-            uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, magic[b]);
-            if (gap >= 0x80000000ll) kJ = 0xFFFFFFFFu;
-            if (b < cap && kJ < kL) {
-                if (gap >= 0x80000000ll && hr != INT64_MAX)  // rare: very long gap
-                    kJ = (uint32_t)min((gap + st - 1) / st, (int64_t)kL);
-                if (kJ < kL) {  // join event: no member leaves before the head joins
-                    T += (int64_t)kJ * st;
-                    I += kJ;
-                    const uint32_t kk = (lane == (b & 31)) ? kJ : 0u;
-                    if (b < 32) c_lo += kk; else c_hi += kk;
-                    continue;
+            if (b < cap) {  // the head may join before the next leave
+                const int64_t gap = h_r - T;  // > 0: the head was not admitted at T
+                uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, magic[b]);
+                const bool far = gap >= 0x80000000ll;  // rare: very long gap, or no head
+                if (kJ < kL || far) {
+                    if (far)  // exact 64-bit path; no head (INT64_MAX) never joins
+                        kJ = (h_r != INT64_MAX && gap <= (int64_t)(kL - 1) * st)
+                                 ? (uint32_t)((gap + st - 1) / st) : 0xFFFFFFFFu;
+                    if (kJ < kL) {  // join event: nobody leaves before the head joins
+                        T += (int64_t)kJ * st;
+                        I += kJ;
+                        c_b += (lane == b) ? kJ : 0u;
+                        continue;
+                    }
                 }
             }
             // leave event at iteration fmin (R16): finish = boundary time
             T += (int64_t)kL * st;
             I = fmin;
-            {
-                const uint32_t kk = (lane == (b & 31)) ? kL : 0u;
-                if (b < 32) c_lo += kk; else c_hi += kk;
-            }
+            c_b += (lane == b) ? kL : 0u;
             const bool lv = Fm == I;
             const unsigned lm = __ballot_sync(FULL, lv);
             if (lv) {
-                out[2 * (int64_t)jm + 1] = T;
+                fin_col[2 * (int64_t)jm] = T;
                 Fm = F_EMPTY;
             }
             fr |= lm;
@@ -410,8 +424,7 @@ __global__ void __launch_bounds__(32, 1)
             mk_dec = T;
             fmin = __reduce_min_sync(FULL, Fm);
         }
-        iters[0] += c_lo;
-        iters[1] += c_hi;
+        iters[0] += c_b;
     } else for (;;) {
         // FCFS joins at boundary T (r <= T) while the batch has room (R16, R18)
         while (b < cap && hr <= T) {
