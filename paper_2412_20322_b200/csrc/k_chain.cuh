@@ -106,6 +106,7 @@ __global__ void __launch_bounds__(32, 1)
             bad |= s < 1;
             magic[b] = s > 1 ? 0xFFFFFFFFFFFFFFFFull / (uint64_t)s + 1ull : 0ull;
         }
+        if (lane == 0) magic[0] = 0;
         if (__any_sync(FULL, bad)) status |= GL_ST_TABLE;
         __syncwarp();
     }
@@ -283,6 +284,8 @@ __global__ void __launch_bounds__(32, 1)
         }
         produced += total;
         chunk_next += CHUNK;
+        // after the last chunk, the two slots past the end read as "no request"
+        if (chunk_next >= n && lane < 2) ring_r[(produced + lane) & RING_MASK] = INT64_MAX;
         __syncwarp();
     };
 
@@ -348,15 +351,30 @@ __global__ void __launch_bounds__(32, 1)
         // iteration) is kept warp-uniform: a join only lowers it (scalar min), so
         // the REDUX runs only after leaves.  The ring head and the request after
         // it are held in registers (h_*, n_*) so a join never waits on shared memory.
-        uint32_t Fm = F_EMPTY, jm = 0, fmin = F_EMPTY;
+        uint32_t Fm = F_EMPTY, fmin = F_EMPTY;
         unsigned fr = free_m[0];
         uint32_t c_b = 0;  // iterations run at batch size b == lane
-        int64_t *fin_col = out + 1;
+        int64_t *const fin_col = out + 1;
+        int64_t *fa = fin_col;  // this lane's member's finish-time address
         int64_t h_r = hr, n_r = nr;
         uint2 h_dj = make_uint2(hd, hj), n_dj = make_uint2(nd, nj);
+        // step[b] and its reciprocal for b-1, b, b+1 in registers, shifted when b
+        // moves by one, so no shared-memory load sits on the event's critical path
+        int32_t st_d = 0, st_c = 0, st_u = 0;
+        uint64_t M_d = 0, M_c = 0, M_u = 0;
+        auto load_nbr = [&](int nb) {
+            st_c = steps[nb];
+            M_c = magic[nb];
+            st_u = steps[min(nb + 1, cap)];
+            M_u = magic[min(nb + 1, cap)];
+            st_d = steps[max(nb - 1, 0)];
+            M_d = magic[max(nb - 1, 0)];
+        };
+        load_nbr(0);
         for (;;) {
-            while (b < cap && h_r <= T) {  // FCFS joins at T (R16, R18)
-                if (I >= 0x80000000u) {    // rebase the 32-bit iteration counter
+            // ---- FCFS joins at boundary T (r <= T) while the batch has room (R16, R18)
+            while (b < cap && h_r <= T) {
+                if (I >= 0x80000000u) {  // rebase the 32-bit iteration counter
                     if (Fm != F_EMPTY) Fm -= I;
                     if (fmin != F_EMPTY) fmin -= I;
                     iters[0] += c_b;
@@ -368,10 +386,16 @@ __global__ void __launch_bounds__(32, 1)
                 const uint32_t fnew = I + h_dj.x;
                 if (lane_bit == bit) {
                     Fm = fnew;
-                    jm = h_dj.y;
+                    fa = fin_col + 2 * (int64_t)h_dj.y;
                 }
                 fmin = min(fmin, fnew);
                 ++b;
+                st_d = st_c;
+                M_d = M_c;
+                st_c = st_u;
+                M_c = M_u;
+                st_u = steps[min(b + 1, cap)];
+                M_u = magic[min(b + 1, cap)];
                 ++nxt;
                 h_r = n_r;
                 h_dj = n_dj;
@@ -379,11 +403,11 @@ __global__ void __launch_bounds__(32, 1)
                     do produce();
                     while (chunk_next < n && produced - nxt < LOOKAHEAD);
                     const int e = nxt & RING_MASK;
-                    h_r = nxt < produced ? ring_r[e] : INT64_MAX;
+                    h_r = ring_r[e];
                     h_dj = ring_dj[e];
                 }
                 const int e1 = (nxt + 1) & RING_MASK;
-                n_r = nxt + 1 < produced ? ring_r[e1] : INT64_MAX;
+                n_r = ring_r[e1];
                 n_dj = ring_dj[e1];
             }
             if (b == 0) {  // idle until the next decode request is ready (R17)
@@ -391,11 +415,147 @@ __global__ void __launch_bounds__(32, 1)
                 T = h_r;
                 continue;
             }
-            const int64_t st = steps[b];
+            if (b == cap) {
+                // Saturated fast path: with a full batch the next event is a leave;
+                // while exactly one member leaves and the head is already ready, the
+                // freed lane takes the head at the same boundary (R16).  Step time is
+                // the constant step[cap]; any other case exits to the general loop.
+                const int64_t stc = st_c;
+                uint32_t it = 0;
+                for (;;) {
+                    const uint32_t kL = fmin - I;
+                    I = fmin;
+                    T += (int64_t)kL * stc;
+                    it += kL;
+                    const bool lv = Fm == I;
+                    const unsigned lm = __ballot_sync(FULL, lv);
+                    if (lv) *fa = T;
+                    mk_dec = T;
+                    const bool one = (lm & (lm - 1u)) == 0u;
+                    if (!(one && h_r <= T && I < 0x80000000u)) {
+                        if (lv) Fm = F_EMPTY;
+                        fr |= lm;
+                        b -= __popc(lm);
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        break;
+                    }
+                    if (lv) {
+                        Fm = I + h_dj.x;
+                        fa = fin_col + 2 * (int64_t)h_dj.y;
+                    }
+                    fmin = __reduce_min_sync(FULL, Fm);
+                    ++nxt;
+                    h_r = n_r;
+                    h_dj = n_dj;
+                    if (chunk_next < n && produced - nxt < LOOKAHEAD) {
+                        do produce();
+                        while (chunk_next < n && produced - nxt < LOOKAHEAD);
+                        const int e = nxt & RING_MASK;
+                        h_r = ring_r[e];
+                        h_dj = ring_dj[e];
+                    }
+                    const int e1 = (nxt + 1) & RING_MASK;
+                    n_r = ring_r[e1];
+                    n_dj = ring_dj[e1];
+                }
+                c_b += (lane == cap) ? it : 0u;
+                if (b == cap - 1) {
+                    st_u = st_c;
+                    M_u = M_c;
+                    st_c = st_d;
+                    M_c = M_d;
+                    st_d = steps[max(b - 1, 0)];
+                    M_d = magic[max(b - 1, 0)];
+                } else {
+                    load_nbr(b);
+                }
+                continue;
+            }
+            {
+                // Light-load fast path (0 < b < cap, head not ready at T): each
+                // step is either the head's join at kJ = ceil(gap / step[b]) or the
+                // next leave at kL; it exits to the general loop when a join finds
+                // the batch full or another ready head, when the batch empties, or
+                // (to the general event code below) on a very long gap or a rebase.
+                bool slow = false;
+                for (;;) {
+                    const int64_t st = st_c;
+                    const uint32_t kL = fmin - I;
+                    const int64_t gap = h_r - T;
+                    const uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, M_c);
+                    if (gap >= 0x80000000ll || I >= 0x80000000u) {
+                        slow = true;
+                        break;
+                    }
+                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;
+                        I += kJ;
+                        c_b += (lane == b) ? kJ : 0u;
+                        const unsigned bit = fr & (0u - fr);
+                        fr ^= bit;
+                        const uint32_t fnew = I + h_dj.x;
+                        if (lane_bit == bit) {
+                            Fm = fnew;
+                            fa = fin_col + 2 * (int64_t)h_dj.y;
+                        }
+                        fmin = min(fmin, fnew);
+                        ++b;
+                        st_d = st_c;
+                        M_d = M_c;
+                        st_c = st_u;
+                        M_c = M_u;
+                        st_u = steps[min(b + 1, cap)];
+                        M_u = magic[min(b + 1, cap)];
+                        ++nxt;
+                        h_r = n_r;
+                        h_dj = n_dj;
+                        if (chunk_next < n && produced - nxt < LOOKAHEAD) {
+                            do produce();
+                            while (chunk_next < n && produced - nxt < LOOKAHEAD);
+                            const int e = nxt & RING_MASK;
+                            h_r = ring_r[e];
+                            h_dj = ring_dj[e];
+                        }
+                        const int e1 = (nxt + 1) & RING_MASK;
+                        n_r = ring_r[e1];
+                        n_dj = ring_dj[e1];
+                        if (b == cap || h_r <= T) break;
+                    } else {  // leave at iteration fmin (R16)
+                        T += (int64_t)kL * st;
+                        I = fmin;
+                        c_b += (lane == b) ? kL : 0u;
+                        const bool lv = Fm == I;
+                        const unsigned lm = __ballot_sync(FULL, lv);
+                        if (lv) {
+                            *fa = T;
+                            Fm = F_EMPTY;
+                        }
+                        fr |= lm;
+                        const int nl = __popc(lm);
+                        b -= nl;
+                        mk_dec = T;
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        if (nl == 1) {
+                            st_u = st_c;
+                            M_u = M_c;
+                            st_c = st_d;
+                            M_c = M_d;
+                            st_d = steps[max(b - 1, 0)];
+                            M_d = magic[max(b - 1, 0)];
+                        } else {
+                            load_nbr(b);
+                        }
+                        if (b == 0 || h_r <= T) break;
+                    }
+                }
+                if (!slow) continue;
+            }
+            // ---- next event: a join at kJ < kL, else the leave at kL (R16)
+            const int64_t st = st_c;
             const uint32_t kL = fmin - I;
             if (b < cap) {  // the head may join before the next leave
                 const int64_t gap = h_r - T;  // > 0: the head was not admitted at T
-                uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, magic[b]);
+                uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, M_c);
                 const bool far = gap >= 0x80000000ll;  // rare: very long gap, or no head
                 if (kJ < kL || far) {
                     if (far)  // exact 64-bit path; no head (INT64_MAX) never joins
@@ -409,20 +569,30 @@ __global__ void __launch_bounds__(32, 1)
                     }
                 }
             }
-            // leave event at iteration fmin (R16): finish = boundary time
             T += (int64_t)kL * st;
             I = fmin;
             c_b += (lane == b) ? kL : 0u;
             const bool lv = Fm == I;
             const unsigned lm = __ballot_sync(FULL, lv);
             if (lv) {
-                fin_col[2 * (int64_t)jm] = T;
+                *fa = T;
                 Fm = F_EMPTY;
             }
             fr |= lm;
-            b -= __popc(lm);
+            const int nl = __popc(lm);
+            b -= nl;
             mk_dec = T;
             fmin = __reduce_min_sync(FULL, Fm);
+            if (nl == 1) {
+                st_u = st_c;
+                M_u = M_c;
+                st_c = st_d;
+                M_c = M_d;
+                st_d = steps[max(b - 1, 0)];
+                M_d = magic[max(b - 1, 0)];
+            } else {  // several members left at once
+                load_nbr(b);
+            }
         }
         iters[0] += c_b;
     } else for (;;) {
