@@ -139,6 +139,22 @@ def test_edge_cases():
     assert_parity(grid_of(pairs))
 
 
+def test_iteration_rebase_and_far_gaps():
+    """> 2^31 decode iterations (the 32-bit iteration counter rebases) and joins
+    more than 2^31 us after the current boundary (the exact 64-bit path), in
+    both the single-row (cap <= 31) and the multi-row (cap 40) loops."""
+    pairs = []
+    for cap in (2, 40):
+        tab = make_tables(4, cap, lambda p: 3 * p, lambda p: p, [0] + [4] * cap,
+                          sbo=[0] + [4] * cap, seo=[0] + [1] * cap)
+        ch = make_chain(tab, MODE_DPD, cap, ttft_slo=100, tpot_slo=4)
+        a = [0, 3_000_000_000, 3_000_000_010, 6_000_000_000, 6_000_000_001, 9_500_000_000,
+             15_000_000_000, 16_000_000_000]
+        o = [1_000_000_000, 5, 7, 1_070_000_000, 600_000_000, 3, 300_000_000, 1000]
+        pairs.append((custom_trace(a, [1, 2, 3, 4, 1, 2, 3, 4], o), ch))
+    assert_parity(grid_of(pairs))
+
+
 def test_status_bits_match_oracle():
     pairs = [(custom_trace([5, 3, 7], [1, 1, 1], [2, 2, 2]), _edge_chain()),
              (custom_trace([0, 3], [0, 99], [2, 2]), _edge_chain()),
