@@ -20,6 +20,24 @@ constexpr uint32_t F_EMPTY = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr uint32_t O_LIMIT = 1u << 30;
 
+constexpr int SEG_LEN = 256;  // decode requests per speculation window (k_segments)
+
+// per-segment result of a helper warp's speculative run (k_decode)
+struct DSegOut {
+    int64_t maxfin;   // last finish time of the segment's isolated run
+    int64_t sums[4];  // decode busy_new, busy_old, e_new, e_old of that run
+    int32_t done;     // 1 once published (release)
+    int32_t pad;
+};
+
+// per-chain decode bookkeeping (stream-ordered scratch, zeroed by the host)
+struct DChainX {
+    int32_t M;           // decode requests (o > 1), set by k_stages
+    int32_t nseg;        // segments, set by k_segments
+    int32_t leader_pos;  // first segment the leader has not yet passed (helpers skip below)
+    int32_t next_seg;    // helper work counter
+};
+
 // one timing chain as the kernels see it (built by the host from gl_chain + gl_trace)
 struct DChain {
     const int64_t *a;
@@ -30,11 +48,29 @@ struct DChain {
     const int64_t *e1, *e2;
     const int32_t *step, *sbn, *sbo;
     const int64_t *sen, *seo;
+    // decode stream written by k_stages: ready time r and (demand, request index)
+    // per decode request q, in FCFS order, with two INT64_MAX sentinels after M
+    int64_t *dec_r;
+    uint2 *dec_dj;
+    int64_t *spec_fin;  // helpers' speculative finish times, indexed by q
+    int32_t *seg_start; // [nseg + 1] segment starts (q), seg_start[nseg] = M
+    DSegOut *seg_out;   // [nseg]
+    DChainX *x;
     int64_t n;
     int64_t ttft_slo, tpot_slo;
     int64_t out_off;  // first row of this chain in the per-request (ttft, finish) array
     int32_t mode, cap, max_prompt, capacity_ok;
 };
+
+// ceil(gap / st) for 0 < gap < 2^31, 1 <= st < 2^31 without a division:
+// Lemire, Kaser & Kurz (2019): with M = floor((2^64 - 1) / d) + 1, floor(x / d) =
+// mulhi64(M, x) for every 32-bit x.  (d = 1 is stored as M = 0 and handled apart.)
+__device__ __forceinline__ uint32_t ceil_div_magic(uint32_t gap, uint32_t st, uint64_t M)
+{
+    const uint32_t x = gap + st - 1u;
+    const uint64_t hi = (uint64_t)(uint32_t)(M >> 32) * x + __umulhi((uint32_t)M, x);
+    return st == 1u ? gap : (uint32_t)(hi >> 32);
+}
 
 // one DSD demand group: requests sharing (output lengths, gamma, alpha, seed)
 struct DGroup {
@@ -112,17 +148,17 @@ __device__ __forceinline__ void mbar_arrive_expect_tx(uint64_t *bar, uint32_t by
                  : "memory");
 }
 
+// The retry loop lives inside the PTX: a C++ spin loop would make the compiler
+// add forward-progress YIELDs to every enclosing loop (the decode loops).
 __device__ __forceinline__ void mbar_wait(uint64_t *bar, uint32_t phase)
 {
-    uint32_t done = 0;
-    while (!done) {
-        asm volatile(
-            "{\n .reg .pred p;\n mbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\n"
-            " selp.u32 %0, 1, 0, p;\n}\n"
-            : "=r"(done)
-            : "r"(smem_u32(bar)), "r"(phase)
-            : "memory");
-    }
+    asm volatile(
+        "{\n .reg .pred p;\n"
+        "GL_MBAR_WAIT_%=:\n"
+        " mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        " @!p bra GL_MBAR_WAIT_%=;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(phase)
+        : "memory");
 }
 
 // TMA bulk copy global -> shared; completion is signalled on the mbarrier's tx count
@@ -136,5 +172,67 @@ __device__ __forceinline__ void tma_bulk_g2s(void *dst, const void *src, uint32_
 }
 
 __host__ __device__ __forceinline__ int round_up4(int x) { return (x + 3) & ~3; }
+
+// Predicated forms (the predicate lives inside the PTX, so a warp-uniform caller
+// needs no divergent branch and no reconvergence barrier around them).
+__device__ __forceinline__ void mbar_arrive_expect_tx_if(bool p, uint64_t *bar, uint32_t bytes)
+{
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n"
+        " @q mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;\n}\n" ::"r"(smem_u32(bar)),
+        "r"(bytes), "r"((uint32_t)p)
+        : "memory");
+}
+__device__ __forceinline__ void tma_bulk_g2s_if(bool p, void *dst, const void *src, uint32_t bytes,
+                                                uint64_t *bar)
+{
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %4, 0;\n"
+        " @q cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];\n}\n" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(bytes), "r"(smem_u32(bar)), "r"((uint32_t)p)
+        : "memory");
+}
+__device__ __forceinline__ void st_relaxed_gpu_if(bool p, int32_t *ptr, int32_t v)
+{
+    asm volatile(
+        "{\n .reg .pred q;\n setp.ne.u32 q, %2, 0;\n @q st.relaxed.gpu.global.s32 [%0], %1;\n}\n" ::"l"(ptr),
+        "r"(v), "r"((uint32_t)p)
+        : "memory");
+}
+
+// Stage a [count] int32 table into shared memory: the 16-B aligned bulk by TMA
+// (lane 0 issues), the ragged tail by plain loads.  Returns the TMA byte count.
+__device__ __forceinline__ uint32_t stage_table(int32_t *dst, const int32_t *src, int count,
+                                                uint64_t *bar, int lane)
+{
+    uint32_t bulk = 0;
+    if ((reinterpret_cast<uintptr_t>(src) & 15) == 0) bulk = (uint32_t)(count * 4) & ~15u;
+    if (bulk && lane == 0) tma_bulk_g2s(dst, src, bulk, bar);
+    for (int i = bulk / 4 + lane; i < count; i += 32) dst[i] = __ldg(src + i);
+    return bulk;
+}
+
+// GPU-scope release store / acquire load (helper -> leader publication in k_decode)
+__device__ __forceinline__ void st_release_gpu(int32_t *p, int32_t v)
+{
+    asm volatile("st.release.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+__device__ __forceinline__ int32_t ld_acquire_gpu(const int32_t *p)
+{
+    int32_t v;
+    asm volatile("ld.acquire.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ int32_t ld_relaxed_gpu(const int32_t *p)
+{
+    int32_t v;
+    asm volatile("ld.relaxed.gpu.global.s32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+    return v;
+}
+__device__ __forceinline__ void st_relaxed_gpu(int32_t *p, int32_t v)
+{
+    asm volatile("st.relaxed.gpu.global.s32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
 
 }  // namespace gl

@@ -14,10 +14,12 @@
  *
  * Kernels, in launch order:
  *   k_dsd_demand  (k_dsd_demand.cuh) one thread per (DSD demand group, request)
- *   k_chain       (k_chain.cuh)      one warp per timing chain: TMA-staged tables,
- *                                    128-bit loads, max-plus warp scans, decode
- *                                    event loop writing per-request finish times
- *   k_finalize    (k_chain.cuh)      whole GPU over (chain, request): SLO, hash
+ *   k_stages      (k_stages.cuh)     one warp per chain: TMA-staged tables, 128-bit
+ *                                    loads, max-plus warp scans -> decode stream
+ *   k_segments    (k_stages.cuh)     speculation segment starts (largest gaps)
+ *   k_decode      (k_decode.cuh)     leader + helper warps per chain: exact
+ *                                    speculative decode event loops
+ *   k_finalize    (k_decode.cuh)     whole GPU over (chain, request): SLO, hash
  *   k_argmin      (k_argmin.cuh)     one warp per Alg. 1 row
  * No tensor cores: nothing on this path is a contraction.
  */
@@ -26,6 +28,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 #include <map>
 #include <tuple>
@@ -34,7 +37,8 @@
 #include "common.cuh"
 #include "greenllm.h"
 #include "k_argmin.cuh"
-#include "k_chain.cuh"
+#include "k_decode.cuh"
+#include "k_stages.cuh"
 #include "k_dsd_demand.cuh"
 
 namespace {
@@ -42,7 +46,6 @@ namespace {
 using gl::DCarbon;
 using gl::DChain;
 using gl::DGroup;
-using gl::SmemLayout;
 
 thread_local int32_t g_last_launches = 0;
 
@@ -167,12 +170,12 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     std::map<std::tuple<const uint32_t *, int64_t, int32_t, uint64_t, std::vector<uint64_t>>, int> gid;
     std::vector<int> chain_group(n_chains, -1);
     int max_cap = 1;
-    size_t smem = 0;
+    size_t smem_st = 0;
     int64_t rows_total = 0, maxn = 0;
     for (int32_t i = 0; i < n_chains; ++i) {
         const gl_chain &c = chains[i];
         max_cap = std::max(max_cap, (int)c.batch_cap);
-        smem = std::max(smem, SmemLayout(c.max_prompt, c.batch_cap).total);
+        smem_st = std::max(smem_st, (size_t)8 * gl::round_up4(c.max_prompt + 1) + 16);
         rows_total += traces[c.trace_idx].n;
         maxn = std::max(maxn, traces[c.trace_idx].n);
         if (c.mode != GL_MODE_DSD) continue;
@@ -191,13 +194,16 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
         }
         chain_group[i] = it->second;
     }
-    int dev = 0;
+    const size_t smem_dec = gl::decode_smem_bytes(max_cap);
+    int dev = 0, n_sm = 0, smem_optin = 0;
     cudaGetDevice(&dev);
-    int smem_optin = 0;
     cudaDeviceGetAttribute(&smem_optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
-    if (smem > (size_t)smem_optin) return GL_E_UNSUPPORTED;
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    if (smem_st > (size_t)smem_optin || smem_dec > (size_t)smem_optin) return GL_E_UNSUPPORTED;
 
-    // stream-ordered scratch: [chains][groups][K arrays][per-request rows if not given]
+    // Stream-ordered scratch: [chains][groups][K arrays][per-request rows if not
+    // given][decode stream r, (d, j), spec_fin: n + 512 per chain][segment starts]
+    // [segment results][per-chain bookkeeping].  The last two are zeroed.
     const size_t off_groups = align256(sizeof(DChain) * n_chains);
     size_t total = off_groups + align256(sizeof(DGroup) * groups.size());
     std::vector<size_t> k_off(groups.size());
@@ -207,6 +213,29 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     }
     const size_t off_rows = total;
     if (!per_request_out) total += align256(sizeof(int64_t) * 2 * (size_t)rows_total);
+    std::vector<int64_t> dec_off(n_chains), seg_off(n_chains);
+    int64_t dec_total = 0, seg_total = 0;
+    for (int32_t i = 0; i < n_chains; ++i) {
+        const int64_t n = traces[chains[i].trace_idx].n;
+        dec_off[i] = dec_total;
+        dec_total += (n + 512 + 31) & ~(int64_t)31;
+        seg_off[i] = seg_total;
+        seg_total += (n + gl::SEG_LEN - 1) / gl::SEG_LEN + 2;
+    }
+    const size_t off_dec_r = total;
+    total += align256(sizeof(int64_t) * (size_t)dec_total);
+    const size_t off_dec_dj = total;
+    total += align256(sizeof(uint2) * (size_t)dec_total);
+    const size_t off_spec = total;
+    total += align256(sizeof(int64_t) * (size_t)dec_total);
+    const size_t off_segs = total;
+    total += align256(sizeof(int32_t) * (size_t)seg_total);
+    const size_t off_zero = total;
+    const size_t off_segout = total;
+    total += align256(sizeof(gl::DSegOut) * (size_t)seg_total);
+    const size_t off_x = total;
+    total += align256(sizeof(gl::DChainX) * (size_t)n_chains);
+    const size_t zero_bytes = total - off_zero;
     unsigned char *scratch = nullptr;
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
         return st;
@@ -234,6 +263,12 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
         d.sbo = c.step_busy_old_us;
         d.sen = c.step_e_new_uj;
         d.seo = c.step_e_old_uj;
+        d.dec_r = reinterpret_cast<int64_t *>(scratch + off_dec_r) + dec_off[i];
+        d.dec_dj = reinterpret_cast<uint2 *>(scratch + off_dec_dj) + dec_off[i];
+        d.spec_fin = reinterpret_cast<int64_t *>(scratch + off_spec) + dec_off[i];
+        d.seg_start = reinterpret_cast<int32_t *>(scratch + off_segs) + seg_off[i];
+        d.seg_out = reinterpret_cast<gl::DSegOut *>(scratch + off_segout) + seg_off[i];
+        d.x = reinterpret_cast<gl::DChainX *>(scratch + off_x) + i;
         d.n = tr.n;
         d.ttft_slo = c.ttft_slo_us;
         d.tpot_slo = c.tpot_slo_us;
@@ -250,6 +285,7 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     if (e == cudaSuccess && !groups.empty())
         e = cudaMemcpyAsync(scratch + off_groups, groups.data(), sizeof(DGroup) * groups.size(),
                             cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) e = cudaMemsetAsync(scratch + off_zero, 0, zero_bytes, stream);
     int launches = 0;
     if (e == cudaSuccess && !groups.empty()) {
         int64_t gmax = 0;
@@ -263,24 +299,47 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
         ++launches;
     }
     if (e == cudaSuccess) {
+        e = cudaFuncSetAttribute(gl::k_stages, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_st);
+        if (e == cudaSuccess) {
+            prof_begin("k_stages", stream);
+            gl::k_stages<<<n_chains, 32, smem_st, stream>>>(dc, stats_out, rows);
+            e = cudaGetLastError();
+            prof_end(stream);
+            ++launches;
+        }
+    }
+    if (e == cudaSuccess) {
+        prof_begin("k_segments", stream);
+        gl::k_segments<<<n_chains, 32, 0, stream>>>(dc);
+        e = cudaGetLastError();
+        prof_end(stream);
+        ++launches;
+    }
+    if (e == cudaSuccess) {
+        // one leader warp per chain plus helper warps: about four warps per SM
+        int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
+        if (getenv("GL_DEBUG_NO_HELPERS")) extra = -1;  // TEMP experiment
+        const unsigned blocks = (unsigned)(n_chains * (1 + std::max(extra, 0)));
+        const int32_t helper_flag = extra < 0 ? -n_chains : n_chains;
         auto launch = [&](auto kern) {
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                                 (int)smem);
+                                                 (int)smem_dec);
             if (r != cudaSuccess) return r;
-            prof_begin("k_chain", stream);
-            kern<<<n_chains, 32, smem, stream>>>(dc, stats_out, rows);
+            prof_begin("k_decode", stream);
+            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, stream>>>(dc, stats_out, rows, helper_flag);
             r = cudaGetLastError();
             prof_end(stream);
             return r;
         };
-        if (max_cap <= 31)  // the one-row fast path needs b < 32
-            e = launch(gl::k_chain<1>);
+        if (max_cap <= 31)  // the one-row fast paths need b < 32
+            e = launch(gl::k_decode<1>);
         else if (max_cap <= 64)
-            e = launch(gl::k_chain<2>);
+            e = launch(gl::k_decode<2>);
         else if (max_cap <= 128)
-            e = launch(gl::k_chain<4>);
+            e = launch(gl::k_decode<4>);
         else
-            e = launch(gl::k_chain<8>);
+            e = launch(gl::k_decode<8>);
         ++launches;
     }
     if (e == cudaSuccess) {

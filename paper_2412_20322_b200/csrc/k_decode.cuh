@@ -1,0 +1,704 @@
+// k_decode.cuh -- S5 + S7: the continuous-batching decode stage (R15-R23) of every
+// timing chain, with exact intra-chain speculation; and k_finalize (S6 + hash).
+//
+// The decode stage of one chain is a serial event chain.  It becomes parallel at
+// idle points: if every decode request before q has finished by r_q, the decode
+// stage is empty when q becomes ready, and the run from q onward depends only on
+// requests >= q (R17: an empty batch restarts exactly at r_q).  k_segments cut the
+// stream into segments at likely idle points; in k_decode
+//   * helper warps simulate segment k from an empty batch at r_{s_k}, using only
+//     its own requests, and publish (finish times, sums, last finish maxfin_k);
+//   * one leader warp per chain walks the segments in order.  Segment 0 starts
+//     idle.  When segment k starts idle (by induction) and its helper run ended no
+//     later than r_{s_{k+1}} (maxfin_k <= r_{s_{k+1}}), no later request can have
+//     joined it, so the helper run IS the true run and s_{k+1} starts idle: the
+//     leader accepts it.  Otherwise (result missing, or segment k overlaps the next
+//     one) the leader simulates from s_k itself and keeps going across segment
+//     starts until it reaches one with an empty batch -- again an idle point.
+// Results are bit-identical to a single sequential run; the speculation only
+// changes how much of the chain one warp has to walk serially.
+//
+// Each run reads the decode stream (r, demand, request) from HBM through a
+// 256-entry shared-memory window refilled in 128-entry halves by TMA bulk copies
+// (cp.async.bulk + one mbarrier per half).  The loop never steps single
+// iterations: a member admitted at iteration I with demand d finishes at
+// F = I + d; the next event is min(REDUX-min F - I, the boundary where the head
+// becomes ready) and T += k * step[b].  For cap <= 31 (one member per lane) a
+// saturated fast path (full batch: one leaves, the freed lane takes the ready
+// head) and a light-load fast path (alternate join / leave) carry almost all
+// events; larger caps use the general multi-row loop (SPL members per lane).
+#pragma once
+
+#include "common.cuh"
+
+namespace gl {
+
+constexpr int DEC_WARPS = 1;  // one warp per k_decode block (leader or helper)
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src)
+{
+    asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(smem_u32(dst)), "l"(src)
+                 : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+__device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wait_group 0;" ::: "memory"); }
+
+// One warp's shared-memory window on the decode stream of its chain, refilled
+// in 128-entry halves by asynchronous 16-byte copies (cp.async / LDGSTS, one
+// commit group per half).  The wait is a single dependency barrier (no retry
+// loop), which keeps the decode loops free of forward-progress YIELDs.
+struct RingW {
+    int64_t *r;      // smem [RING]
+    uint2 *dj;       // smem [RING]
+    const int64_t *gr;
+    const uint2 *gdj;
+    int32_t q_end;      // entries >= q_end read as "no request" (INT64_MAX)
+    int32_t base;       // first chunk fetched by start()
+    int32_t fill_next;  // next chunk to fetch
+    int32_t ready_to;   // chunks below this are waited for
+
+    __device__ __forceinline__ void issue(int32_t q, int lane)
+    {
+        const int h = (q >> 7) & 1;
+        // 128 x 8 B of r and of (d, j): 64 x 16 B each, two copies per lane each
+        const char *sr = reinterpret_cast<const char *>(gr + q);
+        const char *sd = reinterpret_cast<const char *>(gdj + q);
+        char *dr = reinterpret_cast<char *>(r + h * 128);
+        char *dd = reinterpret_cast<char *>(dj + h * 128);
+        cp_async16(dr + 16 * lane, sr + 16 * lane);
+        cp_async16(dr + 16 * (lane + 32), sr + 16 * (lane + 32));
+        cp_async16(dd + 16 * lane, sd + 16 * lane);
+        cp_async16(dd + 16 * (lane + 32), sd + 16 * (lane + 32));
+        cp_async_commit();
+    }
+    // all issued halves have landed (the newest one was issued long before)
+    __device__ __forceinline__ void wait(int32_t q, int lane)
+    {
+        cp_async_wait_all();
+        // the end of this run's input reads as "no request" (lanes 0 and 1)
+        const int32_t qs = q_end + lane;
+        if (lane < 2 && qs >= q && qs < q + 128) r[qs & RING_MASK] = INT64_MAX;
+        __syncwarp();
+    }
+    __device__ __forceinline__ void start(int32_t q0, int lane)
+    {
+        cp_async_wait_all();  // fills the previous run left in flight
+        __syncwarp();         // everyone is done with the previous run's window
+        base = q0 & ~127;
+        issue(base, lane);
+        issue(base + 128, lane);
+        cp_async_wait_all();
+        const int32_t qs = q_end + lane;
+        if (lane < 2 && qs >= base && qs < base + 256) r[qs & RING_MASK] = INT64_MAX;
+        __syncwarp();
+        fill_next = base + 256;
+        ready_to = base + 256;
+    }
+    // called after the head index moved to nxt: recycle the consumed half, and
+    // make sure the half holding nxt + 1 has landed
+    __device__ __forceinline__ void advanced(int32_t nxt, int lane)
+    {
+        if ((nxt & 127) == 0 && nxt >= base + 128) {
+            issue(fill_next, lane);
+            fill_next += 128;
+        }
+        if (nxt + 1 >= ready_to) {
+            wait(ready_to, lane);
+            ready_to += 128;
+        }
+    }
+};
+
+struct RunOut {
+    int64_t mk;       // last finish time of the run (0 if nothing finished)
+    int64_t sums[4];  // decode busy_new, busy_old, e_new, e_old
+    int32_t stop_seg; // extend mode: segment index whose start the run stopped at
+};
+
+struct RunCtx {
+    const DChain *ch;
+    const int32_t *steps;   // smem [cap+1]
+    const uint64_t *magic;  // smem [cap+1] Lemire reciprocals of steps
+    int64_t *rows_fin;      // &perreq[2*out_off + 1]: finish column of this chain
+    int cap, lane;
+    int32_t nseg;
+};
+
+// kept out of line so the decode loops stay free of memory-ordering operations
+__device__ __noinline__ void publish_pos(bool p, int32_t *ptr, int32_t v) { st_relaxed_gpu_if(p, ptr, v); }
+
+// Segment k's helper result is published and clean: its isolated run ended no
+// later than the next segment's first ready time (always true for the last one).
+__device__ __noinline__ bool seg_clean(const DChain &ch, int32_t k, int32_t nseg)
+{
+    if (k >= nseg || !ld_acquire_gpu(&ch.seg_out[k].done)) return false;
+    const int64_t maxfin = __ldcg(&ch.seg_out[k].maxfin);
+    const int64_t r_next = k + 1 < nseg ? __ldcg(ch.dec_r + ch.seg_start[k + 1]) : INT64_MAX;
+    return maxfin <= r_next;
+}
+
+// sums of iterations x batch-indexed tables, reduced over the warp
+template <int SPL>
+__device__ __forceinline__ void run_sums(const RunCtx &cx, const uint64_t (&iters)[SPL + 1],
+                                         int64_t (&s)[4])
+{
+    int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
+#pragma unroll
+    for (int r = 0; r <= SPL; ++r) {
+        const int bb = r * 32 + cx.lane;
+        if (bb >= 1 && bb <= cx.cap && iters[r]) {
+            const int64_t it = (int64_t)iters[r];
+            a0 += it * __ldg(cx.ch->sbn + bb);
+            a1 += it * __ldg(cx.ch->sbo + bb);
+            a2 += it * __ldg(cx.ch->sen + bb);
+            a3 += it * __ldg(cx.ch->seo + bb);
+        }
+    }
+    s[0] = warp_sum_i64(a0);
+    s[1] = warp_sum_i64(a1);
+    s[2] = warp_sum_i64(a2);
+    s[3] = warp_sum_i64(a3);
+}
+
+// One decode run from an empty batch at r_{q0}.  LEADER: finish times go to the
+// chain's (ttft, finish) rows, and the run continues across segment starts until
+// it meets one with an empty batch whose helper result is published and clean
+// (then it stops there and the leader accepts from that segment on).  Helper:
+// finish times go to spec_fin[q]; the run covers its segment only.
+template <int SPL, bool LEADER>
+__device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t k0)
+{
+    constexpr bool to_rows = LEADER, extend = LEADER;
+    const DChain &ch = *cx.ch;
+    const int lane = cx.lane, cap = cx.cap;
+    // shared-memory tables re-derived from the symbol (keeps plain LDS addressing;
+    // layout as set up by k_decode: windows, mbarriers, reciprocals, steps)
+    extern __shared__ __align__(16) unsigned char dyn_smem[];
+    const uint64_t *const magic =
+        reinterpret_cast<const uint64_t *>(dyn_smem + DEC_WARPS * RING * 16) + 2 * DEC_WARPS + 2;
+    const int32_t *const steps = reinterpret_cast<const int32_t *>(magic + round_up4(cap + 1));
+    int64_t *const fin_rows = cx.rows_fin;
+    int64_t *const fin_spec = ch.spec_fin;
+    DChainX *const xx = ch.x;
+    const unsigned lane_bit = 1u << lane;
+
+    RunOut res;
+    res.stop_seg = -1;
+    ring.start(q0, lane);
+    // the window again, straight from the shared-memory symbol (keeps LDS addressing)
+    const int wid = threadIdx.x >> 5;
+    const int64_t *const rr = reinterpret_cast<const int64_t *>(dyn_smem) + wid * RING;
+    const uint2 *const rdj =
+        reinterpret_cast<const uint2 *>(dyn_smem + DEC_WARPS * RING * 8) + wid * RING;
+    int32_t nxt = q0;
+    int64_t h_r = rr[nxt & RING_MASK], n_r = rr[(nxt + 1) & RING_MASK];
+    uint2 h_dj = rdj[nxt & RING_MASK], n_dj = rdj[(nxt + 1) & RING_MASK];
+    // next segment start after k0 (extend mode), for stop checks and leader_pos
+    const int32_t nseg_r = cx.nseg;
+    int32_t kb = k0 + 1;
+    int32_t nb = extend ? ch.seg_start[kb] : INT32_MAX;
+
+    auto advance = [&]() {
+        ++nxt;
+        h_r = n_r;
+        h_dj = n_dj;
+        // all ring maintenance happens where nxt + 1 crosses a 128-entry half
+        if (__builtin_expect((uint32_t)((nxt + 1) & 127) <= 1u, 0)) {
+            ring.advanced(nxt, lane);
+            if (extend && (nxt & 127) == 0) {  // publish the leader's progress
+                while (kb < nseg_r && nb <= nxt) nb = ch.seg_start[++kb];
+                publish_pos(lane == 0, &xx->leader_pos, kb - 1);
+            }
+        }
+        const int e1 = (nxt + 1) & RING_MASK;
+        n_r = rr[e1];
+        n_dj = rdj[e1];
+    };
+    auto fin_addr = [&](uint32_t j, int32_t q) -> int64_t * {
+        return to_rows ? fin_rows + 2 * (int64_t)j : fin_spec + q;
+    };
+
+    int64_t T = 0, mk = 0;
+    uint32_t I = 0;
+    int b = 0;
+    uint64_t iters[SPL + 1];
+#pragma unroll
+    for (int s = 0; s <= SPL; ++s) iters[s] = 0;
+
+    if constexpr (SPL == 1) {
+        uint32_t Fm = F_EMPTY, fmin = F_EMPTY;
+        int64_t *fa = fin_rows;
+        unsigned fr = cap >= 32 ? FULL : ((1u << cap) - 1u);
+        uint32_t c_b = 0;  // iterations at batch size b == lane
+        int32_t st_d = 0, st_c = 0, st_u = 0;
+        uint64_t M_d = 0, M_c = 0, M_u = 0;
+        auto load_nbr = [&](int nbb) {
+            st_c = steps[nbb];
+            M_c = magic[nbb];
+            st_u = steps[min(nbb + 1, cap)];
+            M_u = magic[min(nbb + 1, cap)];
+            st_d = steps[max(nbb - 1, 0)];
+            M_d = magic[max(nbb - 1, 0)];
+        };
+        auto shift_up = [&]() {
+            st_d = st_c;
+            M_d = M_c;
+            st_c = st_u;
+            M_c = M_u;
+            st_u = steps[min(b + 1, cap)];
+            M_u = magic[min(b + 1, cap)];
+        };
+        auto shift_down = [&]() {
+            st_u = st_c;
+            M_u = M_c;
+            st_c = st_d;
+            M_c = M_d;
+            st_d = steps[max(b - 1, 0)];
+            M_d = magic[max(b - 1, 0)];
+        };
+        load_nbr(0);
+        for (;;) {
+            // ---- FCFS joins at boundary T (r <= T) while the batch has room (R16, R18)
+            while (b < cap && h_r <= T) {
+                if (I >= 0x80000000u) {  // rebase the 32-bit iteration counter
+                    if (Fm != F_EMPTY) Fm -= I;
+                    if (fmin != F_EMPTY) fmin -= I;
+                    iters[0] += c_b;
+                    c_b = 0;
+                    I = 0;
+                }
+                const unsigned bit = fr & (0u - fr);
+                fr ^= bit;
+                const uint32_t fnew = I + h_dj.x;
+                if (lane_bit == bit) {
+                    Fm = fnew;
+                    fa = fin_addr(h_dj.y, nxt);
+                }
+                fmin = min(fmin, fnew);
+                ++b;
+                shift_up();
+                advance();
+            }
+            if (b == 0) {  // idle until the next decode request is ready (R17)
+                if (h_r == INT64_MAX) break;
+                if (extend && nxt >= nb) {  // reached (or passed) the next segment start
+                    while (kb < nseg_r && nb < nxt) nb = ch.seg_start[++kb];
+                    if (nb == nxt && seg_clean(ch, kb, nseg_r)) {  // idle point: hand over
+                        res.stop_seg = kb;
+                        break;
+                    }
+                }
+                T = h_r;
+                continue;
+            }
+            if (b == cap) {
+                // Saturated fast path: with a full batch the next event is a leave;
+                // while exactly one member leaves and the head is already ready, the
+                // freed lane takes the head at the same boundary (R16).
+                const int64_t stc = st_c;
+                uint32_t it = 0;
+                for (;;) {
+                    const uint32_t kL = fmin - I;
+                    I = fmin;
+                    T += (int64_t)kL * stc;
+                    it += kL;
+                    const bool lv = Fm == I;
+                    const unsigned lm = __ballot_sync(FULL, lv);
+                    if (lv) *fa = T;
+                    mk = T;
+                    const bool one = (lm & (lm - 1u)) == 0u;
+                    if (!(one && h_r <= T && I < 0x80000000u)) {
+                        if (lv) Fm = F_EMPTY;
+                        fr |= lm;
+                        b -= __popc(lm);
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        break;
+                    }
+                    if (lv) {
+                        Fm = I + h_dj.x;
+                        fa = fin_addr(h_dj.y, nxt);
+                    }
+                    fmin = __reduce_min_sync(FULL, Fm);
+                    advance();
+                }
+                c_b += (lane == cap) ? it : 0u;
+                if (b == cap - 1) shift_down();
+                else load_nbr(b);
+                continue;
+            }
+            {
+                // Light-load fast path (0 < b < cap, head not ready at T): each step
+                // is the head's join at kJ = ceil(gap / step[b]) or the next leave at
+                // kL.  Exits when a join fills the batch or finds another ready head,
+                // when the batch empties, or (to the general code below) on a gap of
+                // 2^31 us or more / a pending counter rebase.
+                bool slow = false;
+                for (;;) {
+                    const int64_t st = st_c;
+                    const uint32_t kL = fmin - I;
+                    const int64_t gap = h_r - T;
+                    const uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, M_c);
+                    if (gap >= 0x80000000ll || I >= 0x80000000u) {
+                        slow = true;
+                        break;
+                    }
+                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;
+                        I += kJ;
+                        c_b += (lane == b) ? kJ : 0u;
+                        const unsigned bit = fr & (0u - fr);
+                        fr ^= bit;
+                        const uint32_t fnew = I + h_dj.x;
+                        if (lane_bit == bit) {
+                            Fm = fnew;
+                            fa = fin_addr(h_dj.y, nxt);
+                        }
+                        fmin = min(fmin, fnew);
+                        ++b;
+                        shift_up();
+                        advance();
+                        if (b == cap || h_r <= T) break;
+                    } else {  // leave at iteration fmin (R16)
+                        T += (int64_t)kL * st;
+                        I = fmin;
+                        c_b += (lane == b) ? kL : 0u;
+                        const bool lv = Fm == I;
+                        const unsigned lm = __ballot_sync(FULL, lv);
+                        if (lv) {
+                            *fa = T;
+                            Fm = F_EMPTY;
+                        }
+                        fr |= lm;
+                        const int nl = __popc(lm);
+                        b -= nl;
+                        mk = T;
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        if (nl == 1) shift_down();
+                        else load_nbr(b);
+                        if (b == 0 || h_r <= T) break;
+                    }
+                }
+                if (!slow) continue;
+            }
+            // ---- general event: a join at kJ < kL, else the leave at kL (R16)
+            const int64_t st = st_c;
+            const uint32_t kL = fmin - I;
+            if (b < cap) {
+                const int64_t gap = h_r - T;  // > 0: the head was not admitted at T
+                uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, M_c);
+                const bool far = gap >= 0x80000000ll;  // very long gap, or no head
+                if (kJ < kL || far) {
+                    if (far)  // exact 64-bit path; no head (INT64_MAX) never joins
+                        kJ = (h_r != INT64_MAX && gap <= (int64_t)(kL - 1) * st)
+                                 ? (uint32_t)((gap + st - 1) / st) : 0xFFFFFFFFu;
+                    if (kJ < kL) {
+                        T += (int64_t)kJ * st;
+                        I += kJ;
+                        c_b += (lane == b) ? kJ : 0u;
+                        continue;
+                    }
+                }
+            }
+            T += (int64_t)kL * st;
+            I = fmin;
+            c_b += (lane == b) ? kL : 0u;
+            const bool lv = Fm == I;
+            const unsigned lm = __ballot_sync(FULL, lv);
+            if (lv) {
+                *fa = T;
+                Fm = F_EMPTY;
+            }
+            fr |= lm;
+            const int nl = __popc(lm);
+            b -= nl;
+            mk = T;
+            fmin = __reduce_min_sync(FULL, Fm);
+            if (nl == 1) shift_down();
+            else load_nbr(b);
+        }
+        iters[0] += c_b;
+    } else {
+        // general loop, caps 32..256: SPL rows of 32 member slots per lane
+        uint32_t F[SPL];
+        int64_t *fa[SPL];
+        unsigned free_m[SPL];
+        uint32_t cnt[SPL + 1];
+#pragma unroll
+        for (int s = 0; s < SPL; ++s) {
+            F[s] = F_EMPTY;
+            fa[s] = fin_rows;
+            const int lo = s * 32;
+            free_m[s] = cap >= lo + 32 ? FULL : (cap > lo ? ((1u << (cap - lo)) - 1u) : 0u);
+        }
+#pragma unroll
+        for (int s = 0; s <= SPL; ++s) cnt[s] = 0;
+        for (;;) {
+            while (b < cap && h_r <= T) {  // FCFS joins (R16, R18)
+                if (I >= 0x80000000u) {     // rebase the 32-bit iteration counter
+#pragma unroll
+                    for (int s = 0; s < SPL; ++s)
+                        if (F[s] != F_EMPTY) F[s] -= I;
+#pragma unroll
+                    for (int s = 0; s <= SPL; ++s) {
+                        iters[s] += cnt[s];
+                        cnt[s] = 0;
+                    }
+                    I = 0;
+                }
+                int s_sel = SPL;
+                unsigned bit = 0;
+#pragma unroll
+                for (int s = SPL - 1; s >= 0; --s)
+                    if (free_m[s]) {
+                        s_sel = s;
+                        bit = free_m[s] & (0u - free_m[s]);
+                    }
+#pragma unroll
+                for (int s = 0; s < SPL; ++s) {
+                    if (s == s_sel) {
+                        free_m[s] ^= bit;
+                        if (lane_bit == bit) {
+                            F[s] = I + h_dj.x;
+                            fa[s] = fin_addr(h_dj.y, nxt);
+                        }
+                    }
+                }
+                ++b;
+                advance();
+            }
+            if (b == 0) {  // idle (R17)
+                if (h_r == INT64_MAX) break;
+                if (extend && nxt >= nb) {  // reached (or passed) the next segment start
+                    while (kb < nseg_r && nb < nxt) nb = ch.seg_start[++kb];
+                    if (nb == nxt && seg_clean(ch, kb, nseg_r)) {  // idle point: hand over
+                        res.stop_seg = kb;
+                        break;
+                    }
+                }
+                T = h_r;
+                continue;
+            }
+            const int64_t st = steps[b];
+            uint32_t kJ = 0xFFFFFFFFu;
+            if (b < cap) {
+                const int64_t gap = h_r - T;
+                if (gap < 0x80000000ll) kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, magic[b]);
+                else if (h_r != INT64_MAX)
+                    kJ = (uint32_t)min((gap + st - 1) / st, (int64_t)0xFFFFFFFF);
+            }
+            uint32_t fmin = F[0];
+#pragma unroll
+            for (int s = 1; s < SPL; ++s) fmin = min(fmin, F[s]);
+            fmin = __reduce_min_sync(FULL, fmin);
+            const uint32_t kL = fmin - I;
+            const uint32_t k = min(kL, kJ);
+            T += (int64_t)k * st;
+            I += k;
+            {
+                const uint32_t kk = (lane == (b & 31)) ? k : 0u;
+                const int row = b >> 5;
+#pragma unroll
+                for (int s = 0; s <= SPL; ++s) cnt[s] += (s == row) ? kk : 0u;
+            }
+            int nl = 0;
+#pragma unroll
+            for (int s = 0; s < SPL; ++s) {  // leaves at T (none when k < kL)
+                const bool lv = F[s] == I;
+                const unsigned lm = __ballot_sync(FULL, lv);
+                if (lv) {
+                    *fa[s] = T;
+                    F[s] = F_EMPTY;
+                }
+                free_m[s] |= lm;
+                nl += __popc(lm);
+            }
+            b -= nl;
+            if (nl) mk = T;
+        }
+#pragma unroll
+        for (int s = 0; s <= SPL; ++s) iters[s] += cnt[s];
+    }
+    res.mk = mk;
+    run_sums<SPL>(cx, iters, res.sums);
+    return res;
+}
+
+// Helpers: speculative isolated runs of segments ahead of the leader.  Out of
+// line so the kernel body holds a single (the leader's) copy of the decode loops.
+template <int SPL>
+__device__ __noinline__ void helper_loop(const RunCtx &cx, RingW &ring)
+{
+    const DChain &ch = *cx.ch;
+    const int lane = cx.lane;
+    const int32_t nseg = cx.nseg;
+    for (;;) {
+        int32_t k = 0;
+        if (lane == 0) k = atomicAdd(&ch.x->next_seg, 1);
+        k = __shfl_sync(FULL, k, 0);
+        if (k >= nseg) break;
+        if (k <= ld_relaxed_gpu(&ch.x->leader_pos)) continue;  // the leader is there
+        ring.q_end = ch.seg_start[k + 1];
+        const RunOut ro = decode_run<SPL, false>(cx, ring, ch.seg_start[k], k);
+        if (lane == 0) {
+            DSegOut &so = ch.seg_out[k];
+            so.maxfin = ro.mk;
+            for (int i = 0; i < 4; ++i) so.sums[i] = ro.sums[i];
+            __threadfence();
+            st_release_gpu(&so.done, 1);
+        }
+    }
+}
+
+// Leader + helpers (see the file comment).  One warp per block: blocks
+// [0, n_chains) are the leaders of chain blockIdx.x, blocks >= n_chains are
+// helpers of chain blockIdx.x % n_chains.
+template <int SPL>
+__global__ void __launch_bounds__(32 * DEC_WARPS, 1)
+    k_decode(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
+             int64_t *__restrict__ perreq, int32_t n_chains_flag)
+{
+    extern __shared__ __align__(16) unsigned char smem[];
+    const bool no_helpers = n_chains_flag < 0;  // TEMP experiment
+    const int32_t n_chains = no_helpers ? -n_chains_flag : n_chains_flag;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int c = blockIdx.x % n_chains;
+    const bool leader = blockIdx.x < n_chains && warp == 0;
+    const DChain &ch = chains[c];
+    const int cap = ch.cap;
+    const int cappad = round_up4(cap + 1);
+    // smem: per-warp windows first (16-B aligned), then mbarriers, then tables
+    int64_t *ring_r = reinterpret_cast<int64_t *>(smem) + warp * RING;
+    uint2 *ring_dj = reinterpret_cast<uint2 *>(smem + DEC_WARPS * RING * 8) + warp * RING;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + DEC_WARPS * RING * 16);
+    uint64_t *magic = bars + 2 * DEC_WARPS + 2;
+    int32_t *steps = reinterpret_cast<int32_t *>(magic + cappad);
+
+    // S0: batch-indexed step table by TMA (warp 0), reciprocals, ring barriers
+    if (threadIdx.x == 0) mbar_init(bars + 2 * DEC_WARPS, 1);
+    if (lane == 0) {
+        mbar_init(bars + 2 * warp, 1);
+        mbar_init(bars + 2 * warp + 1, 1);
+    }
+    __syncthreads();
+    if (warp == 0) {
+        const uint32_t tx = stage_table(steps, ch.step, cap + 1, bars + 2 * DEC_WARPS, lane);
+        if (lane == 0) mbar_arrive_expect_tx(bars + 2 * DEC_WARPS, tx);
+        mbar_wait(bars + 2 * DEC_WARPS, 0);
+    }
+    __syncthreads();
+    for (int bb = threadIdx.x; bb <= cap; bb += blockDim.x) {
+        const int32_t s = steps[bb];
+        magic[bb] = s > 1 ? 0xFFFFFFFFFFFFFFFFull / (uint64_t)s + 1ull : 0ull;
+    }
+    __syncthreads();
+
+    const int32_t nseg = ch.x->nseg;
+    RunCtx cx{&ch, steps, magic, perreq + 2 * ch.out_off + 1, cap, lane, nseg};
+    RingW ring;
+    ring.r = ring_r;
+    ring.dj = ring_dj;
+    ring.gr = ch.dec_r;
+    ring.gdj = ch.dec_dj;
+    ring.fill_next = ring.ready_to = 0;
+
+    if (leader) {
+        int64_t acc[4] = {0, 0, 0, 0};
+        int64_t mk = 0;
+        int32_t k = 0;
+        const int32_t M = ch.x->M;
+        while (k < nseg) {
+            if (k > 0 && seg_clean(ch, k, nseg)) {
+                // published before done (release); read through L2
+                const int64_t so_maxfin = __ldcg(&ch.seg_out[k].maxfin);
+                const int32_t s_lo = ch.seg_start[k], s_hi = ch.seg_start[k + 1];
+                {  // clean: accept the helper's exact run
+                    for (int32_t q = s_lo + lane; q < s_hi; q += 32) {
+                        const uint32_t j = __ldcg(&ch.dec_dj[q].y);
+                        cx.rows_fin[2 * (int64_t)j] = __ldcg(ch.spec_fin + q);
+                    }
+                    for (int i = 0; i < 4; ++i) acc[i] += __ldcg(&ch.seg_out[k].sums[i]);
+                    mk = max(mk, so_maxfin);
+                    ++k;
+                    if (lane == 0) st_relaxed_gpu(&ch.x->leader_pos, k);
+                    continue;
+                }
+            }
+            // simulate from s_k (an idle point) until the next idle segment start
+            ring.q_end = M;
+            const RunOut ro = decode_run<SPL, true>(cx, ring, ch.seg_start[k], k);
+            for (int i = 0; i < 4; ++i) acc[i] += ro.sums[i];
+            mk = max(mk, ro.mk);
+            k = ro.stop_seg >= 0 ? ro.stop_seg : nseg;
+            if (lane == 0) st_relaxed_gpu(&ch.x->leader_pos, k);
+        }
+        if (lane == 0) {
+            gl_chain_stats &s = stats[c];
+            s.busy_new_us += acc[0];
+            s.busy_old_us += acc[1];
+            s.e_new_uj += acc[2];
+            s.e_old_uj += acc[3];
+            s.makespan_us = max(s.makespan_us, mk);
+        }
+    } else {
+        if (no_helpers) return;
+        helper_loop<SPL>(cx, ring);
+    }
+}
+
+__host__ __device__ inline size_t decode_smem_bytes(int cap)
+{
+    return (size_t)DEC_WARPS * RING * 16 + (2 * DEC_WARPS + 2) * 8 + (size_t)round_up4(cap + 1) * 12 + 16;
+}
+
+// ---- S6 + S7: per-request SLO test and hash, the whole GPU over (chain, request)
+//   ok_j = TTFT_j <= SLO_ttft and (o_j = 1 or finish_j - c_j <= SLO_tpot (o_j - 1))
+//   (Table 2; R25-R27), hash += mix64(j, ttft_j, finish_j).
+// Integer atomics commute, so the result is deterministic.
+__global__ void __launch_bounds__(256)
+    k_finalize(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
+               const int64_t *__restrict__ perreq, int per_thread)
+{
+    __shared__ unsigned long long s_ok[8], s_hash[8];
+    const DChain &ch = chains[blockIdx.y];
+    const int64_t n = ch.n;
+    const int64_t *rows = perreq + 2 * ch.out_off;
+    const int64_t ttft_slo = ch.ttft_slo, tpot_slo = ch.tpot_slo;
+    unsigned long long ok = 0, hash = 0;
+    const int64_t base = (int64_t)blockIdx.x * blockDim.x * per_thread;
+    for (int q = 0; q < per_thread; ++q) {
+        const int64_t j = base + (int64_t)q * blockDim.x + threadIdx.x;
+        if (j < n) {
+            const longlong2 tf = __ldg(reinterpret_cast<const longlong2 *>(rows) + j);
+            const int64_t a = __ldg(ch.a + j);
+            uint32_t o = __ldg(ch.o + j);
+            o = min(max(o, 1u), O_LIMIT - 1);
+            const int64_t c = a + tf.x;
+            const bool good = tf.x <= ttft_slo &&
+                              (o == 1 || tf.y - c <= tpot_slo * (int64_t)(o - 1));
+            ok += good ? 1 : 0;
+            hash += splitmix_fin((uint64_t)j ^ rotl64((uint64_t)tf.x, 21) ^
+                                 rotl64((uint64_t)tf.y, 42));
+        }
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        ok += __shfl_xor_sync(FULL, ok, off);
+        hash += __shfl_xor_sync(FULL, hash, off);
+    }
+    const int w = threadIdx.x >> 5;
+    if ((threadIdx.x & 31) == 0) {
+        s_ok[w] = ok;
+        s_hash[w] = hash;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int i = 1; i < (int)(blockDim.x >> 5); ++i) {
+            ok += s_ok[i];
+            hash += s_hash[i];
+        }
+        if (ok) atomicAdd(reinterpret_cast<unsigned long long *>(&stats[blockIdx.y].slo_ok), ok);
+        atomicAdd(reinterpret_cast<unsigned long long *>(&stats[blockIdx.y].req_hash), hash);
+    }
+}
+
+}  // namespace gl

@@ -18,6 +18,6 @@ for ci in range(len(g.chains)):
     kt = dict(N.kernel_times())
     s = api.stats_numpy(st)[0]
     ch = g.chains[ci]
-    out.append((kt['k_chain'], ci, ch.label, int(s['slo_ok']), int(s['makespan_us'])))
+    out.append((kt['k_decode'], ci, ch.label, int(s['slo_ok']), int(s['makespan_us']), kt['k_stages']))
 out.sort(reverse=True)
-for r in out: print("%.2f ms  chain %2d  %-50s ok=%d makespan=%.0fs" % (r[0], r[1], r[2], r[3], r[4]/1e6))
+for r in out: print("%.2f ms  chain %2d  %-50s ok=%d makespan=%.0fs  (k_stages %.2f ms)" % (r[0], r[1], r[2], r[3], r[4]/1e6, r[5]))

@@ -289,7 +289,7 @@ def test_evaluate_host_matches_device_path():
     assert np.array_equal(res.choice, choice.cpu().numpy())
     assert np.array_equal(res.via_fallback, fb.cpu().numpy())
     assert np.array_equal(res.carbon, carbon.cpu().numpy())
-    assert res.launches == 4 and res.h2d_bytes > 0
+    assert res.launches == 6 and res.h2d_bytes > 0
 
 
 def test_abi_errors():
