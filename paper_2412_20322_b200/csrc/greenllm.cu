@@ -303,7 +303,7 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
                                  (int)smem_st);
         if (e == cudaSuccess) {
             prof_begin("k_stages", stream);
-            gl::k_stages<<<n_chains, 32, smem_st, stream>>>(dc, stats_out, rows);
+            gl::k_stages<<<n_chains, 32 * gl::ST_WARPS, smem_st, stream>>>(dc, stats_out, rows);
             e = cudaGetLastError();
             prof_end(stream);
             ++launches;
@@ -311,23 +311,21 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     }
     if (e == cudaSuccess) {
         prof_begin("k_segments", stream);
-        gl::k_segments<<<n_chains, 32, 0, stream>>>(dc);
+        gl::k_segments<<<n_chains, 256, 0, stream>>>(dc);
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;
     }
     if (e == cudaSuccess) {
         // one leader warp per chain plus helper warps: about four warps per SM
-        int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
-        if (getenv("GL_DEBUG_NO_HELPERS")) extra = -1;  // TEMP experiment
-        const unsigned blocks = (unsigned)(n_chains * (1 + std::max(extra, 0)));
-        const int32_t helper_flag = extra < 0 ? -n_chains : n_chains;
+        const int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
+        const unsigned blocks = (unsigned)(n_chains * (1 + extra));
         auto launch = [&](auto kern) {
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem_dec);
             if (r != cudaSuccess) return r;
             prof_begin("k_decode", stream);
-            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, stream>>>(dc, stats_out, rows, helper_flag);
+            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, stream>>>(dc, stats_out, rows, (int32_t)n_chains);
             r = cudaGetLastError();
             prof_end(stream);
             return r;

@@ -555,11 +555,9 @@ __device__ __noinline__ void helper_loop(const RunCtx &cx, RingW &ring)
 template <int SPL>
 __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     k_decode(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
-             int64_t *__restrict__ perreq, int32_t n_chains_flag)
+             int64_t *__restrict__ perreq, int32_t n_chains)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    const bool no_helpers = n_chains_flag < 0;  // TEMP experiment
-    const int32_t n_chains = no_helpers ? -n_chains_flag : n_chains_flag;
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x % n_chains;
     const bool leader = blockIdx.x < n_chains && warp == 0;
@@ -640,7 +638,6 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
             s.makespan_us = max(s.makespan_us, mk);
         }
     } else {
-        if (no_helpers) return;
         helper_loop<SPL>(cx, ring);
     }
 }

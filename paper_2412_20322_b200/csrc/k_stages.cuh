@@ -1,241 +1,355 @@
-// k_stages.cuh -- S0-S4 for every timing chain (one warp per chain) and the
-// segment starts the decode speculation uses.
+// k_stages.cuh -- S0-S4 for every timing chain and the segment starts the decode
+// speculation uses.
 //
 //   stage 1  prefill FCFS on the new GPU   c_i = max(c_{i-1}, a_i) + t1[p_i]
 //            (TTFT_i = c_i - a_i; R8-R10)
 //   stage 2  DPD KV link (R11) / DSD handoff + draft prefill (R12):
 //                                           r_i = max(r_{i-1}, c_i) + t2[p_i]  (o_i > 1)
 //
-// t1/t2 are staged in shared memory by TMA bulk copies (cp.async.bulk + mbarrier).
-// Each 128-request chunk is read with 128-bit loads (4 requests per lane), both
-// stages are warp scans on (A, B) max-plus pairs with carries across chunks, TTFT
-// rows (and the finish of o = 1 requests, R13) are written, and requests with
-// o > 1 are compacted into the decode stream (r, demand, request index) in HBM for
-// k_decode.  The stage busy/energy sums, token count and status bits go to the
-// chain's gl_chain_stats; k_decode and k_finalize add the rest.
+// Both stages are max-plus recurrences: element i is the map x -> max(x + A_i, B_i)
+// (A = s_i, B = a_i + s_i, resp. c_i + s_i) and a prefix is the composition
+// (A, B) o (A', B') = (A + A', max(B + A', B')).  One block of ST_WARPS warps per
+// chain; warp w owns a contiguous run of 128-request chunks:
+//   pass 1  aggregate of stage 1 over the run, decode count, stage sums, status
+//   pass 2  carry-in = composition of the previous runs' aggregates -> c_i, and
+//           the stage-2 aggregate of the run
+//   pass 3  both carries -> c_i, r_i: TTFT rows (and the finish of o = 1 requests,
+//           R13), and the compacted decode stream (r, demand, request index) in
+//           HBM for k_decode, at the run's offset from the decode-count prefix.
+// Within a chunk each lane holds 4 consecutive requests (128-bit loads) and the
+// warp scans (A, B) pairs with shuffles.  The prompt-indexed t1/t2 tables are
+// staged in shared memory by TMA bulk copies (cp.async.bulk + mbarrier).
 #pragma once
 
 #include "common.cuh"
 
 namespace gl {
 
-__global__ void __launch_bounds__(32, 1)
+constexpr int ST_WARPS = 16;
+
+struct MP {  // max-plus map x -> max(x + A, B)
+    int64_t A, B;
+};
+__device__ __forceinline__ MP mp_then(const MP &f, const MP &g)  // g o f (f first)
+{
+    return MP{f.A + g.A, max(f.B + g.A, g.B)};
+}
+
+struct ChunkIn {
+    int64_t av[4];
+    uint32_t pc[4], oc[4], kv[4];
+    bool valid[4], dec[4];
+    int64_t s1[4], s2[4], xa[4];
+};
+
+__device__ __forceinline__ void load_chunk(const DChain &ch, const int32_t *t1s, const int32_t *t2s,
+                                           int32_t i0, int32_t n, int P, bool dsd, ChunkIn &c,
+                                           uint32_t &status)
+{
+    uint32_t pv[4], ov[4];
+    if (i0 + 3 < n) {  // 128-bit loads: 2 x (2 x int64) + (4 x u32) per stream
+        const longlong2 x0 = __ldg(reinterpret_cast<const longlong2 *>(ch.a + i0));
+        const longlong2 x1 = __ldg(reinterpret_cast<const longlong2 *>(ch.a + i0) + 1);
+        const uint4 pp = __ldg(reinterpret_cast<const uint4 *>(ch.p + i0));
+        const uint4 oo = __ldg(reinterpret_cast<const uint4 *>(ch.o + i0));
+        c.av[0] = x0.x; c.av[1] = x0.y; c.av[2] = x1.x; c.av[3] = x1.y;
+        pv[0] = pp.x; pv[1] = pp.y; pv[2] = pp.z; pv[3] = pp.w;
+        ov[0] = oo.x; ov[1] = oo.y; ov[2] = oo.z; ov[3] = oo.w;
+        if (dsd) {
+            const uint4 kk = __ldg(reinterpret_cast<const uint4 *>(ch.K + i0));
+            c.kv[0] = kk.x; c.kv[1] = kk.y; c.kv[2] = kk.z; c.kv[3] = kk.w;
+        } else {
+            c.kv[0] = c.kv[1] = c.kv[2] = c.kv[3] = 0;
+        }
+    } else {
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const bool v = i0 + q < n;
+            c.av[q] = v ? __ldg(ch.a + i0 + q) : 0;
+            pv[q] = v ? __ldg(ch.p + i0 + q) : 1;
+            ov[q] = v ? __ldg(ch.o + i0 + q) : 1;
+            c.kv[q] = (v && dsd) ? __ldg(ch.K + i0 + q) : 0;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        c.valid[q] = i0 + q < n;
+        uint32_t p = pv[q], o = ov[q];
+        if (c.valid[q]) {
+            if (c.av[q] < 0) status |= GL_ST_NEG_ARRIVAL;
+            if (p < 1 || p > (uint32_t)P) status |= GL_ST_PROMPT_RANGE;
+            if (o == 0) status |= GL_ST_OUTPUT_ZERO;
+            if (o >= O_LIMIT) status |= GL_ST_OVERFLOW;
+        }
+        p = min(max(p, 1u), (uint32_t)P);
+        o = min(max(o, 1u), O_LIMIT - 1);
+        c.pc[q] = p;
+        c.oc[q] = o;
+        c.dec[q] = c.valid[q] && o > 1;
+        c.s1[q] = c.valid[q] ? t1s[p] : 0;
+        c.s2[q] = c.dec[q] ? t2s[p] : 0;
+        c.xa[q] = c.valid[q] ? c.av[q] : NEG_INF;
+    }
+}
+
+// inclusive warp scan of per-lane maps (lane order = request order)
+__device__ __forceinline__ MP warp_scan_mp(MP f, int lane)
+{
+#pragma unroll
+    for (int off = 1; off < 32; off <<= 1) {
+        const int64_t Ap = shfl_up_i64(f.A, off), Bp = shfl_up_i64(f.B, off);
+        if (lane >= off) f = mp_then(MP{Ap, Bp}, f);
+    }
+    return f;
+}
+
+// stage-1 values of a chunk given the carry c_prev; returns the new carry
+__device__ __forceinline__ int64_t chunk_stage1(const ChunkIn &c, int64_t carry, int lane,
+                                                int64_t (&cv)[4])
+{
+    MP f{0, NEG_INF};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f = mp_then(f, MP{c.s1[q], c.xa[q] + c.s1[q]});
+    const MP inc = warp_scan_mp(f, lane);
+    int64_t Ax = shfl_up_i64(inc.A, 1), Bx = shfl_up_i64(inc.B, 1);
+    if (lane == 0) {
+        Ax = 0;
+        Bx = NEG_INF;
+    }
+    int64_t x = max(carry + Ax, Bx);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        x = max(x, c.xa[q]) + c.s1[q];
+        cv[q] = c.valid[q] ? x : NEG_INF;
+    }
+    return shfl_i64(x, 31);
+}
+
+// stage-2 values of a chunk given c and the carry r_prev; returns the new carry
+__device__ __forceinline__ int64_t chunk_stage2(const ChunkIn &c, const int64_t (&cv)[4],
+                                                int64_t carry, int lane, int64_t (&rv)[4])
+{
+    MP f{0, NEG_INF};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f = mp_then(f, MP{c.s2[q], cv[q] + c.s2[q]});
+    const MP inc = warp_scan_mp(f, lane);
+    int64_t Ax = shfl_up_i64(inc.A, 1), Bx = shfl_up_i64(inc.B, 1);
+    if (lane == 0) {
+        Ax = 0;
+        Bx = NEG_INF;
+    }
+    int64_t y = max(carry + Ax, Bx);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+        y = max(y, cv[q]) + c.s2[q];
+        rv[q] = y;
+    }
+    return shfl_i64(y, 31);
+}
+
+// aggregate map of a chunk's elements (lane 31's inclusive scan, broadcast)
+__device__ __forceinline__ MP chunk_aggregate(const int64_t (&s)[4], const int64_t (&b)[4], int lane)
+{
+    MP f{0, NEG_INF};
+#pragma unroll
+    for (int q = 0; q < 4; ++q) f = mp_then(f, MP{s[q], b[q] + s[q]});
+    const MP inc = warp_scan_mp(f, lane);
+    return MP{shfl_i64(inc.A, 31), shfl_i64(inc.B, 31)};
+}
+
+__global__ void __launch_bounds__(32 * ST_WARPS, 1)
     k_stages(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
              int64_t *__restrict__ perreq)
 {
     extern __shared__ __align__(16) unsigned char smem[];
-    const int lane = threadIdx.x;
+    __shared__ int64_t agg_A[ST_WARPS], agg_B[ST_WARPS];
+    __shared__ int32_t dcount[ST_WARPS];
+    __shared__ int64_t red[6][ST_WARPS];
+    __shared__ uint32_t red_status[ST_WARPS];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const DChain ch = chains[blockIdx.x];
     const int P = ch.max_prompt, cap = ch.cap;
     const int p1pad = round_up4(P + 1);
     int32_t *t1s = reinterpret_cast<int32_t *>(smem);
     int32_t *t2s = t1s + p1pad;
-    uint64_t *bar = reinterpret_cast<uint64_t *>(t2s + p1pad + ((p1pad & 1) ? 1 : 0));
+    uint64_t *bar = reinterpret_cast<uint64_t *>(t2s + p1pad);
     int64_t *out = perreq + 2 * ch.out_off;
 
     // ---- S0: stage the prompt-indexed tables (TMA bulk copies + mbarrier) -----
-    if (lane == 0) mbar_init(bar, 1);
-    __syncwarp();
-    uint32_t tx = stage_table(t1s, ch.t1, P + 1, bar, lane);
-    tx += stage_table(t2s, ch.t2, P + 1, bar, lane);
-    if (lane == 0) mbar_arrive_expect_tx(bar, tx);
-    mbar_wait(bar, 0);
-    __syncwarp();
+    if (warp == 0) {
+        if (lane == 0) mbar_init(bar, 1);
+        __syncwarp();
+        uint32_t tx = stage_table(t1s, ch.t1, P + 1, bar, lane);
+        tx += stage_table(t2s, ch.t2, P + 1, bar, lane);
+        if (lane == 0) mbar_arrive_expect_tx(bar, tx);
+        mbar_wait(bar, 0);
+    }
+    __syncthreads();
 
     uint32_t status = 0;
     {
         bool bad = false;
-        for (int i = 1 + lane; i <= P; i += 32) bad |= (t1s[i] < 0) | (t2s[i] < 0);
-        for (int b = 1 + lane; b <= cap; b += 32) bad |= __ldg(ch.step + b) < 1;
-        if (__any_sync(FULL, bad)) status |= GL_ST_TABLE;
+        for (int i = 1 + threadIdx.x; i <= P; i += blockDim.x) bad |= (t1s[i] < 0) | (t2s[i] < 0);
+        for (int b = 1 + threadIdx.x; b <= cap; b += blockDim.x) bad |= __ldg(ch.step + b) < 1;
+        if (__syncthreads_or(bad)) status |= GL_ST_TABLE;
     }
+    const bool skip = status & GL_ST_TABLE;
 
-    int64_t acc_busy_new = 0, acc_busy_old = 0, acc_e_new = 0, acc_e_old = 0, acc_tokens = 0;
-    int64_t acc_mk = 0;
     const int32_t n = (int32_t)ch.n;
     const bool dsd = ch.mode == GL_MODE_DSD;
-    int32_t produced = 0;
-    int64_t carry_c = NEG_INF, carry_r = NEG_INF, carry_a = INT64_MIN;
+    const int32_t nchunks = (n + CHUNK - 1) / CHUNK;
+    const int32_t per = (nchunks + ST_WARPS - 1) / ST_WARPS;
+    const int32_t c_lo = min(warp * per, nchunks), c_hi = min(c_lo + per, nchunks);
 
-    for (int32_t chunk = 0; chunk < n && !(status & GL_ST_TABLE); chunk += CHUNK) {
-        const int32_t i0 = chunk + 4 * lane;
-        int64_t av[4];
-        uint32_t pv[4], ov[4], kv[4];
-        if (i0 + 3 < n) {  // 128-bit loads: 2 x (2 x int64) + (4 x u32) per stream
-            const longlong2 x0 = __ldg(reinterpret_cast<const longlong2 *>(ch.a + i0));
-            const longlong2 x1 = __ldg(reinterpret_cast<const longlong2 *>(ch.a + i0) + 1);
-            const uint4 pp = __ldg(reinterpret_cast<const uint4 *>(ch.p + i0));
-            const uint4 oo = __ldg(reinterpret_cast<const uint4 *>(ch.o + i0));
-            av[0] = x0.x; av[1] = x0.y; av[2] = x1.x; av[3] = x1.y;
-            pv[0] = pp.x; pv[1] = pp.y; pv[2] = pp.z; pv[3] = pp.w;
-            ov[0] = oo.x; ov[1] = oo.y; ov[2] = oo.z; ov[3] = oo.w;
-            if (dsd) {
-                const uint4 kk = __ldg(reinterpret_cast<const uint4 *>(ch.K + i0));
-                kv[0] = kk.x; kv[1] = kk.y; kv[2] = kk.z; kv[3] = kk.w;
-            } else {
-                kv[0] = kv[1] = kv[2] = kv[3] = 0;
-            }
-        } else {
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                const bool v = i0 + q < n;
-                av[q] = v ? __ldg(ch.a + i0 + q) : 0;
-                pv[q] = v ? __ldg(ch.p + i0 + q) : 1;
-                ov[q] = v ? __ldg(ch.o + i0 + q) : 1;
-                kv[q] = (v && dsd) ? __ldg(ch.K + i0 + q) : 0;
-            }
-        }
-        bool valid[4], dec[4];
-        int64_t s1[4], s2[4], x_a[4];
+    // ---- pass 1: stage-1 aggregate, decode count, stage sums, status -----------
+    int64_t acc_busy_new = 0, acc_busy_old = 0, acc_e_new = 0, acc_e_old = 0, acc_tokens = 0;
+    MP agg1{0, NEG_INF};
+    int32_t ndec = 0;
+    int64_t carry_a = (c_lo > 0 && c_lo < nchunks) ? __ldg(ch.a + (int64_t)c_lo * CHUNK - 1) : INT64_MIN;
+    for (int32_t ck = c_lo; ck < c_hi && !skip; ++ck) {
+        ChunkIn c;
+        load_chunk(ch, t1s, t2s, ck * CHUNK + 4 * lane, n, P, dsd, c, status);
+        int cnt = 0;
 #pragma unroll
         for (int q = 0; q < 4; ++q) {
-            valid[q] = i0 + q < n;
-            uint32_t pc = pv[q], oc = ov[q];
-            if (valid[q]) {
-                if (av[q] < 0) status |= GL_ST_NEG_ARRIVAL;
-                if (pc < 1 || pc > (uint32_t)P) status |= GL_ST_PROMPT_RANGE;
-                if (oc == 0) status |= GL_ST_OUTPUT_ZERO;
-                if (oc >= O_LIMIT) status |= GL_ST_OVERFLOW;
+            if (c.valid[q]) {
+                acc_busy_new += c.s1[q];
+                acc_e_new += __ldg(ch.e1 + c.pc[q]);
+                acc_tokens += c.oc[q];
             }
-            pc = min(max(pc, 1u), (uint32_t)P);
-            oc = min(max(oc, 1u), O_LIMIT - 1);
-            ov[q] = oc;
-            dec[q] = valid[q] && oc > 1;
-            s1[q] = valid[q] ? t1s[pc] : 0;
-            s2[q] = dec[q] ? t2s[pc] : 0;
-            x_a[q] = valid[q] ? av[q] : NEG_INF;
-            if (valid[q]) {
-                acc_busy_new += s1[q];
-                acc_e_new += __ldg(ch.e1 + pc);
-                acc_tokens += oc;
-            }
-            if (dec[q]) {
-                acc_busy_old += __ldg(ch.b2 + pc);
-                acc_e_old += __ldg(ch.e2 + pc);
+            if (c.dec[q]) {
+                acc_busy_old += __ldg(ch.b2 + c.pc[q]);
+                acc_e_old += __ldg(ch.e2 + c.pc[q]);
+                ++cnt;
             }
         }
-        {  // sortedness across the lane boundary and the chunk boundary
-            int64_t prev = shfl_up_i64(av[3], 1);
+        {  // sortedness across the lane boundary and the chunk / run boundary
+            int64_t prev = shfl_up_i64(c.av[3], 1);
             if (lane == 0) prev = carry_a;
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                if (valid[q] && av[q] < prev) status |= GL_ST_UNSORTED;
-                if (valid[q]) prev = av[q];
+                if (c.valid[q] && c.av[q] < prev) status |= GL_ST_UNSORTED;
+                if (c.valid[q]) prev = c.av[q];
             }
             carry_a = shfl_i64(prev, 31);
         }
-        // S3: prefill FCFS max-plus scan, element = (A = s1, B = a + s1)
-        int64_t c[4];
-        {
-            int64_t A = 0, B = NEG_INF;
+        agg1 = mp_then(agg1, chunk_aggregate(c.s1, c.xa, lane));
+        ndec += __reduce_add_sync(FULL, (unsigned)cnt);
+    }
+    if (lane == 0) {
+        agg_A[warp] = agg1.A;
+        agg_B[warp] = agg1.B;
+        dcount[warp] = ndec;
+    }
+    __syncthreads();
+    int64_t carry_c = NEG_INF;  // = B of the composition of the previous runs
+    int32_t dbase = 0;
+    for (int w = 0; w < warp; ++w) {
+        carry_c = max(carry_c + agg_A[w], agg_B[w]);
+        dbase += dcount[w];
+    }
+    int32_t M = 0;
+    for (int w = 0; w < ST_WARPS; ++w) M += dcount[w];
+    __syncthreads();
+
+    // ---- pass 2: c with the true carry, stage-2 aggregate ---------------------
+    MP agg2{0, NEG_INF};
+    {
+        int64_t cc = carry_c;
+        for (int32_t ck = c_lo; ck < c_hi && !skip; ++ck) {
+            ChunkIn c;
+            uint32_t dummy = 0;
+            load_chunk(ch, t1s, t2s, ck * CHUNK + 4 * lane, n, P, dsd, c, dummy);
+            int64_t cv[4];
+            cc = chunk_stage1(c, cc, lane, cv);
+            agg2 = mp_then(agg2, chunk_aggregate(c.s2, cv, lane));
+        }
+    }
+    if (lane == 0) {
+        agg_A[warp] = agg2.A;
+        agg_B[warp] = agg2.B;
+    }
+    __syncthreads();
+    int64_t carry_r = NEG_INF;
+    for (int w = 0; w < warp; ++w) carry_r = max(carry_r + agg_A[w], agg_B[w]);
+
+    // ---- pass 3: c, r -> rows and the compacted decode stream -----------------
+    int64_t acc_mk = 0;
+    {
+        int64_t cc = carry_c, rr = carry_r;
+        int32_t produced = dbase;
+        for (int32_t ck = c_lo; ck < c_hi && !skip; ++ck) {
+            ChunkIn c;
+            uint32_t dummy = 0;
+            const int32_t i0 = ck * CHUNK + 4 * lane;
+            load_chunk(ch, t1s, t2s, i0, n, P, dsd, c, dummy);
+            int64_t cv[4], rv[4];
+            cc = chunk_stage1(c, cc, lane, cv);
+            rr = chunk_stage2(c, cv, rr, lane, rv);
+            int cnt = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cnt += c.dec[q] ? 1 : 0;
+            const unsigned b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),
+                           b2 = __ballot_sync(FULL, cnt & 4);
+            const unsigned lt = (1u << lane) - 1u;
+            int pos = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
+            const int total = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
-                A += s1[q];
-                B = max(B + s1[q], x_a[q] + s1[q]);
-            }
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int64_t Ap = shfl_up_i64(A, off), Bp = shfl_up_i64(B, off);
-                if (lane >= off) {
-                    B = max(Bp + A, B);
-                    A = Ap + A;
+                if (!c.valid[q]) continue;
+                const int32_t j = i0 + q;
+                if (!c.dec[q]) {
+                    *reinterpret_cast<longlong2 *>(out + 2 * (int64_t)j) =
+                        make_longlong2(cv[q] - c.av[q], cv[q]);
+                    acc_mk = max(acc_mk, cv[q]);
+                } else {
+                    out[2 * (int64_t)j] = cv[q] - c.av[q];
+                    const int64_t e = (int64_t)produced + pos;
+                    ch.dec_r[e] = rv[q];
+                    ch.dec_dj[e] = make_uint2(dsd ? c.kv[q] : c.oc[q] - 1, (uint32_t)j);
+                    ++pos;
                 }
             }
-            int64_t Ax = shfl_up_i64(A, 1), Bx = shfl_up_i64(B, 1);
-            if (lane == 0) {
-                Ax = 0;
-                Bx = NEG_INF;
-            }
-            int64_t x = max(carry_c + Ax, Bx);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                x = max(x, x_a[q]) + s1[q];
-                c[q] = valid[q] ? x : NEG_INF;
-            }
-            carry_c = shfl_i64(x, 31);
+            produced += total;
         }
-        // S4: stage-2 FIFO max-plus scan, element = (A = s2, B = c + s2)
-        int64_t r[4];
-        {
-            int64_t A = 0, B = NEG_INF;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                A += s2[q];
-                B = max(B + s2[q], c[q] + s2[q]);
-            }
-#pragma unroll
-            for (int off = 1; off < 32; off <<= 1) {
-                const int64_t Ap = shfl_up_i64(A, off), Bp = shfl_up_i64(B, off);
-                if (lane >= off) {
-                    B = max(Bp + A, B);
-                    A = Ap + A;
-                }
-            }
-            int64_t Ax = shfl_up_i64(A, 1), Bx = shfl_up_i64(B, 1);
-            if (lane == 0) {
-                Ax = 0;
-                Bx = NEG_INF;
-            }
-            int64_t y = max(carry_r + Ax, Bx);
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                y = max(y, c[q]) + s2[q];
-                r[q] = y;
-            }
-            carry_r = shfl_i64(y, 31);
-        }
-        // per request: TTFT row; o = 1 finishes at c (R13); others -> decode stream
-        int cnt = 0;
-#pragma unroll
-        for (int q = 0; q < 4; ++q) cnt += dec[q] ? 1 : 0;
-        const unsigned b0 = __ballot_sync(FULL, cnt & 1), b1 = __ballot_sync(FULL, cnt & 2),
-                       b2 = __ballot_sync(FULL, cnt & 4);
-        const unsigned lt = (1u << lane) - 1u;
-        int pos = __popc(b0 & lt) + 2 * __popc(b1 & lt) + 4 * __popc(b2 & lt);
-        const int total = __popc(b0) + 2 * __popc(b1) + 4 * __popc(b2);
-#pragma unroll
-        for (int q = 0; q < 4; ++q) {
-            if (!valid[q]) continue;
-            const int32_t j = i0 + q;
-            if (!dec[q]) {
-                *reinterpret_cast<longlong2 *>(out + 2 * (int64_t)j) =
-                    make_longlong2(c[q] - av[q], c[q]);
-                acc_mk = max(acc_mk, c[q]);
-            } else {
-                out[2 * (int64_t)j] = c[q] - av[q];
-                const int64_t e = (int64_t)produced + pos;
-                ch.dec_r[e] = r[q];
-                ch.dec_dj[e] = make_uint2(dsd ? kv[q] : ov[q] - 1, (uint32_t)j);
-                ++pos;
-            }
-        }
-        produced += total;
     }
-    // two sentinels after the last decode request read as "no request"
-    if (lane < 2) {
-        ch.dec_r[(int64_t)produced + lane] = INT64_MAX;
-        ch.dec_dj[(int64_t)produced + lane] = make_uint2(0u, 0u);
-    }
-    const int64_t busy_new = warp_sum_i64(acc_busy_new), busy_old = warp_sum_i64(acc_busy_old);
-    const int64_t e_new = warp_sum_i64(acc_e_new), e_old = warp_sum_i64(acc_e_old);
-    const int64_t tokens = warp_sum_i64(acc_tokens);
-    const int64_t mk = warp_max_i64(acc_mk);
+
+    // ---- block reductions and the chain's partial statistics ---------------------
+    const int64_t v[6] = {warp_sum_i64(acc_busy_new), warp_sum_i64(acc_busy_old),
+                          warp_sum_i64(acc_e_new), warp_sum_i64(acc_e_old),
+                          warp_sum_i64(acc_tokens), warp_max_i64(acc_mk)};
     status = __reduce_or_sync(FULL, status);
     if (lane == 0) {
+        for (int i = 0; i < 6; ++i) red[i][warp] = v[i];
+        red_status[warp] = status;
+    }
+    __syncthreads();
+    if (threadIdx.x < 2) {  // two sentinels after the last decode request
+        ch.dec_r[(int64_t)M + threadIdx.x] = INT64_MAX;
+        ch.dec_dj[(int64_t)M + threadIdx.x] = make_uint2(0u, 0u);
+    }
+    if (threadIdx.x == 0) {
+        int64_t s[6] = {0, 0, 0, 0, 0, 0};
+        uint32_t st = 0;
+        for (int w = 0; w < ST_WARPS; ++w) {
+            for (int i = 0; i < 5; ++i) s[i] += red[i][w];
+            s[5] = max(s[5], red[5][w]);
+            st |= red_status[w];
+        }
         gl_chain_stats o;
         o.n = ch.n;
         o.slo_ok = 0;
-        o.tokens = tokens;
-        o.busy_new_us = busy_new;
-        o.busy_old_us = busy_old;
-        o.e_new_uj = e_new;
-        o.e_old_uj = e_old;
-        o.makespan_us = mk;
+        o.tokens = s[4];
+        o.busy_new_us = s[0];
+        o.busy_old_us = s[1];
+        o.e_new_uj = s[2];
+        o.e_old_uj = s[3];
+        o.makespan_us = s[5];
         o.req_hash = 0;
-        o.status = status;
+        o.status = st;
         o.capacity_ok = (uint32_t)ch.capacity_ok;
         stats[blockIdx.x] = o;
-        ch.x->M = produced;
+        ch.x->M = skip ? 0 : M;
     }
 }
 
@@ -243,15 +357,16 @@ __global__ void __launch_bounds__(32, 1)
 // requests contributes the request with the largest gap r_q - r_{q-1} in it (ties:
 // the first), the request most likely to find the decode stage idle.  Any choice is
 // exact -- k_decode verifies every boundary -- this one just makes most of them
-// true idle points on lightly loaded chains.  One warp per chain.
-__global__ void __launch_bounds__(32)
+// true idle points on lightly loaded chains.  One block per chain, one warp per
+// window.
+__global__ void __launch_bounds__(256)
     k_segments(const DChain *__restrict__ chains)
 {
-    const int lane = threadIdx.x;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const DChain &ch = chains[blockIdx.x];
     const int32_t M = ch.x->M;
     const int32_t nseg = M > 0 ? (M + SEG_LEN - 1) / SEG_LEN : 0;
-    for (int32_t w = 1; w < nseg; ++w) {
+    for (int32_t w = 1 + warp; w < nseg; w += nw) {
         const int32_t lo = w * SEG_LEN, hi = min(lo + SEG_LEN, M);
         int64_t best_gap = -1;
         int32_t best_q = hi;
@@ -273,7 +388,7 @@ __global__ void __launch_bounds__(32)
         }
         if (lane == 0) ch.seg_start[w] = best_q;
     }
-    if (lane == 0) {
+    if (threadIdx.x == 0) {
         ch.seg_start[0] = 0;
         ch.seg_start[nseg] = M;
         ch.x->nseg = nseg;
