@@ -3,7 +3,7 @@
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
 
 One step = the whole hot path over the grid: gl_eval_grid on this rank's
-shard of timing chains (k_dsd_demand + k_chain), one NCCL all_gather of the
+shard of timing chains (k_dsd_demand, k_stages, k_segments, k_decode, k_finalize), one NCCL all_gather of the
 80-byte chain statistics (N > 1), gl_argmin_feasible (k_argmin) over all
 8,192 rows x 8 columns.  Inputs are resident in HBM; L2 is flushed (512 MiB
 write) between timed steps, outside the timed events.  Rank 0 prints one JSON
@@ -51,14 +51,28 @@ def dist_env():
     return rank, world, local
 
 
-def algorithmic_bytes(grid, lo, hi):
-    """16 B per (chain, request) (a i64 + p u32 + o u32) read by
-    k_chain, +4 B for the DSD demand K_j it also reads; tables amortise to ~0."""
-    tot = 0
+DECODE_BYTES_PER_REQUEST = 24  # k_decode: reads r (i64) + (demand, j) (2 x u32), writes the finish (i64)
+
+
+def decode_requests(grid, lo, hi):
+    """Decode requests (o > 1) per chain of the shard: the units k_decode processes."""
+    import numpy as np
+    per_trace = {}
+    out = []
     for ch in grid.chains[lo:hi]:
-        n = grid.traces[ch.trace_idx].n
-        tot += n * (20 if ch.mode == 1 else 16)
-    return tot
+        if ch.trace_idx not in per_trace:
+            per_trace[ch.trace_idx] = int(np.count_nonzero(np.asarray(grid.traces[ch.trace_idx].output_len) > 1))
+        out.append(per_trace[ch.trace_idx])
+    return out
+
+
+def algorithmic_bytes(grid, lo, hi):
+    """Algorithmic bytes of one k_decode launch: 24 B per decode
+    request -- the decode stream k_stages wrote (r i64 + demand u32 + request index
+    u32) is read once and each finish time (i64) is written once.  The step-table
+    staging is O(cap) per chain and the speculation's scratch (helpers' finish times,
+    segment results) is not algorithmic."""
+    return DECODE_BYTES_PER_REQUEST * sum(decode_requests(grid, lo, hi))
 
 
 def shard_bounds(n_chains, world):
@@ -299,8 +313,8 @@ def run_ours(args):
     evals = grid.grid_points * reqs
     value = evals / (ms_per_step / 1e3)
     chain_req = dg.chain_n.sum() / (ms_per_step / 1e3)
-    kchain = kt.get("k_chain", [])
-    kchain_ms = sum(kchain) / max(1, len(kchain))
+    kdec = kt.get("k_decode", [])
+    kdec_ms = sum(kdec) / max(1, len(kdec))
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
@@ -308,9 +322,9 @@ def run_ours(args):
         pass
     hbm_peak = peaks.get("hbm_gbs", 6650.0)
     alg_bytes = algorithmic_bytes(grid, lo, hi)
-    achieved = alg_bytes / (kchain_ms / 1e3) / 1e9 if kchain_ms > 0 else 0.0
+    achieved = alg_bytes / (kdec_ms / 1e3) / 1e9 if kdec_ms > 0 else 0.0
     traffic = None
-    prof_path = os.path.join(ROOT, "profiles", "k_chain_dram_bytes.json")
+    prof_path = os.path.join(ROOT, "profiles", "k_decode_dram_bytes.json")
     if os.path.exists(prof_path):
         try:
             traffic = json.load(open(prof_path)).get("dram_bytes_per_launch")
@@ -326,6 +340,14 @@ def run_ours(args):
                          f"{cb['seconds']:.1f} s",
                "chain_request_sims_per_s": cb["chain_request_sims_per_s"]}
     clocks = sampler.summary(t_wall0, t_wall1)
+    # cycles per decode event on the critical path.  Every
+    # decode request is one join and one leave event; the launch lasts as long as
+    # its slowest chain, so this is an upper bound for that chain.
+    m_max = max(decode_requests(grid, lo, hi) or [0])
+    sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
+    latency = {"max_decode_requests_per_chain": m_max, "events_per_chain": 2 * m_max,
+               "cycles_per_event_bound": (kdec_ms * 1e-3 * sm_mhz * 1e6 / (2 * m_max)) if m_max
+               else None, "sm_mhz": sm_mhz}
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
@@ -341,10 +363,13 @@ def run_ours(args):
         "kernel_ms_per_step": step_total,
         "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
                      "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "k_chain", "algorithmic_bytes_per_launch": alg_bytes,
-                     "kernel_ms": kchain_ms,
-                     "note": "k_chain is bound by the dependent latency of each chain's serial "
-                             "decode event loop, not by HBM (DESIGN.md §5)"},
+                     "kernel": "k_decode", "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_per_unit": DECODE_BYTES_PER_REQUEST, "unit_name": "decode request",
+                     "kernel_ms": kdec_ms,
+                     "latency": latency,
+                     "note": "k_decode is bound by the dependent latency of the slowest chain's "
+                             "serial decode event loop (busy periods cannot be split exactly), "
+                             "not by HBM (DESIGN.md §5)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -1,6 +1,6 @@
 """Summarise ncu outputs from gpurun_out/ into profiles/ (committed evidence).
 
-usage: python scripts/summarize_profiles.py <round tag> <launches.csv> <k_chain.ncu-rep>
+usage: python scripts/summarize_profiles.py <round tag> <launches.csv> <kernel.ncu-rep> [kernel]
 """
 import csv
 import json
@@ -11,6 +11,7 @@ from collections import defaultdict
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 tag, launches, rep = sys.argv[1], sys.argv[2], sys.argv[3]
+kern = sys.argv[4] if len(sys.argv) > 4 else "k_decode"
 out_dir = os.path.join(ROOT, "profiles")
 
 # ---- launch list: per-kernel count, mean device time, share of the step
@@ -22,8 +23,7 @@ d = defaultdict(list)
 for r in rows[hdr + 1:]:
     if len(r) > vi:
         d[r[ki]].append(float(r[vi].replace(",", "")))
-ours = {k: v for k, v in d.items() if "gl::" in k or "k_chain" in k or "k_argmin" in k or
-        "k_finalize" in k or "k_dsd_demand" in k}
+ours = {k: v for k, v in d.items() if "gl::" in k}
 tot = sum(sum(v) for v in ours.values())
 lines = [f"# {tag}: ncu --metrics gpu__time_duration.sum --clock-control none (cold-cache, "
          f"serialised launches) of `python bench.py --steps 3 --warmup 3`", "",
@@ -38,7 +38,7 @@ if other:
                  ", ".join(f"{k.split('(')[0][:60]} x{len(v)}" for k, v in other.items()))
 open(os.path.join(out_dir, f"{tag}_launches.md"), "w").write("\n".join(lines) + "\n")
 
-# ---- full capture of k_chain
+# ---- full capture of the dominant kernel
 raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_output=True,
                      text=True).stdout
 rr = list(csv.reader(raw.splitlines()))
@@ -53,7 +53,7 @@ m = {}
 for i, n in enumerate(names):
     if n in want or n.startswith("smsp__pcsamp_warps_issue_stalled_"):
         m[n] = (vals[i], units[i])
-lines = [f"# {tag}: `ncu --set full --clock-control none --import-source on -k regex:k_chain` "
+lines = [f"# {tag}: `ncu --set full --clock-control none --import-source on -k regex:{kern}` "
          "on `python bench.py --steps 1 --warmup 3` (config 4, 64 chains x 100k requests)", ""]
 for n in want:
     if n in m:
@@ -67,7 +67,7 @@ for n, v in sorted(stalls.items(), key=lambda kv: -kv[1]):
     if v > 0:
         lines.append(f"- {n.replace('smsp__pcsamp_warps_issue_stalled_', '')}: {v:.0f} "
                      f"({100 * v / tot_s:.1f}%)")
-open(os.path.join(out_dir, f"{tag}_k_chain_ncu.md"), "w").write("\n".join(lines) + "\n")
+open(os.path.join(out_dir, f"{tag}_{kern}_ncu.md"), "w").write("\n".join(lines) + "\n")
 
 
 def num(n):
@@ -78,8 +78,8 @@ def num(n):
 
 
 dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
-json.dump({"round": tag, "kernel": "k_chain", "dram_bytes_per_launch": dram,
-           "source": f"profiles/{tag}_k_chain_ncu.md"},
-          open(os.path.join(out_dir, "k_chain_dram_bytes.json"), "w"), indent=1)
+json.dump({"round": tag, "kernel": kern, "dram_bytes_per_launch": dram,
+           "source": f"profiles/{tag}_{kern}_ncu.md"},
+          open(os.path.join(out_dir, f"{kern}_dram_bytes.json"), "w"), indent=1)
 print(open(os.path.join(out_dir, f"{tag}_launches.md")).read())
-print(open(os.path.join(out_dir, f"{tag}_k_chain_ncu.md")).read())
+print(open(os.path.join(out_dir, f"{tag}_{kern}_ncu.md")).read())
