@@ -19,8 +19,8 @@
 // changes how much of the chain one warp has to walk serially.
 //
 // Each run reads the decode stream (r, demand, request) from HBM through a
-// 256-entry shared-memory window refilled in 128-entry halves by TMA bulk copies
-// (cp.async.bulk + one mbarrier per half).  The loop never steps single
+// 256-entry shared-memory window refilled in 128-entry halves by asynchronous
+// 16-byte copies (cp.async, one commit group per half).  The loop never steps single
 // iterations: a member admitted at iteration I with demand d finishes at
 // F = I + d; the next event is min(REDUX-min F - I, the boundary where the head
 // becomes ready) and T += k * step[b].  For cap <= 31 (one member per lane) a

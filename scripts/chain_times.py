@@ -1,4 +1,4 @@
-"""Per-chain k_chain time of config 4 (one launch per chain)."""
+"""Per-chain k_decode time of config 4 (one launch per chain)."""
 import sys, json
 import numpy as np, torch
 sys.path.insert(0, '.')

@@ -1,4 +1,4 @@
-"""Launch k_chain on a subset of config-4 chains (for ncu)."""
+"""Launch the decode pipeline on a subset of config-4 chains (for ncu)."""
 import sys
 import torch
 sys.path.insert(0, '.')
