@@ -20,21 +20,24 @@ constexpr uint32_t F_EMPTY = 0xFFFFFFFFu;
 constexpr unsigned FULL = 0xFFFFFFFFu;
 constexpr uint32_t O_LIMIT = 1u << 30;
 
-constexpr int SEG_LEN = 256;  // decode requests per speculation window (k_segments)
+constexpr int SEG_LEN = 256;  // decode requests per candidate window (k_segments)
 
-// per-segment result of a helper warp's speculative run (k_decode)
+// per-candidate result of a speculative run (k_decode)
 struct DSegOut {
-    int64_t maxfin;   // last finish time of the segment's isolated run
+    int64_t maxfin;   // last finish time of the run
     int64_t sums[4];  // decode busy_new, busy_old, e_new, e_old of that run
-    int32_t done;     // 1 once published (release)
+    int32_t state;    // 0 unclaimed, 1 claimed, 2 published (release)
+    int32_t next;     // candidate index at which the run stopped (idle there)
+    int32_t helper;   // whose finish-time buffer holds the run
     int32_t pad;
 };
+constexpr int32_t SEG_FREE = 0, SEG_CLAIMED = 1, SEG_DONE = 2;
 
 // per-chain decode bookkeeping (stream-ordered scratch, zeroed by the host)
 struct DChainX {
     int32_t M;           // decode requests (o > 1), set by k_stages
-    int32_t nseg;        // segments, set by k_segments
-    int32_t leader_pos;  // first segment the leader has not yet passed (helpers skip below)
+    int32_t nseg;        // idle-point candidates, set by k_segments
+    int32_t leader_pos;  // candidate the leader is at (helpers skip and abort below)
     int32_t next_seg;    // helper work counter
 };
 
@@ -52,8 +55,9 @@ struct DChain {
     // per decode request q, in FCFS order, with two INT64_MAX sentinels after M
     int64_t *dec_r;
     uint2 *dec_dj;
-    int64_t *spec_fin;  // helpers' speculative finish times, indexed by q
-    int32_t *seg_start; // [nseg + 1] segment starts (q), seg_start[nseg] = M
+    int64_t *spec_fin;  // helper h's speculative finish times: spec_fin[h * spec_stride + q]
+    int64_t spec_stride;
+    int32_t *seg_start; // [nseg + 1] candidate starts (q), seg_start[nseg] = M
     DSegOut *seg_out;   // [nseg]
     DChainX *x;
     int64_t n;

@@ -16,7 +16,7 @@
  *   k_dsd_demand  (k_dsd_demand.cuh) one thread per (DSD demand group, request)
  *   k_stages      (k_stages.cuh)     one warp per chain: TMA-staged tables, 128-bit
  *                                    loads, max-plus warp scans -> decode stream
- *   k_segments    (k_stages.cuh)     speculation segment starts (largest gaps)
+ *   k_segments    (k_stages.cuh)     idle-point candidates for the decode speculation
  *   k_decode      (k_decode.cuh)     leader + helper warps per chain: exact
  *                                    speculative decode event loops
  *   k_finalize    (k_decode.cuh)     whole GPU over (chain, request): SLO, hash
@@ -202,7 +202,8 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     if (smem_st > (size_t)smem_optin || smem_dec > (size_t)smem_optin) return GL_E_UNSUPPORTED;
 
     // Stream-ordered scratch: [chains][groups][K arrays][per-request rows if not
-    // given][decode stream r, (d, j), spec_fin: n + 512 per chain][segment starts]
+    // given][decode stream r, (d, j): n + 512 per chain][helpers' finish-time
+    // buffers: helpers x (n + 512) per chain][candidates]
     // [segment results][per-chain bookkeeping].  The last two are zeroed.
     const size_t off_groups = align256(sizeof(DChain) * n_chains);
     size_t total = off_groups + align256(sizeof(DGroup) * groups.size());
@@ -226,8 +227,13 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     total += align256(sizeof(int64_t) * (size_t)dec_total);
     const size_t off_dec_dj = total;
     total += align256(sizeof(uint2) * (size_t)dec_total);
+    // k_decode: one leader warp per chain plus helper warps, about four warps per
+    // SM in total; each helper keeps its finish times in a buffer of its own
+    // (capped at 8 GiB of scratch)
+    int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
+    while (extra > 0 && (size_t)dec_total * extra * sizeof(int64_t) > ((size_t)8 << 30)) --extra;
     const size_t off_spec = total;
-    total += align256(sizeof(int64_t) * (size_t)dec_total);
+    total += align256(sizeof(int64_t) * (size_t)dec_total * (size_t)std::max(extra, 1));
     const size_t off_segs = total;
     total += align256(sizeof(int32_t) * (size_t)seg_total);
     const size_t off_zero = total;
@@ -265,7 +271,8 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
         d.seo = c.step_e_old_uj;
         d.dec_r = reinterpret_cast<int64_t *>(scratch + off_dec_r) + dec_off[i];
         d.dec_dj = reinterpret_cast<uint2 *>(scratch + off_dec_dj) + dec_off[i];
-        d.spec_fin = reinterpret_cast<int64_t *>(scratch + off_spec) + dec_off[i];
+        d.spec_fin = reinterpret_cast<int64_t *>(scratch + off_spec) + dec_off[i] * std::max(extra, 1);
+        d.spec_stride = (tr.n + 512 + 31) & ~(int64_t)31;
         d.seg_start = reinterpret_cast<int32_t *>(scratch + off_segs) + seg_off[i];
         d.seg_out = reinterpret_cast<gl::DSegOut *>(scratch + off_segout) + seg_off[i];
         d.x = reinterpret_cast<gl::DChainX *>(scratch + off_x) + i;
@@ -311,14 +318,12 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     }
     if (e == cudaSuccess) {
         prof_begin("k_segments", stream);
-        gl::k_segments<<<n_chains, 256, 0, stream>>>(dc);
+        gl::k_segments<<<n_chains, 1024, 0, stream>>>(dc);
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;
     }
     if (e == cudaSuccess) {
-        // one leader warp per chain plus helper warps: about four warps per SM
-        const int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
         const unsigned blocks = (unsigned)(n_chains * (1 + extra));
         auto launch = [&](auto kern) {
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,

@@ -4,19 +4,21 @@
 // The decode stage of one chain is a serial event chain.  It becomes parallel at
 // idle points: if every decode request before q has finished by r_q, the decode
 // stage is empty when q becomes ready, and the run from q onward depends only on
-// requests >= q (R17: an empty batch restarts exactly at r_q).  k_segments cut the
-// stream into segments at likely idle points; in k_decode
-//   * helper warps simulate segment k from an empty batch at r_{s_k}, using only
-//     its own requests, and publish (finish times, sums, last finish maxfin_k);
-//   * one leader warp per chain walks the segments in order.  Segment 0 starts
-//     idle.  When segment k starts idle (by induction) and its helper run ended no
-//     later than r_{s_{k+1}} (maxfin_k <= r_{s_{k+1}}), no later request can have
-//     joined it, so the helper run IS the true run and s_{k+1} starts idle: the
-//     leader accepts it.  Otherwise (result missing, or segment k overlaps the next
-//     one) the leader simulates from s_k itself and keeps going across segment
-//     starts until it reaches one with an empty batch -- again an idle point.
-// Results are bit-identical to a single sequential run; the speculation only
-// changes how much of the chain one warp has to walk serially.
+// requests >= q (R17: an empty batch restarts exactly at r_q).  k_segments picks
+// candidates that are almost always idle points; in k_decode every run starts from
+// an empty batch at a candidate and stops at the first later candidate where its
+// batch is empty.
+//   * Helper warps claim candidates in order and run them speculatively, keeping
+//     the finish times in a buffer of their own; they publish (next candidate,
+//     sums, last finish) and abort once the leader has moved past their start.
+//   * One leader warp per chain hops from idle point to idle point.  Candidate 0
+//     is one.  A run from an idle point is the true run, so the candidate where it
+//     stopped (empty batch) is the next idle point: the leader copies the run's
+//     finish times into the rows, adds its sums and moves there.  A candidate
+//     nobody has claimed it runs itself, straight into the rows; one a helper is
+//     running it waits for.
+// Results are bit-identical to a single sequential run; speculation only changes
+// how much of the chain one warp has to walk serially.
 //
 // Each run reads the decode stream (r, demand, request) from HBM through a
 // 256-entry shared-memory window refilled in 128-entry halves by asynchronous
@@ -112,7 +114,7 @@ struct RingW {
 struct RunOut {
     int64_t mk;       // last finish time of the run (0 if nothing finished)
     int64_t sums[4];  // decode busy_new, busy_old, e_new, e_old
-    int32_t stop_seg; // extend mode: segment index whose start the run stopped at
+    int32_t stop_seg; // candidate the run stopped at (idle there; nseg = end), -1 aborted
 };
 
 struct RunCtx {
@@ -120,22 +122,15 @@ struct RunCtx {
     const int32_t *steps;   // smem [cap+1]
     const uint64_t *magic;  // smem [cap+1] Lemire reciprocals of steps
     int64_t *rows_fin;      // &perreq[2*out_off + 1]: finish column of this chain
+    int64_t *spec;          // helpers: this helper's finish-time buffer, indexed by q
     int cap, lane;
     int32_t nseg;
+    int32_t hid;  // helper index (buffer), -1 for the leader
 };
 
 // kept out of line so the decode loops stay free of memory-ordering operations
 __device__ __noinline__ void publish_pos(bool p, int32_t *ptr, int32_t v) { st_relaxed_gpu_if(p, ptr, v); }
-
-// Segment k's helper result is published and clean: its isolated run ended no
-// later than the next segment's first ready time (always true for the last one).
-__device__ __noinline__ bool seg_clean(const DChain &ch, int32_t k, int32_t nseg)
-{
-    if (k >= nseg || !ld_acquire_gpu(&ch.seg_out[k].done)) return false;
-    const int64_t maxfin = __ldcg(&ch.seg_out[k].maxfin);
-    const int64_t r_next = k + 1 < nseg ? __ldcg(ch.dec_r + ch.seg_start[k + 1]) : INT64_MAX;
-    return maxfin <= r_next;
-}
+__device__ __noinline__ int32_t poll_pos(const int32_t *ptr) { return ld_relaxed_gpu(ptr); }
 
 // sums of iterations x batch-indexed tables, reduced over the warp
 template <int SPL>
@@ -160,25 +155,42 @@ __device__ __forceinline__ void run_sums(const RunCtx &cx, const uint64_t (&iter
     s[3] = warp_sum_i64(a3);
 }
 
-// One decode run from an empty batch at r_{q0}.  LEADER: finish times go to the
-// chain's (ttft, finish) rows, and the run continues across segment starts until
-// it meets one with an empty batch whose helper result is published and clean
-// (then it stops there and the leader accepts from that segment on).  Helper:
-// finish times go to spec_fin[q]; the run covers its segment only.
-template <int SPL, bool LEADER>
-__device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t k0)
+// One decode run from an empty batch at r_{q0} = r at candidate k0.  It continues
+// across later candidates until it reaches one with an empty batch (an idle point:
+// every earlier request finished by its ready time) and stops there.
+//   ROWS   finish times go to the chain's (ttft, finish) rows (the leader's own
+//          runs, whose start is a known idle point); the leader (pub) publishes
+//          the candidate it has passed.
+//   !ROWS  a helper's speculative run: finish times go to the helper's own buffer
+//          (indexed by q); the run aborts once the leader has moved past k0 (the
+//          result is then moot).
+template <int SPL, bool ROWS>
+__device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t k0, bool pub)
 {
-    constexpr bool to_rows = LEADER, extend = LEADER;
+    constexpr bool to_rows = ROWS;
     const DChain &ch = *cx.ch;
     const int lane = cx.lane, cap = cx.cap;
     // shared-memory tables re-derived from the symbol (keeps plain LDS addressing;
     // layout as set up by k_decode: windows, mbarriers, reciprocals, steps)
     extern __shared__ __align__(16) unsigned char dyn_smem[];
-    const uint64_t *const magic =
-        reinterpret_cast<const uint64_t *>(dyn_smem + DEC_WARPS * RING * 16) + 2 * DEC_WARPS + 2;
-    const int32_t *const steps = reinterpret_cast<const int32_t *>(magic + round_up4(cap + 1));
+    // Table bases as opaque 32-bit shared addresses: kept in registers (ptxas would
+    // otherwise rematerialise them from SR_CgaCtaId inside the loops) and read
+    // with ld.shared (LDS).
+    uint32_t magic_s = smem_u32(dyn_smem + DEC_WARPS * RING * 16 + (2 * DEC_WARPS + 2) * 8);
+    asm volatile("" : "+r"(magic_s));
+    const uint32_t steps_s = magic_s + 8u * (uint32_t)round_up4(cap + 1);
+    auto ld_step = [&](int bb) -> int32_t {
+        int32_t v;
+        asm("ld.shared.s32 %0, [%1];" : "=r"(v) : "r"(steps_s + 4u * (uint32_t)bb));
+        return v;
+    };
+    auto ld_magic = [&](int bb) -> uint64_t {
+        uint64_t v;
+        asm("ld.shared.u64 %0, [%1];" : "=l"(v) : "r"(magic_s + 8u * (uint32_t)bb));
+        return v;
+    };
     int64_t *const fin_rows = cx.rows_fin;
-    int64_t *const fin_spec = ch.spec_fin;
+    int64_t *const fin_spec = cx.spec;
     DChainX *const xx = ch.x;
     const unsigned lane_bit = 1u << lane;
 
@@ -193,10 +205,11 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
     int32_t nxt = q0;
     int64_t h_r = rr[nxt & RING_MASK], n_r = rr[(nxt + 1) & RING_MASK];
     uint2 h_dj = rdj[nxt & RING_MASK], n_dj = rdj[(nxt + 1) & RING_MASK];
-    // next segment start after k0 (extend mode), for stop checks and leader_pos
+    // next candidate after k0, for stop checks and leader_pos
     const int32_t nseg_r = cx.nseg;
     int32_t kb = k0 + 1;
-    int32_t nb = extend ? ch.seg_start[kb] : INT32_MAX;
+    int32_t nb = ch.seg_start[kb];
+    bool aborted = false;
 
     auto advance = [&]() {
         ++nxt;
@@ -205,9 +218,16 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
         // all ring maintenance happens where nxt + 1 crosses a 128-entry half
         if (__builtin_expect((uint32_t)((nxt + 1) & 127) <= 1u, 0)) {
             ring.advanced(nxt, lane);
-            if (extend && (nxt & 127) == 0) {  // publish the leader's progress
-                while (kb < nseg_r && nb <= nxt) nb = ch.seg_start[++kb];
-                publish_pos(lane == 0, &xx->leader_pos, kb - 1);
+            if ((nxt & 127) == 0) {
+                while (kb < nseg_r && nb < nxt) nb = ch.seg_start[++kb];
+                if (ROWS) {  // publish the leader's progress
+                    publish_pos(pub && lane == 0, &xx->leader_pos, kb - 1);
+                } else if (!aborted && __shfl_sync(FULL, poll_pos(&xx->leader_pos), 0) > k0) {
+                    // the leader is past this run's start: end the input at the next
+                    // half (its sentinels are written when that half is waited for)
+                    aborted = true;
+                    ring.q_end = min(ring.q_end, ring.ready_to);
+                }
             }
         }
         const int e1 = (nxt + 1) & RING_MASK;
@@ -233,28 +253,28 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
         int32_t st_d = 0, st_c = 0, st_u = 0;
         uint64_t M_d = 0, M_c = 0, M_u = 0;
         auto load_nbr = [&](int nbb) {
-            st_c = steps[nbb];
-            M_c = magic[nbb];
-            st_u = steps[min(nbb + 1, cap)];
-            M_u = magic[min(nbb + 1, cap)];
-            st_d = steps[max(nbb - 1, 0)];
-            M_d = magic[max(nbb - 1, 0)];
+            st_c = ld_step(nbb);
+            M_c = ld_magic(nbb);
+            st_u = ld_step(min(nbb + 1, cap));
+            M_u = ld_magic(min(nbb + 1, cap));
+            st_d = ld_step(max(nbb - 1, 0));
+            M_d = ld_magic(max(nbb - 1, 0));
         };
         auto shift_up = [&]() {
             st_d = st_c;
             M_d = M_c;
             st_c = st_u;
             M_c = M_u;
-            st_u = steps[min(b + 1, cap)];
-            M_u = magic[min(b + 1, cap)];
+            st_u = ld_step(min(b + 1, cap));
+            M_u = ld_magic(min(b + 1, cap));
         };
         auto shift_down = [&]() {
             st_u = st_c;
             M_u = M_c;
             st_c = st_d;
             M_c = M_d;
-            st_d = steps[max(b - 1, 0)];
-            M_d = magic[max(b - 1, 0)];
+            st_d = ld_step(max(b - 1, 0));
+            M_d = ld_magic(max(b - 1, 0));
         };
         load_nbr(0);
         for (;;) {
@@ -280,10 +300,13 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                 advance();
             }
             if (b == 0) {  // idle until the next decode request is ready (R17)
-                if (h_r == INT64_MAX) break;
-                if (extend && nxt >= nb) {  // reached (or passed) the next segment start
+                if (h_r == INT64_MAX) {
+                    res.stop_seg = aborted ? -1 : nseg_r;
+                    break;
+                }
+                if (nxt >= nb) {  // reached (or passed) the next candidate
                     while (kb < nseg_r && nb < nxt) nb = ch.seg_start[++kb];
-                    if (nb == nxt && seg_clean(ch, kb, nseg_r)) {  // idle point: hand over
+                    if (nb == nxt) {  // an idle point: stop here
                         res.stop_seg = kb;
                         break;
                     }
@@ -467,10 +490,13 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                 advance();
             }
             if (b == 0) {  // idle (R17)
-                if (h_r == INT64_MAX) break;
-                if (extend && nxt >= nb) {  // reached (or passed) the next segment start
+                if (h_r == INT64_MAX) {
+                    res.stop_seg = aborted ? -1 : nseg_r;
+                    break;
+                }
+                if (nxt >= nb) {  // reached (or passed) the next candidate
                     while (kb < nseg_r && nb < nxt) nb = ch.seg_start[++kb];
-                    if (nb == nxt && seg_clean(ch, kb, nseg_r)) {  // idle point: hand over
+                    if (nb == nxt) {  // an idle point: stop here
                         res.stop_seg = kb;
                         break;
                     }
@@ -478,11 +504,11 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                 T = h_r;
                 continue;
             }
-            const int64_t st = steps[b];
+            const int64_t st = ld_step(b);
             uint32_t kJ = 0xFFFFFFFFu;
             if (b < cap) {
                 const int64_t gap = h_r - T;
-                if (gap < 0x80000000ll) kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, magic[b]);
+                if (gap < 0x80000000ll) kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, ld_magic(b));
                 else if (h_r != INT64_MAX)
                     kJ = (uint32_t)min((gap + st - 1) / st, (int64_t)0xFFFFFFFF);
             }
@@ -523,28 +549,43 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
     return res;
 }
 
-// Helpers: speculative isolated runs of segments ahead of the leader.  Out of
-// line so the kernel body holds a single (the leader's) copy of the decode loops.
+__device__ __forceinline__ void backoff() { __nanosleep(64); }
+
+// Helpers: speculative runs from the candidates ahead of the leader.  Out of line
+// so the kernel body holds a single (the leader's) copy of the decode loops.
+// A helper's runs write disjoint stretches of its buffer: it skips candidates
+// inside its previous run (if that run was the true one they are not idle points;
+// if not, the leader runs them itself).
 template <int SPL>
-__device__ __noinline__ void helper_loop(const RunCtx &cx, RingW &ring)
+__device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
 {
     const DChain &ch = *cx.ch;
     const int lane = cx.lane;
     const int32_t nseg = cx.nseg;
+    int32_t k_end = 0;  // candidate where this helper's previous run stopped
     for (;;) {
         int32_t k = 0;
-        if (lane == 0) k = atomicAdd(&ch.x->next_seg, 1);
+        if (lane == 0) {
+            k = atomicAdd(&ch.x->next_seg, 1);
+            if (k < nseg && (k < k_end || k <= ld_relaxed_gpu(&ch.x->leader_pos) ||
+                             atomicCAS(&ch.seg_out[k].state, SEG_FREE, SEG_CLAIMED) != SEG_FREE))
+                k = -1;  // inside our last run, or the leader is there (or took it)
+        }
         k = __shfl_sync(FULL, k, 0);
         if (k >= nseg) break;
-        if (k <= ld_relaxed_gpu(&ch.x->leader_pos)) continue;  // the leader is there
-        ring.q_end = ch.seg_start[k + 1];
-        const RunOut ro = decode_run<SPL, false>(cx, ring, ch.seg_start[k], k);
+        if (k < 0) continue;
+        ring.q_end = ch.x->M;
+        const RunOut ro = decode_run<SPL, false>(cx, ring, ch.seg_start[k], k, false);
+        if (ro.stop_seg < 0) continue;  // aborted: the leader passed k (moot values)
+        k_end = ro.stop_seg;
         if (lane == 0) {
             DSegOut &so = ch.seg_out[k];
             so.maxfin = ro.mk;
             for (int i = 0; i < 4; ++i) so.sums[i] = ro.sums[i];
+            so.next = ro.stop_seg;
+            so.helper = cx.hid;
             __threadfence();
-            st_release_gpu(&so.done, 1);
+            st_release_gpu(&so.state, SEG_DONE);
         }
     }
 }
@@ -571,12 +612,8 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     uint64_t *magic = bars + 2 * DEC_WARPS + 2;
     int32_t *steps = reinterpret_cast<int32_t *>(magic + cappad);
 
-    // S0: batch-indexed step table by TMA (warp 0), reciprocals, ring barriers
+    // S0: batch-indexed step table by TMA (warp 0), reciprocals
     if (threadIdx.x == 0) mbar_init(bars + 2 * DEC_WARPS, 1);
-    if (lane == 0) {
-        mbar_init(bars + 2 * warp, 1);
-        mbar_init(bars + 2 * warp + 1, 1);
-    }
     __syncthreads();
     if (warp == 0) {
         const uint32_t tx = stage_table(steps, ch.step, cap + 1, bars + 2 * DEC_WARPS, lane);
@@ -591,7 +628,9 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     __syncthreads();
 
     const int32_t nseg = ch.x->nseg;
-    RunCtx cx{&ch, steps, magic, perreq + 2 * ch.out_off + 1, cap, lane, nseg};
+    const int32_t hid = leader ? -1 : (int32_t)(blockIdx.x / n_chains) - 1;
+    RunCtx cx{&ch, steps, magic, perreq + 2 * ch.out_off + 1,
+              ch.spec_fin + (int64_t)max(hid, 0) * ch.spec_stride, cap, lane, nseg, hid};
     RingW ring;
     ring.r = ring_r;
     ring.dj = ring_dj;
@@ -599,46 +638,75 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     ring.gdj = ch.dec_dj;
     ring.fill_next = ring.ready_to = 0;
 
-    if (leader) {
-        int64_t acc[4] = {0, 0, 0, 0};
-        int64_t mk = 0;
-        int32_t k = 0;
-        const int32_t M = ch.x->M;
-        while (k < nseg) {
-            if (k > 0 && seg_clean(ch, k, nseg)) {
-                // published before done (release); read through L2
-                const int64_t so_maxfin = __ldcg(&ch.seg_out[k].maxfin);
-                const int32_t s_lo = ch.seg_start[k], s_hi = ch.seg_start[k + 1];
-                {  // clean: accept the helper's exact run
-                    for (int32_t q = s_lo + lane; q < s_hi; q += 32) {
-                        const uint32_t j = __ldcg(&ch.dec_dj[q].y);
-                        cx.rows_fin[2 * (int64_t)j] = __ldcg(ch.spec_fin + q);
-                    }
-                    for (int i = 0; i < 4; ++i) acc[i] += __ldcg(&ch.seg_out[k].sums[i]);
-                    mk = max(mk, so_maxfin);
-                    ++k;
-                    if (lane == 0) st_relaxed_gpu(&ch.x->leader_pos, k);
-                    continue;
-                }
+    if (!leader) {
+        helper_loop<SPL>(cx, ring);
+        return;
+    }
+    // The leader hops from idle point to idle point: candidate 0 is one, and a run
+    // from an idle point is the true run, so where it stops is the next one.
+    int64_t acc[4] = {0, 0, 0, 0};
+    int64_t mk = 0;
+    int32_t k = 0;
+    const int32_t M = ch.x->M;
+    while (k < nseg) {
+        if (lane == 0) st_relaxed_gpu(&ch.x->leader_pos, k);
+        int32_t st = 0;
+        if (lane == 0) {
+            st = ld_acquire_gpu(&ch.seg_out[k].state);
+            if (st == SEG_FREE) {
+                st = atomicCAS(&ch.seg_out[k].state, SEG_FREE, SEG_CLAIMED);
+                if (st == SEG_FREE) st = -1;  // ours now
             }
-            // simulate from s_k (an idle point) until the next idle segment start
+        }
+        st = __shfl_sync(FULL, st, 0);
+        if (st < 0) {  // nobody has run k: simulate it here, into the rows
             ring.q_end = M;
-            const RunOut ro = decode_run<SPL, true>(cx, ring, ch.seg_start[k], k);
+            const RunOut ro = decode_run<SPL, true>(cx, ring, ch.seg_start[k], k, true);
             for (int i = 0; i < 4; ++i) acc[i] += ro.sums[i];
             mk = max(mk, ro.mk);
-            k = ro.stop_seg >= 0 ? ro.stop_seg : nseg;
-            if (lane == 0) st_relaxed_gpu(&ch.x->leader_pos, k);
+            k = ro.stop_seg;
+            continue;
         }
-        if (lane == 0) {
-            gl_chain_stats &s = stats[c];
-            s.busy_new_us += acc[0];
-            s.busy_old_us += acc[1];
-            s.e_new_uj += acc[2];
-            s.e_old_uj += acc[3];
-            s.makespan_us = max(s.makespan_us, mk);
+        if (st != SEG_DONE) {  // a helper is running k: wait for it
+            int32_t d = 0;
+            do {
+                if (lane == 0) d = ld_acquire_gpu(&ch.seg_out[k].state) == SEG_DONE;
+                d = __shfl_sync(FULL, d, 0);
+            } while (!d);
         }
-    } else {
-        helper_loop<SPL>(cx, ring);
+        const DSegOut &so = ch.seg_out[k];
+        const int32_t m = __ldcg(&so.next);
+        for (int i = 0; i < 4; ++i) acc[i] += __ldcg(&so.sums[i]);
+        mk = max(mk, __ldcg(&so.maxfin));
+        {  // copy the run's finish times from the helper's buffer into the rows
+            const int64_t *src = ch.spec_fin + (int64_t)__ldcg(&so.helper) * ch.spec_stride;
+            const int32_t s_lo = ch.seg_start[k], s_hi = ch.seg_start[m];
+            for (int32_t q0 = s_lo; q0 < s_hi; q0 += 128) {
+                int64_t f[4];
+                uint32_t j[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int32_t q = q0 + 32 * u + lane;
+                    if (q < s_hi) {
+                        f[u] = __ldcg(src + q);
+                        j[u] = __ldcg(&ch.dec_dj[q].y);
+                    }
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u)
+                    if (q0 + 32 * u + lane < s_hi) cx.rows_fin[2 * (int64_t)j[u]] = f[u];
+            }
+        }
+        k = m;
+    }
+    if (lane == 0) {
+        st_release_gpu(&ch.x->leader_pos, nseg);
+        gl_chain_stats &s = stats[c];
+        s.busy_new_us += acc[0];
+        s.busy_old_us += acc[1];
+        s.e_new_uj += acc[2];
+        s.e_old_uj += acc[3];
+        s.makespan_us = max(s.makespan_us, mk);
     }
 }
 

@@ -353,45 +353,125 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     }
 }
 
-// Segment starts for the decode speculation: window w >= 1 of SEG_LEN decode
-// requests contributes the request with the largest gap r_q - r_{q-1} in it (ties:
-// the first), the request most likely to find the decode stage idle.  Any choice is
-// exact -- k_decode verifies every boundary -- this one just makes most of them
-// true idle points on lightly loaded chains.  One block per chain, one warp per
-// window.
-__global__ void __launch_bounds__(256)
+// Idle-point candidates for the decode speculation.  Request q can only find the
+// decode stage empty if every earlier request has finished by r_q, and request q'
+// cannot finish before r_q' + d_q' * step_min (it joins at or after r_q' and runs
+// d_q' iterations of at least step_min = min_b step[b]).  So
+//     slack_q = r_q - max_{q' < q} (r_q' + d_q' step_min) < 0
+// proves q busy; the candidates are request 0 and, per window of SEG_LEN decode
+// requests, the request with the largest slack if it is >= 0 (ties: the first).
+// Any choice is exact -- k_decode verifies every candidate it uses -- this one
+// makes almost all candidates true idle points (SEG_LEN bounds how many there are).
+// One 1024-thread block per chain; windows are processed in rounds of SEG_ROUND:
+//   pass 1  warp per window: max of the lower bounds          -> smem
+//   scan    exclusive prefix max over windows (carry across rounds)
+//   pass 2  warp per window: in-window prefix max (8 warp scans), best slack
+//   compact candidate flags -> seg_start[]
+constexpr int SEG_ROUND = 1024;
+
+__global__ void __launch_bounds__(1024)
     k_segments(const DChain *__restrict__ chains)
 {
+    __shared__ int64_t wpre[SEG_ROUND];
+    __shared__ int32_t wcand[SEG_ROUND];
+    __shared__ int32_t s_min_step;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const DChain &ch = chains[blockIdx.x];
     const int32_t M = ch.x->M;
-    const int32_t nseg = M > 0 ? (M + SEG_LEN - 1) / SEG_LEN : 0;
-    for (int32_t w = 1 + warp; w < nseg; w += nw) {
-        const int32_t lo = w * SEG_LEN, hi = min(lo + SEG_LEN, M);
-        int64_t best_gap = -1;
-        int32_t best_q = hi;
-        for (int32_t q = lo + lane; q < hi; q += 32) {
-            const int64_t g = __ldg(ch.dec_r + q) - __ldg(ch.dec_r + q - 1);
-            if (g > best_gap) {
-                best_gap = g;
-                best_q = q;
-            }
+    if (threadIdx.x == 0) s_min_step = INT32_MAX;
+    __syncthreads();
+    {
+        int32_t m = INT32_MAX;
+        for (int b = 1 + threadIdx.x; b <= ch.cap; b += blockDim.x) m = min(m, __ldg(ch.step + b));
+        m = __reduce_min_sync(FULL, (unsigned)m);
+        if (lane == 0) atomicMin(&s_min_step, m);
+    }
+    __syncthreads();
+    const int64_t smin = s_min_step;
+    const int32_t nwin = (M + SEG_LEN - 1) / SEG_LEN;
+    int64_t carry = NEG_INF;  // max lower bound over all earlier rounds
+    int32_t ncand = 0;
+    for (int32_t w0 = 0; w0 < nwin; w0 += SEG_ROUND) {
+        const int32_t nwr = min(SEG_ROUND, nwin - w0);
+        for (int32_t w = warp; w < nwr; w += nw) {  // pass 1
+            const int32_t lo = (w0 + w) * SEG_LEN, hi = min(lo + SEG_LEN, M);
+            int64_t m = NEG_INF;
+            for (int32_t q = lo + lane; q < hi; q += 32)
+                m = max(m, __ldg(ch.dec_r + q) + (int64_t)__ldg(&ch.dec_dj[q].x) * smin);
+            m = warp_max_i64(m);
+            if (lane == 0) wpre[w] = m;
         }
+        __syncthreads();
+        if (warp == 0) {  // exclusive prefix max over the round's windows
+            int64_t run = carry;
+            for (int32_t base = 0; base < nwr; base += 32) {
+                const int32_t w = base + lane;
+                int64_t v = w < nwr ? wpre[w] : NEG_INF;
 #pragma unroll
-        for (int off = 16; off; off >>= 1) {
-            const int64_t og = __shfl_xor_sync(FULL, best_gap, off);
-            const int32_t oq = __shfl_xor_sync(FULL, best_q, off);
-            if (og > best_gap || (og == best_gap && oq < best_q)) {
-                best_gap = og;
-                best_q = oq;
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int64_t u = shfl_up_i64(v, off);
+                    if (lane >= off) v = max(v, u);
+                }
+                int64_t ex = shfl_up_i64(v, 1);
+                ex = lane == 0 ? run : max(run, ex);
+                if (w < nwr) wpre[w] = ex;
+                run = max(run, shfl_i64(v, 31));
+            }
+            if (lane == 0) wcand[0] = 0;  // placeholder, rewritten in pass 2
+            carry = run;                   // lane-uniform
+        }
+        __syncthreads();
+        for (int32_t w = warp; w < nwr; w += nw) {  // pass 2
+            const int32_t lo = (w0 + w) * SEG_LEN, hi = min(lo + SEG_LEN, M);
+            int64_t pre = wpre[w];
+            int64_t best = -1;
+            int32_t best_q = INT32_MAX;
+            for (int32_t q0 = lo; q0 < hi; q0 += 32) {
+                const int32_t q = q0 + lane;
+                const bool v = q < hi;
+                const int64_t rq = v ? __ldg(ch.dec_r + q) : 0;
+                int64_t lb = v ? rq + (int64_t)__ldg(&ch.dec_dj[q].x) * smin : NEG_INF;
+                int64_t inc = lb;
+#pragma unroll
+                for (int off = 1; off < 32; off <<= 1) {
+                    const int64_t u = shfl_up_i64(inc, off);
+                    if (lane >= off) inc = max(inc, u);
+                }
+                int64_t ex = shfl_up_i64(inc, 1);
+                ex = lane == 0 ? pre : max(pre, ex);
+                const int64_t slack = rq - ex;
+                if (v && slack >= 0 && (slack > best || (slack == best && q < best_q))) {
+                    best = slack;
+                    best_q = q;
+                }
+                pre = max(pre, shfl_i64(inc, 31));
+            }
+#pragma unroll
+            for (int off = 16; off; off >>= 1) {
+                const int64_t ob = __shfl_xor_sync(FULL, best, off);
+                const int32_t oq = __shfl_xor_sync(FULL, best_q, off);
+                if (ob > best || (ob == best && oq < best_q)) {
+                    best = ob;
+                    best_q = oq;
+                }
+            }
+            if (lane == 0) wcand[w] = (w0 + w == 0) ? 0 : (best >= 0 ? best_q : -1);
+        }
+        __syncthreads();
+        if (warp == 0) {  // compact the round's candidates
+            for (int32_t base = 0; base < nwr; base += 32) {
+                const int32_t w = base + lane;
+                const int32_t cq = w < nwr ? wcand[w] : -1;
+                const unsigned bal = __ballot_sync(FULL, cq >= 0);
+                if (cq >= 0) ch.seg_start[ncand + __popc(bal & ((1u << lane) - 1u))] = cq;
+                ncand += __popc(bal);
             }
         }
-        if (lane == 0) ch.seg_start[w] = best_q;
+        __syncthreads();
     }
     if (threadIdx.x == 0) {
-        ch.seg_start[0] = 0;
-        ch.seg_start[nseg] = M;
-        ch.x->nseg = nseg;
+        ch.seg_start[ncand] = M;
+        ch.x->nseg = ncand;
         ch.x->leader_pos = 0;
         ch.x->next_seg = 1;
     }

@@ -14,3 +14,10 @@ for _ in range(3):
     api.eval_grid(dg)
 torch.cuda.synchronize()
 print(native.kernel_times())
+kt = {}
+for _ in range(3):
+    api.eval_grid(dg)
+torch.cuda.synchronize()
+for name, ms in native.kernel_times():
+    kt.setdefault(name, []).append(ms)
+print("RESULT", " ".join(f"{k}={sum(v) / len(v):.3f}" for k, v in kt.items()))

@@ -139,6 +139,42 @@ def test_edge_cases():
     assert_parity(grid_of(pairs))
 
 
+def _phased_case(rng, n, mode, cap, monotone=True):
+    """Quiet and busy phases of random length: many idle points, long busy periods,
+    candidates that are not idle (a loose step_min when the step table is not
+    monotone), runs that extend past several candidates."""
+    gaps = []
+    while len(gaps) < n:
+        busy = rng.random() < 0.5
+        gaps.extend(rng.exponential(300.0 if busy else 40000.0, int(rng.integers(20, 3000))))
+    a = np.cumsum(np.asarray(gaps[:n])).astype(np.int64)
+    p = rng.integers(1, 9, n)
+    o = rng.integers(1, 300, n)
+    if monotone:
+        step = [0] + [40 + 25 * b for b in range(1, cap + 1)]
+    else:
+        step = [0] + [int(x) for x in rng.integers(1, 400, cap)]
+    tab = make_tables(8, cap, lambda q: 30 * q, lambda q: 7 * q, step, b2=lambda q: q,
+                      e1=lambda q: 5 * q, e2=lambda q: 3 * q, sbn=[0] + [3] * cap,
+                      sbo=[0] + [4] * cap, sen=[0] + [7] * cap, seo=[0] + [9] * cap)
+    ch = make_chain(tab, mode, cap, 4 if mode == MODE_DSD else 0, 0.8 if mode == MODE_DSD else 0.0,
+                    seed=int(rng.integers(0, 2**63)), ttft_slo=5000, tpot_slo=700)
+    return custom_trace(a, p, o), ch
+
+
+@pytest.mark.parametrize("n_chains,n", [(6, 30000), (100, 3000)])
+def test_decode_speculation_stress(n_chains, n):
+    """Leader / helper protocol of k_decode: few chains (many helpers each: long
+    helper runs, aborts, waits) and many chains (few helpers: the leader walks
+    unclaimed candidates).  Every request's finish must match the oracle."""
+    rng = np.random.default_rng(n_chains * 7919 + n)
+    pairs = []
+    for i in range(n_chains):
+        pairs.append(_phased_case(rng, n, MODE_DSD if i % 3 == 2 else MODE_DPD,
+                                  int(rng.choice([4, 16, 31, 48])), monotone=(i % 2 == 0)))
+    assert_parity(grid_of(pairs))
+
+
 def test_iteration_rebase_and_far_gaps():
     """> 2^31 decode iterations (the 32-bit iteration counter rebases) and joins
     more than 2^31 us after the current boundary (the exact 64-bit path), in
