@@ -57,7 +57,10 @@ enum {
     GL_E_UNSUPPORTED = -5  /* current device is not sm_100 (B200) */
 };
 
-enum { GL_MODE_DPD = 0, GL_MODE_DSD = 1 };           /* Disg-Pref-Decode / Disg-Spec-Decode */
+/* Disg-Pref-Decode / Disg-Spec-Decode, and the two single-GPU
+ * configurations the paper compares against: Standalone (target
+ * only) and SpecDecode (draft + target) co-located on the new GPU. */
+enum { GL_MODE_DPD = 0, GL_MODE_DSD = 1, GL_MODE_STANDALONE = 2, GL_MODE_SPEC_COLO = 3 };
 enum { GL_PRIORITY_SLO = 0, GL_PRIORITY_DEFAULT = 1 }; /* Alg. 1 FallbackStrategy */
 
 /* per-chain status bits, set on the device */
@@ -92,19 +95,25 @@ typedef struct {
  *   step_us[b]    decode iteration (DPD) / speculative step (DSD, Fig. 7) latency
  *                 at batch size b; step_busy_{new,old}_us[b], step_e_{new,old}_uj[b]
  *                 the per-GPU busy time and energy of that iteration
- * DSD acceptance: thr_c = floor(alpha^c * 2^32) (alpha^c by repeated products),
+ * Co-located modes (STANDALONE, SPEC_COLO; R41-R44): one GPU runs prefills
+ * (t1_us, e1_new_uj) and decode iterations / speculative steps (step_*) one at a
+ * time, prefill first: at every iteration boundary each arrived request is
+ * admitted FCFS while the batch has room, its prefill runs alone (first token at
+ * its end), and it then joins the batch if o > 1.  t2_us, b2_old_us, e2_old_uj
+ * are not used; old-GPU step tables are added as given (normally zero).
+ * DSD / SPEC_COLO acceptance: thr_c = floor(alpha^c * 2^32) (alpha^c by repeated products),
  * accepted tokens per member-step = 1 + #{c in 1..gamma : u < thr_c}, u = word
  * (s mod 4) of Philox4x32-10(counter (s/4, j, 0x41434350, 0), key = seed) for
  * request j's own step s (R22; rejection rule P:111-114 as a marginal rate). */
 typedef struct {
-    int32_t mode;          /* GL_MODE_DPD or GL_MODE_DSD */
+    int32_t mode;          /* GL_MODE_DPD, _DSD, _STANDALONE or _SPEC_COLO */
     int32_t trace_idx;     /* index into the traces array */
     int32_t batch_cap;     /* [1, GL_MAX_CAP] */
-    int32_t gamma;         /* DSD: [1, GL_MAX_GAMMA]; ignored for DPD */
+    int32_t gamma;         /* DSD, SPEC_COLO: [1, GL_MAX_GAMMA]; ignored otherwise */
     int32_t max_prompt;    /* [1, GL_MAX_PROMPT] */
     int32_t capacity_ok;   /* 0 => excluded from Alg. 1's feasible set (R38), still simulated */
-    double alpha;          /* DSD marginal acceptance rate in [0, 1] */
-    uint64_t seed;         /* DSD Philox key */
+    double alpha;          /* DSD, SPEC_COLO: marginal acceptance rate in [0, 1] */
+    uint64_t seed;         /* DSD, SPEC_COLO: Philox key */
     const int32_t *t1_us;
     const int64_t *e1_new_uj;
     const int32_t *t2_us;
@@ -118,7 +127,7 @@ typedef struct {
     int64_t ttft_slo_us;   /* Table 2 TTFT SLO, >= 0 */
     int64_t tpot_slo_us;   /* Table 2 TPOT SLO, >= 0 */
     double ce_new_g;       /* Table 1 embodied carbon of the new GPU, grams (> 0) */
-    double ce_old_g;       /* ... of the old GPU */
+    double ce_old_g;       /* ... of the old GPU (>= 0; 0 for the co-located modes) */
 } gl_chain;
 
 /* Sufficient statistics of one simulated chain (integers => bit-exact). 80 B. */

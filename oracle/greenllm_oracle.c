@@ -49,7 +49,7 @@
 #define OR_ACCEPT_STREAM 0x41434350u /* "ACCP": third Philox counter word */
 
 typedef struct {
-    int32_t mode; /* 0 = DPD, 1 = DSD */
+    int32_t mode; /* 0 = DPD, 1 = DSD, 2 = Standalone, 3 = SpecDecode (co-located) */
     int32_t cap;
     int32_t gamma;
     int32_t max_prompt;
@@ -176,7 +176,65 @@ uint32_t oracle_simulate_chain(const int64_t *a, const uint32_t *p, const uint32
     int64_t *fin = malloc(sizeof(int64_t) * n);
     or_member *A = malloc(sizeof(or_member) * (ch->cap > 0 ? ch->cap : 1));
     uint64_t thr[64];
-    if (ch->mode == 1) oracle_thresholds(ch->alpha, ch->gamma, thr);
+    if (ch->mode == 1 || ch->mode == 3) oracle_thresholds(ch->alpha, ch->gamma, thr);
+    const int colo = ch->mode >= 2;
+
+    if (colo) {
+        /* Co-located serving on one GPU: Standalone (target only) and SpecDecode
+         * (draft + target).  At every iteration boundary T the
+         * scheduler first admits, FCFS, every arrived request (a <= T) while the
+         * running batch has room; each admitted prefill runs alone on the GPU
+         * (T += t1[p], first token at T) and a request with o > 1 then joins the
+         * batch.  Decode iterations run only when no admissible request waits
+         * (prefill priority, R41-R44).  Stepped one iteration at a time. */
+        int64_t T = 0;
+        int32_t size = 0;
+        int64_t nxt = 0;
+        while (nxt < n || size > 0) {
+            while (nxt < n && size < ch->cap && a[nxt] <= T) {
+                T += ch->t1_us[p[nxt]];
+                st->busy_new_us += ch->t1_us[p[nxt]];
+                st->e_new_uj += ch->e1_new_uj[p[nxt]];
+                c[nxt] = T;
+                r[nxt] = a[nxt];
+                fin[nxt] = T;
+                if (o[nxt] > 1) {
+                    A[size].j = nxt;
+                    A[size].rem = (int64_t)o[nxt] - 1;
+                    A[size].s = 0;
+                    ++size;
+                }
+                ++nxt;
+            }
+            if (size == 0) { /* idle until the next arrival */
+                T = or_max(T, a[nxt]);
+                continue;
+            }
+            int32_t b = size;
+            T += ch->step_us[b];
+            st->busy_new_us += ch->step_busy_new_us[b];
+            st->busy_old_us += ch->step_busy_old_us[b];
+            st->e_new_uj += ch->step_e_new_uj[b];
+            st->e_old_uj += ch->step_e_old_uj[b];
+            for (int32_t m = 0; m < size;) {
+                if (ch->mode == 2) {
+                    A[m].rem -= 1;
+                } else {
+                    uint32_t u = or_accept_word(ch->seed, (uint32_t)A[m].j, A[m].s);
+                    A[m].rem -= oracle_accept_count(u, thr, ch->gamma);
+                    A[m].s += 1;
+                }
+                if (A[m].rem <= 0) {
+                    fin[A[m].j] = T;
+                    A[m] = A[size - 1];
+                    --size;
+                } else {
+                    ++m;
+                }
+            }
+        }
+        goto slo;
+    }
 
     /* stage 1: prefill FCFS on the new GPU */
     for (int64_t i = 0; i < n; ++i) {
@@ -242,6 +300,7 @@ uint32_t oracle_simulate_chain(const int64_t *a, const uint32_t *p, const uint32
         }
     }
 
+slo:
     /* per-request SLO and chain statistics */
     for (int64_t i = 0; i < n; ++i) {
         int64_t ttft = c[i] - a[i];

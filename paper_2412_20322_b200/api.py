@@ -58,7 +58,7 @@ class DeviceGrid:
                                                  "step_busy_old_us", "step_e_new_uj",
                                                  "step_e_old_uj")]
             self.gl_chains.append(N.GlChain(
-                ch.mode, ch.trace_idx, ch.cap, ch.gamma if ch.mode == N.GL_MODE_DSD else 0,
+                ch.mode, ch.trace_idx, ch.cap, ch.gamma if ch.mode in (N.GL_MODE_DSD, N.GL_MODE_SPEC_COLO) else 0,
                 t.max_prompt, int(ch.capacity_ok), float(ch.alpha), int(ch.seed) & (2**64 - 1),
                 *[x.data_ptr() for x in tabs], int(ch.ttft_slo_us), int(ch.tpot_slo_us),
                 float(ch.ce_new_g), float(ch.ce_old_g)))

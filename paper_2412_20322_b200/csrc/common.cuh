@@ -52,9 +52,11 @@ struct DChain {
     const int32_t *step, *sbn, *sbo;
     const int64_t *sen, *seo;
     // decode stream written by k_stages: ready time r and (demand, request index)
-    // per decode request q, in FCFS order, with two INT64_MAX sentinels after M
+    // per decode request q, in FCFS order, with two INT64_MAX sentinels after M.
+    // Co-located modes: every request, r = arrival, plus its prefill time.
     int64_t *dec_r;
     uint2 *dec_dj;
+    int32_t *dec_pf;    // co-located modes: prefill time t1[p] per stream entry
     int64_t *spec_fin;  // helper h's speculative finish times: spec_fin[h * spec_stride + q]
     int64_t spec_stride;
     int32_t *seg_start; // [nseg + 1] candidate starts (q), seg_start[nseg] = M

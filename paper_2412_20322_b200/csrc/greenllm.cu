@@ -131,15 +131,16 @@ gl_status validate_traces(const gl_trace *traces, int32_t n_traces)
 
 gl_status validate_chain(const gl_chain &c, int32_t n_traces)
 {
-    if (c.mode != GL_MODE_DPD && c.mode != GL_MODE_DSD) return GL_E_INVALID;
+    if (c.mode < GL_MODE_DPD || c.mode > GL_MODE_SPEC_COLO) return GL_E_INVALID;
+    const bool spec = c.mode == GL_MODE_DSD || c.mode == GL_MODE_SPEC_COLO;
     if (c.trace_idx < 0 || c.trace_idx >= n_traces) return GL_E_LOOKUP;
     if (c.batch_cap < 1 || c.batch_cap > GL_MAX_CAP) return GL_E_INVALID;
     if (c.max_prompt < 1 || c.max_prompt > GL_MAX_PROMPT) return GL_E_INVALID;
-    if (c.mode == GL_MODE_DSD && (c.gamma < 1 || c.gamma > GL_MAX_GAMMA)) return GL_E_INVALID;
+    if (spec && (c.gamma < 1 || c.gamma > GL_MAX_GAMMA)) return GL_E_INVALID;
     if (!c.t1_us || !c.e1_new_uj || !c.t2_us || !c.b2_old_us || !c.e2_old_uj || !c.step_us ||
         !c.step_busy_new_us || !c.step_busy_old_us || !c.step_e_new_uj || !c.step_e_old_uj)
         return GL_E_INVALID;
-    if (c.mode == GL_MODE_DSD && !(c.alpha >= 0.0 && c.alpha <= 1.0)) return GL_E_DOMAIN;
+    if (spec && !(c.alpha >= 0.0 && c.alpha <= 1.0)) return GL_E_DOMAIN;
     if (c.ttft_slo_us < 0 || c.tpot_slo_us < 0) return GL_E_DOMAIN;
     if (c.tpot_slo_us > ((int64_t)1 << 32)) return GL_E_DOMAIN;  // keeps deadlines in int64
     return GL_OK;
@@ -172,13 +173,16 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     int max_cap = 1;
     size_t smem_st = 0;
     int64_t rows_total = 0, maxn = 0;
+    bool has_colo = false, has_disg = false;
     for (int32_t i = 0; i < n_chains; ++i) {
         const gl_chain &c = chains[i];
         max_cap = std::max(max_cap, (int)c.batch_cap);
         smem_st = std::max(smem_st, (size_t)8 * gl::round_up4(c.max_prompt + 1) + 16);
         rows_total += traces[c.trace_idx].n;
         maxn = std::max(maxn, traces[c.trace_idx].n);
-        if (c.mode != GL_MODE_DSD) continue;
+        if (c.mode == GL_MODE_STANDALONE || c.mode == GL_MODE_SPEC_COLO) has_colo = true;
+        else has_disg = true;
+        if (c.mode != GL_MODE_DSD && c.mode != GL_MODE_SPEC_COLO) continue;
         DGroup g{};
         g.o = traces[c.trace_idx].output_len;
         g.n = traces[c.trace_idx].n;
@@ -227,13 +231,16 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     total += align256(sizeof(int64_t) * (size_t)dec_total);
     const size_t off_dec_dj = total;
     total += align256(sizeof(uint2) * (size_t)dec_total);
+    const size_t off_dec_pf = total;
+    total += align256(sizeof(int32_t) * (size_t)dec_total);
     // k_decode: one leader warp per chain plus helper warps, about four warps per
     // SM in total; each helper keeps its finish times in a buffer of its own
     // (capped at 8 GiB of scratch)
     int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
-    while (extra > 0 && (size_t)dec_total * extra * sizeof(int64_t) > ((size_t)8 << 30)) --extra;
+    while (extra > 0 && (size_t)dec_total * 2 * extra * sizeof(int64_t) > ((size_t)8 << 30)) --extra;
     const size_t off_spec = total;
-    total += align256(sizeof(int64_t) * (size_t)dec_total * (size_t)std::max(extra, 1));
+    // (co-located chains keep two columns per helper: finish and TTFT)
+    total += align256(sizeof(int64_t) * (size_t)dec_total * 2 * (size_t)std::max(extra, 1));
     const size_t off_segs = total;
     total += align256(sizeof(int32_t) * (size_t)seg_total);
     const size_t off_zero = total;
@@ -271,8 +278,10 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
         d.seo = c.step_e_old_uj;
         d.dec_r = reinterpret_cast<int64_t *>(scratch + off_dec_r) + dec_off[i];
         d.dec_dj = reinterpret_cast<uint2 *>(scratch + off_dec_dj) + dec_off[i];
-        d.spec_fin = reinterpret_cast<int64_t *>(scratch + off_spec) + dec_off[i] * std::max(extra, 1);
-        d.spec_stride = (tr.n + 512 + 31) & ~(int64_t)31;
+        d.dec_pf = reinterpret_cast<int32_t *>(scratch + off_dec_pf) + dec_off[i];
+        d.spec_fin = reinterpret_cast<int64_t *>(scratch + off_spec) + dec_off[i] * 2 * std::max(extra, 1);
+        d.spec_stride = ((tr.n + 512 + 31) & ~(int64_t)31) *
+                        ((c.mode == GL_MODE_STANDALONE || c.mode == GL_MODE_SPEC_COLO) ? 2 : 1);
         d.seg_start = reinterpret_cast<int32_t *>(scratch + off_segs) + seg_off[i];
         d.seg_out = reinterpret_cast<gl::DSegOut *>(scratch + off_segout) + seg_off[i];
         d.x = reinterpret_cast<gl::DChainX *>(scratch + off_x) + i;
@@ -325,25 +334,38 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     }
     if (e == cudaSuccess) {
         const unsigned blocks = (unsigned)(n_chains * (1 + extra));
-        auto launch = [&](auto kern) {
+        auto launch = [&](auto kern, const char *name) {
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem_dec);
             if (r != cudaSuccess) return r;
-            prof_begin("k_decode", stream);
+            prof_begin(name, stream);
             kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, stream>>>(dc, stats_out, rows, (int32_t)n_chains);
             r = cudaGetLastError();
             prof_end(stream);
+            ++launches;
             return r;
         };
-        if (max_cap <= 31)  // the one-row fast paths need b < 32
-            e = launch(gl::k_decode<1>);
-        else if (max_cap <= 64)
-            e = launch(gl::k_decode<2>);
-        else if (max_cap <= 128)
-            e = launch(gl::k_decode<4>);
-        else
-            e = launch(gl::k_decode<8>);
-        ++launches;
+        // disaggregated chains, then co-located ones (each launch skips the others)
+        if (has_disg) {
+            if (max_cap <= 31)  // the one-row fast paths need b < 32
+                e = launch(gl::k_decode<1, false>, "k_decode");
+            else if (max_cap <= 64)
+                e = launch(gl::k_decode<2, false>, "k_decode");
+            else if (max_cap <= 128)
+                e = launch(gl::k_decode<4, false>, "k_decode");
+            else
+                e = launch(gl::k_decode<8, false>, "k_decode");
+        }
+        if (has_colo && e == cudaSuccess) {
+            if (max_cap <= 32)
+                e = launch(gl::k_decode<1, true>, "k_decode_colo");
+            else if (max_cap <= 64)
+                e = launch(gl::k_decode<2, true>, "k_decode_colo");
+            else if (max_cap <= 128)
+                e = launch(gl::k_decode<4, true>, "k_decode_colo");
+            else
+                e = launch(gl::k_decode<8, true>, "k_decode_colo");
+        }
     }
     if (e == cudaSuccess) {
         const int per_thread = 8;
@@ -387,7 +409,7 @@ gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains, cons
     std::vector<DCarbon> cp(n_chains);
     for (int32_t i = 0; i < n_chains; ++i) {
         if (!(std::isfinite(chains[i].ce_new_g) && chains[i].ce_new_g > 0.0)) return GL_E_DOMAIN;
-        if (!(std::isfinite(chains[i].ce_old_g) && chains[i].ce_old_g > 0.0)) return GL_E_DOMAIN;
+        if (!(std::isfinite(chains[i].ce_old_g) && chains[i].ce_old_g >= 0.0)) return GL_E_DOMAIN;
         cp[i] = DCarbon{chains[i].ce_new_g, chains[i].ce_old_g, chains[i].capacity_ok ? 1 : 0, 0};
     }
     const int64_t rows = grid->rows, cols = grid->cols;

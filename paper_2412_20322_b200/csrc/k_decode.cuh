@@ -36,6 +36,12 @@
 namespace gl {
 
 constexpr int DEC_WARPS = 1;  // one warp per k_decode block (leader or helper)
+// dynamic shared memory layout of k_decode (bytes)
+constexpr int SM_R = 0;                                   // [DEC_WARPS][RING] int64 ready times
+constexpr int SM_DJ = DEC_WARPS * RING * 8;               // [DEC_WARPS][RING] (demand, j)
+constexpr int SM_PF = DEC_WARPS * RING * 16;              // [DEC_WARPS][RING] prefill (co-located)
+constexpr int SM_BARS = DEC_WARPS * RING * 20;            // mbarriers
+constexpr int SM_MAGIC = SM_BARS + (2 * DEC_WARPS + 2) * 8;  // [cap+1] reciprocals, then steps
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src)
 {
@@ -52,8 +58,10 @@ __device__ __forceinline__ void cp_async_wait_all() { asm volatile("cp.async.wai
 struct RingW {
     int64_t *r;      // smem [RING]
     uint2 *dj;       // smem [RING]
+    int32_t *pf;     // smem [RING] (co-located modes)
     const int64_t *gr;
     const uint2 *gdj;
+    const int32_t *gpf;  // null unless co-located
     int32_t q_end;      // entries >= q_end read as "no request" (INT64_MAX)
     int32_t base;       // first chunk fetched by start()
     int32_t fill_next;  // next chunk to fetch
@@ -71,6 +79,9 @@ struct RingW {
         cp_async16(dr + 16 * (lane + 32), sr + 16 * (lane + 32));
         cp_async16(dd + 16 * lane, sd + 16 * lane);
         cp_async16(dd + 16 * (lane + 32), sd + 16 * (lane + 32));
+        if (gpf)  // 128 x 4 B of prefill times: one copy per lane
+            cp_async16(reinterpret_cast<char *>(pf + h * 128) + 16 * lane,
+                       reinterpret_cast<const char *>(gpf + q) + 16 * lane);
         cp_async_commit();
     }
     // all issued halves have landed (the newest one was issued long before)
@@ -164,7 +175,11 @@ __device__ __forceinline__ void run_sums(const RunCtx &cx, const uint64_t (&iter
 //   !ROWS  a helper's speculative run: finish times go to the helper's own buffer
 //          (indexed by q); the run aborts once the leader has moved past k0 (the
 //          result is then moot).
-template <int SPL, bool ROWS>
+//   COLO   co-located modes (R41-R44): a join first runs the request's prefill alone
+//          on the GPU (T += pf, its first token at T: the TTFT is written here), and a
+//          request with no decode demand (o = 1) finishes there without joining.
+//          Uses the general loop (the one-row fast paths assume free joins).
+template <int SPL, bool ROWS, bool COLO>
 __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t k0, bool pub)
 {
     constexpr bool to_rows = ROWS;
@@ -176,7 +191,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
     // Table bases as opaque 32-bit shared addresses: kept in registers (ptxas would
     // otherwise rematerialise them from SR_CgaCtaId inside the loops) and read
     // with ld.shared (LDS).
-    uint32_t magic_s = smem_u32(dyn_smem + DEC_WARPS * RING * 16 + (2 * DEC_WARPS + 2) * 8);
+    uint32_t magic_s = smem_u32(dyn_smem + SM_MAGIC);
     asm volatile("" : "+r"(magic_s));
     const uint32_t steps_s = magic_s + 8u * (uint32_t)round_up4(cap + 1);
     auto ld_step = [&](int bb) -> int32_t {
@@ -200,8 +215,10 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
     // the window again, straight from the shared-memory symbol (keeps LDS addressing)
     const int wid = threadIdx.x >> 5;
     const int64_t *const rr = reinterpret_cast<const int64_t *>(dyn_smem) + wid * RING;
-    const uint2 *const rdj =
-        reinterpret_cast<const uint2 *>(dyn_smem + DEC_WARPS * RING * 8) + wid * RING;
+    const uint2 *const rdj = reinterpret_cast<const uint2 *>(dyn_smem + SM_DJ) + wid * RING;
+    const int32_t *const rpf = reinterpret_cast<const int32_t *>(dyn_smem + SM_PF) + wid * RING;
+    // co-located: helper buffers hold finish times, then TTFTs (second half)
+    int64_t *const ttft_spec = fin_spec + (COLO ? ch.spec_stride / 2 : 0);
     int32_t nxt = q0;
     int64_t h_r = rr[nxt & RING_MASK], n_r = rr[(nxt + 1) & RING_MASK];
     uint2 h_dj = rdj[nxt & RING_MASK], n_dj = rdj[(nxt + 1) & RING_MASK];
@@ -245,7 +262,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
 #pragma unroll
     for (int s = 0; s <= SPL; ++s) iters[s] = 0;
 
-    if constexpr (SPL == 1) {
+    if constexpr (SPL == 1 && !COLO) {
         uint32_t Fm = F_EMPTY, fmin = F_EMPTY;
         int64_t *fa = fin_rows;
         unsigned fr = cap >= 32 ? FULL : ((1u << cap) - 1u);
@@ -468,6 +485,20 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                     }
                     I = 0;
                 }
+                if constexpr (COLO) {  // the prefill runs alone on the GPU (R42)
+                    T += (int64_t)rpf[nxt & RING_MASK];
+                    const uint32_t j = h_dj.y;
+                    if (lane == 0) {
+                        if (to_rows) fin_rows[2 * (int64_t)j - 1] = T - h_r;
+                        else ttft_spec[nxt] = T - h_r;
+                    }
+                    if (h_dj.x == 0) {  // o = 1: done at its first token (R13)
+                        if (lane == 0) *fin_addr(j, nxt) = T;
+                        mk = T;
+                        advance();
+                        continue;
+                    }
+                }
                 int s_sel = SPL;
                 unsigned bit = 0;
 #pragma unroll
@@ -556,7 +587,7 @@ __device__ __forceinline__ void backoff() { __nanosleep(64); }
 // A helper's runs write disjoint stretches of its buffer: it skips candidates
 // inside its previous run (if that run was the true one they are not idle points;
 // if not, the leader runs them itself).
-template <int SPL>
+template <int SPL, bool COLO>
 __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
 {
     const DChain &ch = *cx.ch;
@@ -575,7 +606,7 @@ __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
         if (k >= nseg) break;
         if (k < 0) continue;
         ring.q_end = ch.x->M;
-        const RunOut ro = decode_run<SPL, false>(cx, ring, ch.seg_start[k], k, false);
+        const RunOut ro = decode_run<SPL, false, COLO>(cx, ring, ch.seg_start[k], k, false);
         if (ro.stop_seg < 0) continue;  // aborted: the leader passed k (moot values)
         k_end = ro.stop_seg;
         if (lane == 0) {
@@ -593,7 +624,7 @@ __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
 // Leader + helpers (see the file comment).  One warp per block: blocks
 // [0, n_chains) are the leaders of chain blockIdx.x, blocks >= n_chains are
 // helpers of chain blockIdx.x % n_chains.
-template <int SPL>
+template <int SPL, bool COLO>
 __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     k_decode(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
              int64_t *__restrict__ perreq, int32_t n_chains)
@@ -603,13 +634,16 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     const int c = blockIdx.x % n_chains;
     const bool leader = blockIdx.x < n_chains && warp == 0;
     const DChain &ch = chains[c];
+    // one launch per family: the other launch handles this chain
+    if ((ch.mode == GL_MODE_STANDALONE || ch.mode == GL_MODE_SPEC_COLO) != COLO) return;
     const int cap = ch.cap;
     const int cappad = round_up4(cap + 1);
     // smem: per-warp windows first (16-B aligned), then mbarriers, then tables
-    int64_t *ring_r = reinterpret_cast<int64_t *>(smem) + warp * RING;
-    uint2 *ring_dj = reinterpret_cast<uint2 *>(smem + DEC_WARPS * RING * 8) + warp * RING;
-    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + DEC_WARPS * RING * 16);
-    uint64_t *magic = bars + 2 * DEC_WARPS + 2;
+    int64_t *ring_r = reinterpret_cast<int64_t *>(smem + SM_R) + warp * RING;
+    uint2 *ring_dj = reinterpret_cast<uint2 *>(smem + SM_DJ) + warp * RING;
+    int32_t *ring_pf = reinterpret_cast<int32_t *>(smem + SM_PF) + warp * RING;
+    uint64_t *bars = reinterpret_cast<uint64_t *>(smem + SM_BARS);
+    uint64_t *magic = reinterpret_cast<uint64_t *>(smem + SM_MAGIC);
     int32_t *steps = reinterpret_cast<int32_t *>(magic + cappad);
 
     // S0: batch-indexed step table by TMA (warp 0), reciprocals
@@ -634,12 +668,14 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     RingW ring;
     ring.r = ring_r;
     ring.dj = ring_dj;
+    ring.pf = ring_pf;
     ring.gr = ch.dec_r;
     ring.gdj = ch.dec_dj;
+    ring.gpf = COLO ? ch.dec_pf : nullptr;
     ring.fill_next = ring.ready_to = 0;
 
     if (!leader) {
-        helper_loop<SPL>(cx, ring);
+        helper_loop<SPL, COLO>(cx, ring);
         return;
     }
     // The leader hops from idle point to idle point: candidate 0 is one, and a run
@@ -661,7 +697,7 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
         st = __shfl_sync(FULL, st, 0);
         if (st < 0) {  // nobody has run k: simulate it here, into the rows
             ring.q_end = M;
-            const RunOut ro = decode_run<SPL, true>(cx, ring, ch.seg_start[k], k, true);
+            const RunOut ro = decode_run<SPL, true, COLO>(cx, ring, ch.seg_start[k], k, true);
             for (int i = 0; i < 4; ++i) acc[i] += ro.sums[i];
             mk = max(mk, ro.mk);
             k = ro.stop_seg;
@@ -692,9 +728,24 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
                         j[u] = __ldcg(&ch.dec_dj[q].y);
                     }
                 }
+                if constexpr (COLO) {  // (ttft, finish) pairs: TTFTs in the second half
+                    const int64_t *src_t = src + ch.spec_stride / 2;
+                    int64_t t[4];
 #pragma unroll
-                for (int u = 0; u < 4; ++u)
-                    if (q0 + 32 * u + lane < s_hi) cx.rows_fin[2 * (int64_t)j[u]] = f[u];
+                    for (int u = 0; u < 4; ++u) {
+                        const int32_t q = q0 + 32 * u + lane;
+                        if (q < s_hi) t[u] = __ldcg(src_t + q);
+                    }
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (q0 + 32 * u + lane < s_hi)
+                            *reinterpret_cast<longlong2 *>(cx.rows_fin - 1 + 2 * (int64_t)j[u]) =
+                                make_longlong2(t[u], f[u]);
+                } else {
+#pragma unroll
+                    for (int u = 0; u < 4; ++u)
+                        if (q0 + 32 * u + lane < s_hi) cx.rows_fin[2 * (int64_t)j[u]] = f[u];
+                }
             }
         }
         k = m;
@@ -712,7 +763,7 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
 
 __host__ __device__ inline size_t decode_smem_bytes(int cap)
 {
-    return (size_t)DEC_WARPS * RING * 16 + (2 * DEC_WARPS + 2) * 8 + (size_t)round_up4(cap + 1) * 12 + 16;
+    return (size_t)SM_MAGIC + (size_t)round_up4(cap + 1) * 12 + 16;
 }
 
 // ---- S6 + S7: per-request SLO test and hash, the whole GPU over (chain, request)

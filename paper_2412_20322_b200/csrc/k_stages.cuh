@@ -196,7 +196,8 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     const bool skip = status & GL_ST_TABLE;
 
     const int32_t n = (int32_t)ch.n;
-    const bool dsd = ch.mode == GL_MODE_DSD;
+    const bool colo = ch.mode == GL_MODE_STANDALONE || ch.mode == GL_MODE_SPEC_COLO;
+    const bool dsd = ch.mode == GL_MODE_DSD || ch.mode == GL_MODE_SPEC_COLO;  // demand K_j
     const int32_t nchunks = (n + CHUNK - 1) / CHUNK;
     const int32_t per = (nchunks + ST_WARPS - 1) / ST_WARPS;
     const int32_t c_lo = min(warp * per, nchunks), c_hi = min(c_lo + per, nchunks);
@@ -217,11 +218,40 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
                 acc_e_new += __ldg(ch.e1 + c.pc[q]);
                 acc_tokens += c.oc[q];
             }
-            if (c.dec[q]) {
+            if (c.dec[q] && !colo) {
                 acc_busy_old += __ldg(ch.b2 + c.pc[q]);
                 acc_e_old += __ldg(ch.e2 + c.pc[q]);
                 ++cnt;
             }
+        }
+        if (colo) {
+            // Co-located modes: no stage scans; every request enters the decode
+            // stream at its arrival with its demand and prefill time (k_decode
+            // runs prefills and iterations on the one GPU, R41-R42).
+            const int32_t i0 = ck * CHUNK + 4 * lane;
+            if (i0 + 3 < n) {
+                int64_t *dr = ch.dec_r + i0;
+                *reinterpret_cast<longlong2 *>(dr) = make_longlong2(c.av[0], c.av[1]);
+                *reinterpret_cast<longlong2 *>(dr + 2) = make_longlong2(c.av[2], c.av[3]);
+                uint4 *dd = reinterpret_cast<uint4 *>(ch.dec_dj + i0);
+                const uint32_t d0 = dsd ? c.kv[0] : c.oc[0] - 1, d1 = dsd ? c.kv[1] : c.oc[1] - 1;
+                const uint32_t d2 = dsd ? c.kv[2] : c.oc[2] - 1, d3 = dsd ? c.kv[3] : c.oc[3] - 1;
+                dd[0] = make_uint4(d0, (uint32_t)i0, d1, (uint32_t)i0 + 1);
+                dd[1] = make_uint4(d2, (uint32_t)i0 + 2, d3, (uint32_t)i0 + 3);
+                *reinterpret_cast<int4 *>(ch.dec_pf + i0) =
+                    make_int4((int)c.s1[0], (int)c.s1[1], (int)c.s1[2], (int)c.s1[3]);
+            } else {
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    if (!c.valid[q]) continue;
+                    ch.dec_r[i0 + q] = c.av[q];
+                    ch.dec_dj[i0 + q] = make_uint2(dsd ? c.kv[q] : c.oc[q] - 1, (uint32_t)(i0 + q));
+                    ch.dec_pf[i0 + q] = (int32_t)c.s1[q];
+                }
+            }
+            cnt = 0;
+#pragma unroll
+            for (int q = 0; q < 4; ++q) cnt += c.valid[q] ? 1 : 0;
         }
         {  // sortedness across the lane boundary and the chunk / run boundary
             int64_t prev = shfl_up_i64(c.av[3], 1);
@@ -254,7 +284,7 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
 
     // ---- pass 2: c with the true carry, stage-2 aggregate ---------------------
     MP agg2{0, NEG_INF};
-    {
+    if (!colo) {
         int64_t cc = carry_c;
         for (int32_t ck = c_lo; ck < c_hi && !skip; ++ck) {
             ChunkIn c;
@@ -275,7 +305,7 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
 
     // ---- pass 3: c, r -> rows and the compacted decode stream -----------------
     int64_t acc_mk = 0;
-    {
+    if (!colo) {
         int64_t cc = carry_c, rr = carry_r;
         int32_t produced = dbase;
         for (int32_t ck = c_lo; ck < c_hi && !skip; ++ck) {
@@ -355,9 +385,10 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
 
 // Idle-point candidates for the decode speculation.  Request q can only find the
 // decode stage empty if every earlier request has finished by r_q, and request q'
-// cannot finish before r_q' + d_q' * step_min (it joins at or after r_q' and runs
-// d_q' iterations of at least step_min = min_b step[b]).  So
-//     slack_q = r_q - max_{q' < q} (r_q' + d_q' step_min) < 0
+// cannot finish before r_q' + pf_q' + d_q' * step_min (it joins at or after r_q',
+// after its prefill pf (co-located modes; 0 otherwise), and runs d_q' iterations of
+// at least step_min = min_b step[b]).  So
+//     slack_q = r_q - max_{q' < q} (r_q' + pf_q' + d_q' step_min) < 0
 // proves q busy; the candidates are request 0 and, per window of SEG_LEN decode
 // requests, the request with the largest slack if it is >= 0 (ties: the first).
 // Any choice is exact -- k_decode verifies every candidate it uses -- this one
@@ -378,6 +409,7 @@ __global__ void __launch_bounds__(1024)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
     const DChain &ch = chains[blockIdx.x];
     const int32_t M = ch.x->M;
+    const bool colo = ch.mode == GL_MODE_STANDALONE || ch.mode == GL_MODE_SPEC_COLO;
     if (threadIdx.x == 0) s_min_step = INT32_MAX;
     __syncthreads();
     {
@@ -397,7 +429,8 @@ __global__ void __launch_bounds__(1024)
             const int32_t lo = (w0 + w) * SEG_LEN, hi = min(lo + SEG_LEN, M);
             int64_t m = NEG_INF;
             for (int32_t q = lo + lane; q < hi; q += 32)
-                m = max(m, __ldg(ch.dec_r + q) + (int64_t)__ldg(&ch.dec_dj[q].x) * smin);
+                m = max(m, __ldg(ch.dec_r + q) + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
+                               (colo ? __ldg(ch.dec_pf + q) : 0));
             m = warp_max_i64(m);
             if (lane == 0) wpre[w] = m;
         }
@@ -430,7 +463,9 @@ __global__ void __launch_bounds__(1024)
                 const int32_t q = q0 + lane;
                 const bool v = q < hi;
                 const int64_t rq = v ? __ldg(ch.dec_r + q) : 0;
-                int64_t lb = v ? rq + (int64_t)__ldg(&ch.dec_dj[q].x) * smin : NEG_INF;
+                int64_t lb = v ? rq + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
+                                     (colo ? __ldg(ch.dec_pf + q) : 0)
+                               : NEG_INF;
                 int64_t inc = lb;
 #pragma unroll
                 for (int off = 1; off < 32; off <<= 1) {

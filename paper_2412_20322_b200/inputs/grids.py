@@ -18,11 +18,14 @@ from dataclasses import dataclass, field
 
 import numpy as np
 
-from .tables import GPUS, ChainTables, capacity_ok, dpd_tables, dsd_tables
+from .tables import (GPUS, ChainTables, capacity_ok, dpd_tables, dsd_tables, spec_colo_tables,
+                     standalone_tables)
 from .workload import BASE_SEED, RATES8, WORKLOADS, Trace, lengths, make_trace
 
 MODE_DPD = 0
 MODE_DSD = 1
+MODE_STANDALONE = 2   # co-located on one GPU: target only
+MODE_SPEC_COLO = 3    # co-located on one GPU: draft + target
 PRIORITY_SLO = 0
 PRIORITY_DEFAULT = 1
 YEAR_S = 365 * 24 * 3600  # 31,536,000 s
@@ -95,10 +98,12 @@ def _slo_us(workload: str):
 def _chain(mode, trace_idx, cap, tables, workload, new, old, target, draft,
            gamma=0, alpha=0.0, seed=BASE_SEED, label=""):
     ttft, tpot = _slo_us(workload)
-    cap_ok = capacity_ok("dpd" if mode == MODE_DPD else "dsd", new, old, target, draft,
-                         cap, WORKLOADS[workload].p50)
+    kind = {MODE_DPD: "dpd", MODE_DSD: "dsd", MODE_STANDALONE: "standalone",
+            MODE_SPEC_COLO: "spec_colo"}[mode]
+    cap_ok = capacity_ok(kind, new, old, target, draft, cap, WORKLOADS[workload].p50)
+    ce_old = GPUS[old].embodied_g if old is not None else 0.0  # co-located: one GPU
     return ChainSpec(mode, trace_idx, cap, gamma, float(alpha), seed, tables, ttft, tpot,
-                     GPUS[new].embodied_g, GPUS[old].embodied_g, cap_ok, label)
+                     GPUS[new].embodied_g, ce_old, cap_ok, label)
 
 
 def _default_scenario():
@@ -219,7 +224,37 @@ def config5(n: int = 1_000_000, cap: int = 16, rates=RATES8) -> GridSpec:
                     workload="summ")
 
 
-CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5}
+def config6(n: int = 100_000, cap: int = 16, rates=RATES8) -> GridSpec:
+    """config 4 plus the paper's two single-GPU columns
+     -- Standalone 7B on an A100 (the paper's baseline) and
+    SpecDecode 7B/1B (gamma 4, alpha 0.8) co-located on an A100 -- so Alg. 1
+    chooses among all four configuration families.  80 timing chains score
+    8,192 rows x 10 columns."""
+    g4 = config4(n, cap, rates)
+    chains = list(g4.chains)
+    st = standalone_tables("A100", "7B", cap)
+    sc = spec_colo_tables("A100", "7B", "1B", 4, cap)
+    extra = {}
+    for ri, r in enumerate(rates):
+        extra[(ri, 0)] = len(chains)
+        chains.append(_chain(MODE_STANDALONE, ri, cap, st, "chat", "A100", None, "7B", None,
+                             label=f"{st.label} {r}rps"))
+        extra[(ri, 1)] = len(chains)
+        chains.append(_chain(MODE_SPEC_COLO, ri, cap, sc, "chat", "A100", None, "7B", "1B", 4,
+                             0.8, label=f"{sc.label} {r}rps"))
+    cells4 = g4.cell_chain.reshape(g4.rows, g4.cols)
+    n_scen = len(g4.scenarios)
+    cells = []
+    for row in range(g4.rows):
+        ri = row // n_scen
+        cells.extend(list(cells4[row]) + [extra[(ri, 0)], extra[(ri, 1)]])
+    return GridSpec("cfg6", g4.traces, chains, g4.scenarios, g4.row_scenario,
+                    np.array(cells, np.int32), g4.rows, g4.cols + 2, row_labels=g4.row_labels,
+                    col_labels=g4.col_labels + ["Standalone A100", "SpecDecode A100"],
+                    workload="chat")
+
+
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5, 6: config6}
 
 
 def build_config(k: int, **kw) -> GridSpec:

@@ -226,12 +226,71 @@ def dsd_tables(new: str, old: str, target: str, draft: str, gamma: int, cap: int
                        f"DSD {target}/{draft} {new}+{old} g{gamma} {bw_gbps}Gbps cap{cap}")
 
 
+def standalone_tables(gpu: str, model: str, cap: int, max_prompt: int = 4096) -> ChainTables:
+    """Standalone: the target alone on one GPU.  Prefill t1[p] and
+    decode iterations step[b] run on that GPU one at a time (R41-R43); no link,
+    no old GPU (old-GPU tables zero)."""
+    g, m = GPUS[gpu], MODELS[model]
+    p = np.arange(max_prompt + 1)
+    lat1, en1 = roofline(g, m, p)
+    t1, e1 = ceil_us(lat1), round_uj(en1)
+    t1[0] = 0
+    e1[0] = 0
+    zero_p = np.zeros(max_prompt + 1, dtype=np.int64)
+    b = np.arange(cap + 1)
+    latd, end = roofline(g, m, b, b * KV_CTX)
+    step, ed = ceil_us(latd), round_uj(end)
+    step[0] = 0
+    ed[0] = 0
+    zero_b = np.zeros(cap + 1, dtype=np.int64)
+    return ChainTables(_i32(t1), e1, _i32(zero_p), _i32(zero_p), zero_p.copy(),
+                       _i32(step), _i32(step), _i32(zero_b), ed, zero_b.copy(),
+                       f"Standalone {model} {gpu} cap{cap}")
+
+
+def spec_colo_tables(gpu: str, target: str, draft: str, gamma: int, cap: int,
+                     max_prompt: int = 4096) -> ChainTables:
+    """SpecDecode: draft and target co-located on one GPU.  The
+    prefill runs both models' prompt passes back to back; a step is gamma draft
+    passes then the target's verification of gamma+1 tokens per sequence, all on
+    the same GPU (no transfers): S[b] = gamma*D[b] + V[b] (R43)."""
+    g, mt, md = GPUS[gpu], MODELS[target], MODELS[draft]
+    p = np.arange(max_prompt + 1)
+    lat_t, en_t = roofline(g, mt, p)
+    lat_d, en_d = roofline(g, md, p)
+    t1 = ceil_us(lat_t) + ceil_us(lat_d)
+    e1 = round_uj(en_t) + round_uj(en_d)
+    t1[0] = 0
+    e1[0] = 0
+    zero_p = np.zeros(max_prompt + 1, dtype=np.int64)
+    b = np.arange(cap + 1)
+    latd, end = roofline(g, md, b, b * KV_CTX)
+    d_pass, e_d = ceil_us(latd), round_uj(end)
+    latv, env = roofline(g, mt, b * (gamma + 1), b * KV_CTX)
+    v_pass, e_v = ceil_us(latv), round_uj(env)
+    step = gamma * d_pass + v_pass
+    se = gamma * e_d + e_v
+    step[0] = 0
+    se[0] = 0
+    zero_b = np.zeros(cap + 1, dtype=np.int64)
+    return ChainTables(_i32(t1), e1, _i32(zero_p), _i32(zero_p), zero_p.copy(),
+                       _i32(step), _i32(step), _i32(zero_b), se, zero_b.copy(),
+                       f"SpecDecode {target}/{draft} {gpu} g{gamma} cap{cap}")
+
+
 def capacity_ok(mode: str, new: str, old: str, target: str, draft, cap: int,
                 p50: tuple) -> int:
     """R38: weights + cap * (P50 in + P50 out) * kv <= VRAM.
     Capacity-infeasible chains are still simulated; only Alg. 1 excludes them."""
-    g_new, g_old, mt = GPUS[new], GPUS[old], MODELS[target]
+    g_new, mt = GPUS[new], MODELS[target]
     seq = p50[0] + p50[1]
+    if mode in ("standalone", "spec_colo"):  # everything on the one GPU
+        need = mt.weight_bytes + cap * seq * mt.kv_bytes_per_token
+        if mode == "spec_colo":
+            md = MODELS[draft]
+            need += md.weight_bytes + cap * seq * md.kv_bytes_per_token
+        return int(need <= g_new.vram_gb * GIB)
+    g_old = GPUS[old]
     if mode == "dpd":
         ok_new = mt.weight_bytes + (p50[0] + 1) * mt.kv_bytes_per_token <= g_new.vram_gb * GIB
         ok_old = mt.weight_bytes + cap * seq * mt.kv_bytes_per_token <= g_old.vram_gb * GIB

@@ -15,7 +15,7 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 LIB_PATH = os.path.join(HERE, "libgreenllm.so")
 
 GL_OK, GL_E_INVALID, GL_E_DOMAIN, GL_E_LOOKUP, GL_E_CUDA, GL_E_UNSUPPORTED = 0, -1, -2, -3, -4, -5
-GL_MODE_DPD, GL_MODE_DSD = 0, 1
+GL_MODE_DPD, GL_MODE_DSD, GL_MODE_STANDALONE, GL_MODE_SPEC_COLO = 0, 1, 2, 3
 GL_PRIORITY_SLO, GL_PRIORITY_DEFAULT = 0, 1
 GL_MAX_CAP, GL_MAX_GAMMA, GL_MAX_PROMPT = 256, 16, 16384
 ST_UNSORTED, ST_PROMPT_RANGE, ST_OUTPUT_ZERO, ST_OVERFLOW, ST_NEG_ARRIVAL, ST_TABLE = \

@@ -46,6 +46,8 @@ def mix64(j, ttft, finish):
 
 
 def tick_simulate(trace, ch, t_max=10**6):
+    if ch.mode >= 2:
+        return tick_simulate_colo(trace, ch, t_max)
     a = [int(x) for x in trace.arrival_us]
     p = [int(x) for x in trace.prompt_len]
     o = [int(x) for x in trace.output_len]
@@ -135,6 +137,85 @@ def tick_simulate(trace, ch, t_max=10**6):
         if ttft[i] <= ch.ttft_slo_us and (o[i] == 1 or fin[i] - c[i] <= ch.tpot_slo_us * (o[i] - 1)):
             ok += 1
     return dict(ttft=ttft, finish=fin, ready=r, c=c, slo_ok=ok, busy_new_us=busy_new,
+                busy_old_us=busy_old, e_new_uj=e_new, e_old_uj=e_old, tokens=sum(o),
+                makespan_us=max(fin),
+                req_hash=sum(mix64(i, ttft[i], fin[i]) for i in range(n)) & M64)
+
+
+def tick_simulate_colo(trace, ch, t_max=10**6):
+    """Co-located serving (Standalone, SpecDecode; R41-R44): one GPU that runs
+    one job at a time -- a prefill (t1[p]) or one decode iteration at batch b
+    (step[b]).  When the GPU frees up at t: finish the job (a prefill's request
+    joins the batch, or finishes if o = 1; an iteration's members advance and
+    leave), then start the next job: a prefill of the oldest arrived request if
+    the batch has room, else an iteration if the batch is non-empty, else idle."""
+    a = [int(x) for x in trace.arrival_us]
+    p = [int(x) for x in trace.prompt_len]
+    o = [int(x) for x in trace.output_len]
+    n = len(a)
+    tb = ch.tables
+    thr = _thresholds(ch.alpha, ch.gamma) if ch.mode == 3 else []
+    c = [None] * n
+    fin = [None] * n
+    busy_new = busy_old = e_new = e_old = 0
+    arrived = 0
+    queue = []
+    batch = {}
+    job, job_end = None, None  # ("pf", j) or ("it", b)
+    done = 0
+    t = 0
+    while done < n:
+        if t > t_max:
+            raise RuntimeError("tick simulation did not terminate")
+        while arrived < n and a[arrived] == t:
+            queue.append(arrived)
+            arrived += 1
+        if job is not None and job_end == t:
+            if job[0] == "pf":
+                j = job[1]
+                c[j] = t
+                if o[j] > 1:
+                    batch[j] = [o[j] - 1, 0]
+                else:
+                    fin[j] = t
+                    done += 1
+            else:
+                for j in list(batch):
+                    if ch.mode == 2:
+                        batch[j][0] -= 1
+                    else:
+                        u = _draw(ch.seed, j, batch[j][1])
+                        batch[j][0] -= 1 + sum(1 for th in thr if u < th)
+                        batch[j][1] += 1
+                    if batch[j][0] <= 0:
+                        fin[j] = t
+                        done += 1
+                        del batch[j]
+            job = None
+        if job is None:
+            if queue and len(batch) < ch.cap:
+                j = queue.pop(0)
+                job, job_end = ("pf", j), t + int(tb.t1_us[p[j]])
+                busy_new += int(tb.t1_us[p[j]])
+                e_new += int(tb.e1_new_uj[p[j]])
+                if job_end == t:  # zero-length prefill: handle at this tick again
+                    continue
+            elif batch:
+                b = len(batch)
+                job, job_end = ("it", b), t + int(tb.step_us[b])
+                busy_new += int(tb.step_busy_new_us[b])
+                busy_old += int(tb.step_busy_old_us[b])
+                e_new += int(tb.step_e_new_uj[b])
+                e_old += int(tb.step_e_old_uj[b])
+                if job_end == t:
+                    continue
+        t += 1
+    ttft = [c[i] - a[i] for i in range(n)]
+    ok = 0
+    for i in range(n):
+        if ttft[i] <= ch.ttft_slo_us and (o[i] == 1 or fin[i] - c[i] <= ch.tpot_slo_us * (o[i] - 1)):
+            ok += 1
+    return dict(ttft=ttft, finish=fin, ready=list(a), c=c, slo_ok=ok, busy_new_us=busy_new,
                 busy_old_us=busy_old, e_new_uj=e_new, e_old_uj=e_old, tokens=sum(o),
                 makespan_us=max(fin),
                 req_hash=sum(mix64(i, ttft[i], fin[i]) for i in range(n)) & M64)

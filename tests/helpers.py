@@ -3,7 +3,8 @@ from __future__ import annotations
 
 import numpy as np
 
-from paper_2412_20322_b200.inputs import MODE_DPD, MODE_DSD, ChainSpec, ChainTables, custom_trace
+from paper_2412_20322_b200.inputs import (MODE_DPD, MODE_DSD, MODE_SPEC_COLO, MODE_STANDALONE,
+                                          ChainSpec, ChainTables, custom_trace)
 
 
 def make_tables(max_prompt, cap, t1, t2, step, b2=None, e1=None, e2=None, sbn=None, sbo=None,
@@ -39,7 +40,7 @@ def make_chain(tables, mode=MODE_DPD, cap=None, gamma=0, alpha=0.0, seed=0x1234,
 def random_case(rng: np.random.Generator, n=None, mode=None, cap=None, small=True):
     """A random tiny (trace, chain) pair sized for the 1-us tick brute force."""
     n = int(rng.integers(1, 11)) if n is None else n
-    mode = int(rng.integers(0, 2)) if mode is None else mode
+    mode = int(rng.integers(0, 4)) if mode is None else mode
     cap = int(rng.integers(1, 5)) if cap is None else cap
     max_prompt = 6
     span = int(rng.integers(0, 150))
@@ -48,7 +49,7 @@ def random_case(rng: np.random.Generator, n=None, mode=None, cap=None, small=Tru
         a[: n // 2] = a[0]
         a = np.sort(a)
     p = rng.integers(1, max_prompt + 1, n)
-    o = rng.integers(1, 9 if mode == MODE_DPD else 14, n)
+    o = rng.integers(1, 9 if mode in (MODE_DPD, MODE_STANDALONE) else 14, n)
     if rng.random() < 0.2:
         o[rng.integers(0, n)] = 1
     t1v = rng.integers(1, 25, max_prompt + 1)
@@ -63,8 +64,9 @@ def random_case(rng: np.random.Generator, n=None, mode=None, cap=None, small=Tru
     seo = rng.integers(0, 5000, cap + 1)
     tab = make_tables(max_prompt, cap, t1v, t2v, stepv, b2v, e1v, e2v, sbn, sbo, sen, seo,
                       label="random")
-    gamma = int(rng.integers(1, 6)) if mode == MODE_DSD else 0
-    alpha = float(rng.choice([0.0, 0.3, 0.5, 0.8, 0.95, 1.0])) if mode == MODE_DSD else 0.0
+    spec = mode in (MODE_DSD, MODE_SPEC_COLO)
+    gamma = int(rng.integers(1, 6)) if spec else 0
+    alpha = float(rng.choice([0.0, 0.3, 0.5, 0.8, 0.95, 1.0])) if spec else 0.0
     ttft_slo = int(rng.integers(10, 200))
     tpot_slo = int(rng.integers(5, 40))
     ch = make_chain(tab, mode, cap, gamma, alpha, seed=int(rng.integers(0, 2**63)),

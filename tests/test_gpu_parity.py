@@ -13,8 +13,10 @@ import torch
 from oracle import oracle as O
 from paper_2412_20322_b200 import api
 from paper_2412_20322_b200 import native as N
-from paper_2412_20322_b200.inputs import (MODE_DPD, MODE_DSD, GridSpec, build_config,
-                                          custom_trace)
+from paper_2412_20322_b200.inputs import (MODE_DPD, MODE_DSD, MODE_SPEC_COLO, MODE_STANDALONE,
+                                          GridSpec, build_config, custom_trace)
+
+ALL_MODES = (MODE_DPD, MODE_DSD, MODE_STANDALONE, MODE_SPEC_COLO)
 from tests.helpers import make_chain, make_tables, random_case
 
 pytestmark = pytest.mark.gpu
@@ -86,7 +88,7 @@ def test_caps_and_slot_layouts(cap):
     """SPL = 1/2/4/8 slots per lane, caps at and across the 32-lane boundaries."""
     rng = np.random.default_rng(cap)
     pairs = []
-    for mode in (MODE_DPD, MODE_DSD):
+    for mode in ALL_MODES:
         for n in (1, 7, 129, 1000):
             tr, ch = random_case(rng, n=n, mode=mode, cap=cap)
             a = np.sort(rng.integers(0, 40 * n, n))  # dense enough to fill big batches
@@ -99,7 +101,7 @@ def test_medium_random_traces():
     rng = np.random.default_rng(5)
     pairs = []
     for n in (127, 128, 129, 255, 256, 257, 1000, 4099, 20000):
-        for mode in (MODE_DPD, MODE_DSD):
+        for mode in ALL_MODES:
             tr, ch = random_case(rng, n=n, mode=mode, cap=int(rng.integers(1, 40)))
             a = np.sort(rng.integers(0, int(rng.integers(1, 200)) * n, n))
             pairs.append((custom_trace(a, tr.prompt_len, tr.output_len), ch))
@@ -132,6 +134,14 @@ def test_edge_cases():
     # int64-large timestamps
     big = 2**52 + np.arange(0, 500 * 37, 37)
     pairs.append((custom_trace(big, [3] * 500, [6] * 500), _edge_chain(cap=8)))
+    # co-located modes: o = 1 only, bursts, cap 1, cap >= N, large timestamps
+    for m, g, a in ((MODE_STANDALONE, 0, 0.0), (MODE_SPEC_COLO, 3, 0.7)):
+        pairs.append((custom_trace([0, 0, 0, 0, 9], [1, 2, 3, 4, 5], [1, 1, 1, 1, 1]),
+                      _edge_chain(mode=m, gamma=g, alpha=a)))
+        pairs.append((custom_trace([0] * 300, [2] * 300, [5] * 300), _edge_chain(cap=1, mode=m, gamma=g, alpha=a)))
+        pairs.append((custom_trace(np.arange(50), [1] * 50, [3] * 50), _edge_chain(cap=256, mode=m, gamma=g, alpha=a)))
+        pairs.append((custom_trace(big, [3] * 500, [6] * 500), _edge_chain(cap=8, mode=m, gamma=g, alpha=a)))
+        pairs.append((custom_trace([5], [3], [4]), _edge_chain(mode=m, gamma=g, alpha=a)))
     # large prompt tables (GL_MAX_PROMPT) and a 1-entry table
     pairs.append((custom_trace(np.arange(300) * 50, np.arange(1, 301) * 50, [3] * 300),
                   _edge_chain(max_prompt=16384)))
@@ -157,7 +167,8 @@ def _phased_case(rng, n, mode, cap, monotone=True):
     tab = make_tables(8, cap, lambda q: 30 * q, lambda q: 7 * q, step, b2=lambda q: q,
                       e1=lambda q: 5 * q, e2=lambda q: 3 * q, sbn=[0] + [3] * cap,
                       sbo=[0] + [4] * cap, sen=[0] + [7] * cap, seo=[0] + [9] * cap)
-    ch = make_chain(tab, mode, cap, 4 if mode == MODE_DSD else 0, 0.8 if mode == MODE_DSD else 0.0,
+    spec = mode in (MODE_DSD, MODE_SPEC_COLO)
+    ch = make_chain(tab, mode, cap, 4 if spec else 0, 0.8 if spec else 0.0,
                     seed=int(rng.integers(0, 2**63)), ttft_slo=5000, tpot_slo=700)
     return custom_trace(a, p, o), ch
 
@@ -170,8 +181,8 @@ def test_decode_speculation_stress(n_chains, n):
     rng = np.random.default_rng(n_chains * 7919 + n)
     pairs = []
     for i in range(n_chains):
-        pairs.append(_phased_case(rng, n, MODE_DSD if i % 3 == 2 else MODE_DPD,
-                                  int(rng.choice([4, 16, 31, 48])), monotone=(i % 2 == 0)))
+        pairs.append(_phased_case(rng, n, ALL_MODES[i % 4], int(rng.choice([4, 16, 31, 48])),
+                                  monotone=(i % 2 == 0)))
     assert_parity(grid_of(pairs))
 
 
@@ -222,6 +233,12 @@ def test_config3_reduced_all_chains():
 
 def test_config4_reduced_all_chains():
     assert_parity(build_config(4, n=5000))
+
+
+def test_config6_colocated_columns_all_chains():
+    """NEXT #1: config 4 plus the Standalone / SpecDecode A100 columns, every
+    chain and every Alg. 1 row (20k requests per trace)."""
+    assert_parity(build_config(6, n=20_000))
 
 
 def test_config4_full_size_all_chains():

@@ -11,7 +11,8 @@ import numpy as np
 import pytest
 
 from oracle import oracle as O
-from paper_2412_20322_b200.inputs import MODE_DPD, MODE_DSD, custom_trace
+from paper_2412_20322_b200.inputs import (MODE_DPD, MODE_DSD, MODE_SPEC_COLO, MODE_STANDALONE,
+                                          custom_trace)
 from tests.bruteforce import tick_simulate
 from tests.helpers import make_chain, make_tables, random_case
 
@@ -438,6 +439,91 @@ def test_exhaustive_tiny_enumeration():
                             assert list(fin) == bf["finish"] and st["slo_ok"] == bf["slo_ok"]
                             count += 1
     assert count > 3000
+
+
+def test_exhaustive_tiny_enumeration_colocated():
+    """Co-located modes (R41-R44): all N<=2 traces with arrivals on 0..5, p, o in
+    {1,2,3}, cap in {1,2}, Standalone and SpecDecode, against the tick brute force."""
+    import itertools
+    count = 0
+    for cap in (1, 2):
+        for mode, gamma, alpha in ((MODE_STANDALONE, 0, 0.0), (MODE_SPEC_COLO, 2, 0.5)):
+            tab = make_tables(3, cap, lambda p: 2 * p, lambda p: 0, [0, 3, 5][: cap + 1],
+                              e1=lambda p: 7 * p, sbn=[0, 3, 5][: cap + 1], sen=[0, 11, 13][: cap + 1])
+            ch = make_chain(tab, mode, cap, gamma, alpha, ttft_slo=5, tpot_slo=4)
+            for n in (1, 2):
+                for a in itertools.combinations_with_replacement(range(6), n):
+                    for p in itertools.product((1, 2, 3), repeat=n):
+                        for o in itertools.product((1, 2, 3), repeat=n):
+                            tr = custom_trace(a, p, o)
+                            st, ttft, fin = O.simulate_chain(tr, ch)
+                            bf = tick_simulate(tr, ch)
+                            assert list(fin) == bf["finish"] and list(ttft) == bf["ttft"]
+                            assert st["slo_ok"] == bf["slo_ok"] and st["e_new_uj"] == bf["e_new_uj"]
+                            count += 1
+    assert count > 2000
+
+
+def _colo_chain(mode=MODE_STANDALONE, cap=4, step=None, gamma=0, alpha=0.0):
+    step = step or [0] + [8 + b for b in range(1, cap + 1)]
+    tab = make_tables(8, cap, lambda p: 10 * p, lambda p: 0, step, e1=lambda p: 7 * p,
+                      sbn=step, sen=[0] + [5 * b for b in range(1, cap + 1)])
+    return make_chain(tab, mode, cap, gamma, alpha, ttft_slo=10**9, tpot_slo=10**9)
+
+
+def test_colocated_isolated_request_closed_form():
+    """Standalone, one request: TTFT = L_p, finish = a + L_p + (o-1) L_d."""
+    for p_, o_ in ((1, 1), (5, 2), (8, 30)):
+        ch = _colo_chain()
+        st, ttft, fin = O.simulate_chain(custom_trace([1000], [p_], [o_]), ch)
+        assert ttft[0] == 10 * p_
+        assert fin[0] == 1000 + 10 * p_ + (o_ - 1) * 9
+        assert st["busy_new_us"] == 10 * p_ + (o_ - 1) * 9
+        assert st["busy_old_us"] == 0 and st["e_old_uj"] == 0
+
+
+def test_colocated_cap1_is_lindley():
+    """cap = 1: one request at a time on the GPU, prefill then decode:
+    finish_j = max(finish_prev, a_j) + t1[p_j] + (o_j - 1) S[1] (Lindley)."""
+    rng = np.random.default_rng(41)
+    for _ in range(50):
+        n = int(rng.integers(1, 60))
+        a = np.sort(rng.integers(0, 3000, n))
+        p = rng.integers(1, 9, n)
+        o = rng.integers(1, 12, n)
+        ch = _colo_chain(cap=1, step=[0, 13])
+        st, ttft, fin = O.simulate_chain(custom_trace(a, p, o), ch)
+        prev = -10**18
+        for j in range(n):
+            start = max(prev, a[j])
+            assert ttft[j] == start + 10 * p[j] - a[j]
+            prev = start + 10 * p[j] + (o[j] - 1) * 13
+            assert fin[j] == prev
+
+
+def test_colocated_prefill_priority_burst():
+    """k simultaneous arrivals, cap >= k, o = 2: all k prefills run first (prefill
+    priority), then ONE iteration at batch k finishes everyone (R42)."""
+    for k in (1, 2, 5, 8):
+        ch = _colo_chain(cap=8)
+        p = np.arange(1, k + 1)
+        st, ttft, fin = O.simulate_chain(custom_trace(np.zeros(k), p, np.full(k, 2)), ch)
+        assert list(ttft) == list(np.cumsum(10 * p))
+        assert np.all(fin == 10 * p.sum() + 8 + k)
+
+
+def test_specdecode_colocated_steps_match_eacc():
+    """Isolated SpecDecode requests: (finish - c)/S[1] = K_j steps whose mean
+    accepted tokens approach E[acc] = (1 - alpha^(g+1))/(1 - alpha)."""
+    n, o_ = 400, 60
+    gamma, alpha = 4, 0.8
+    ch = _colo_chain(mode=MODE_SPEC_COLO, cap=2, step=[0, 9, 9], gamma=gamma, alpha=alpha)
+    a = np.arange(n) * 10**6
+    st, ttft, fin = O.simulate_chain(custom_trace(a, np.ones(n), np.full(n, o_)), ch)
+    K = (fin - (a + ttft)) / 9
+    assert np.all(K == np.round(K))
+    eacc = (1 - alpha ** (gamma + 1)) / (1 - alpha)
+    assert abs((o_ - 1) / K.mean() - eacc) < 0.25
 
 
 # ----------------------------------------------------------- invariants
