@@ -151,13 +151,37 @@ typedef struct {
     uint32_t s;
 } or_member;
 
+/* Link impulses of one chain (NEXT #2, R45-R47): payload bytes put on the
+ * GPU-GPU link at their issue times.  Two streams, each in time order:
+ * per-request stage-2 payloads and per-iteration decode payloads. */
+typedef struct {
+    int64_t bytes_per_token;       /* request payload = bytes_per_token * (p + 1) */
+    int64_t bytes_per_member_step; /* iteration payload = b * bytes_per_member_step */
+    int64_t *req_t, *req_w, n_req;
+    int64_t *it_t, *it_w, n_it, cap_it;
+} or_link;
+
+static void or_link_iter(or_link *lk, int64_t t, int64_t w)
+{
+    if (!lk || w <= 0) return;
+    if (lk->n_it == lk->cap_it) {
+        lk->cap_it = lk->cap_it ? 2 * lk->cap_it : 1024;
+        lk->it_t = realloc(lk->it_t, sizeof(int64_t) * lk->cap_it);
+        lk->it_w = realloc(lk->it_w, sizeof(int64_t) * lk->cap_it);
+    }
+    lk->it_t[lk->n_it] = t;
+    lk->it_w[lk->n_it] = w;
+    lk->n_it += 1;
+}
+
 /*
  * Simulate one timing chain.  ttft_out / finish_out / ready_out (stage-2
  * completion r_i) may be NULL.  Returns the status bits (0 = valid input).
+ * lk (may be NULL) collects the link impulses of the disaggregated modes.
  */
-uint32_t oracle_simulate_chain(const int64_t *a, const uint32_t *p, const uint32_t *o, int64_t n,
-                               const or_chain *ch, or_stats *st, int64_t *ttft_out,
-                               int64_t *finish_out, int64_t *ready_out)
+static uint32_t or_simulate(const int64_t *a, const uint32_t *p, const uint32_t *o, int64_t n,
+                            const or_chain *ch, or_stats *st, int64_t *ttft_out,
+                            int64_t *finish_out, int64_t *ready_out, or_link *lk)
 {
     memset(st, 0, sizeof *st);
     st->n = n;
@@ -251,6 +275,13 @@ uint32_t oracle_simulate_chain(const int64_t *a, const uint32_t *p, const uint32
         if (o[i] > 1) {
             st->busy_old_us += ch->b2_old_us[p[i]];
             st->e_old_uj += ch->e2_old_uj[p[i]];
+            /* R46: the stage-2 payload (DPD: KV of p+1 tokens, R11; DSD: the
+             * prompt-ID handoff, R12) is issued when the prefill completes */
+            if (lk && lk->bytes_per_token > 0) {
+                lk->req_t[lk->n_req] = c[i];
+                lk->req_w[lk->n_req] = lk->bytes_per_token * ((int64_t)p[i] + 1);
+                lk->n_req += 1;
+            }
         }
     }
     /* requests with a single output token finish at prefill completion */
@@ -275,8 +306,10 @@ uint32_t oracle_simulate_chain(const int64_t *a, const uint32_t *p, const uint32
             T = r[nxt];
             continue;
         }
-        /* one iteration at batch size b */
+        /* one iteration at batch size b; R47: its link payload (DSD: draft IDs,
+         * probabilities and accepted IDs of every member, R21) is issued at its start */
         int32_t b = size;
+        if (lk) or_link_iter(lk, T, (int64_t)b * lk->bytes_per_member_step);
         T += ch->step_us[b];
         st->busy_new_us += ch->step_busy_new_us[b];
         st->busy_old_us += ch->step_busy_old_us[b];
@@ -395,6 +428,86 @@ void oracle_alg1(int32_t rows, int32_t cols, const uint8_t *present, const doubl
         }
         choice[row] = best;
     }
+}
+
+uint32_t oracle_simulate_chain(const int64_t *a, const uint32_t *p, const uint32_t *o, int64_t n,
+                               const or_chain *ch, or_stats *st, int64_t *ttft_out,
+                               int64_t *finish_out, int64_t *ready_out)
+{
+    return or_simulate(a, p, o, n, ch, st, ttft_out, finish_out, ready_out, NULL);
+}
+
+/*
+ * Bandwidth demand of one chain's GPU-GPU link (Fig. 4,
+ * P:230-247, "bandwidth requirement"; "peak bandwidth demand over a
+ * 1 s sliding window", S:372 bandwidth accounting).  Readings R45-R47
+ * (DESIGN.md §2): every payload is an impulse of bytes at its issue time; the
+ * demand at t is the bytes issued in the half-open window [t, t + window_us);
+ * the peak is its maximum over t, which is attained at an impulse time.
+ *   out[0] total bytes, out[1] peak window bytes, out[2] the earliest impulse
+ *   time whose window attains the peak (-1 if there is no impulse), out[3] the
+ *   number of impulses.
+ * Stepped the plain way: the chain is simulated one iteration at a time
+ * recording every impulse, the two time-ordered streams are merged, and a
+ * two-pointer sweep evaluates the window at every distinct impulse time.
+ */
+uint32_t oracle_link_demand(const int64_t *a, const uint32_t *p, const uint32_t *o, int64_t n,
+                            const or_chain *ch, int64_t bytes_per_token,
+                            int64_t bytes_per_member_step, int64_t window_us, or_stats *st,
+                            int64_t out[4])
+{
+    or_link lk;
+    memset(&lk, 0, sizeof lk);
+    lk.bytes_per_token = bytes_per_token;
+    lk.bytes_per_member_step = bytes_per_member_step;
+    lk.req_t = malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    lk.req_w = malloc(sizeof(int64_t) * (n > 0 ? n : 1));
+    out[0] = 0;
+    out[1] = 0;
+    out[2] = -1;
+    out[3] = 0;
+    /* the co-located modes have no link (R45) */
+    uint32_t status = or_simulate(a, p, o, n, ch, st, NULL, NULL, NULL, ch->mode >= 2 ? NULL : &lk);
+    if (status == 0) {
+        int64_t K = lk.n_req + lk.n_it;
+        int64_t *t = malloc(sizeof(int64_t) * (K > 0 ? K : 1));
+        int64_t *w = malloc(sizeof(int64_t) * (K > 0 ? K : 1));
+        int64_t *pre = malloc(sizeof(int64_t) * (K + 1));
+        int64_t x = 0, y = 0;
+        for (int64_t k = 0; k < K; ++k) { /* merge of the two time-ordered streams */
+            if (y >= lk.n_it || (x < lk.n_req && lk.req_t[x] <= lk.it_t[y])) {
+                t[k] = lk.req_t[x];
+                w[k] = lk.req_w[x];
+                ++x;
+            } else {
+                t[k] = lk.it_t[y];
+                w[k] = lk.it_w[y];
+                ++y;
+            }
+        }
+        pre[0] = 0;
+        for (int64_t k = 0; k < K; ++k) pre[k + 1] = pre[k] + w[k];
+        int64_t hi = 0;
+        for (int64_t k = 0; k < K; ++k) {
+            if (k > 0 && t[k] == t[k - 1]) continue; /* same window as the group's first */
+            while (hi < K && t[hi] < t[k] + window_us) ++hi;
+            int64_t v = pre[hi] - pre[k];
+            if (v > out[1]) {
+                out[1] = v;
+                out[2] = t[k];
+            }
+        }
+        out[0] = pre[K];
+        out[3] = K;
+        free(t);
+        free(w);
+        free(pre);
+    }
+    free(lk.req_t);
+    free(lk.req_w);
+    free(lk.it_t);
+    free(lk.it_w);
+    return status;
 }
 
 int32_t oracle_version(void) { return 1; }

@@ -66,6 +66,11 @@ def lib():
             L.oracle_simulate_chain.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                                 C.POINTER(OrChain), C.POINTER(OrStats),
                                                 C.c_void_p, C.c_void_p, C.c_void_p]
+            L.oracle_link_demand.restype = C.c_uint32
+            L.oracle_link_demand.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
+                                             C.POINTER(OrChain), C.c_int64, C.c_int64,
+                                             C.c_int64, C.POINTER(OrStats),
+                                             C.POINTER(C.c_int64)]
             L.oracle_carbon.restype = None
             L.oracle_carbon.argtypes = [C.POINTER(OrStats), C.c_double, C.c_double, C.c_double,
                                         C.c_double, C.c_double, C.POINTER(C.c_double)]
@@ -139,6 +144,34 @@ def simulate_chain(trace, ch, per_request: bool = True, ready: bool = False):
     if ready:
         return d, ttft, fin, r
     return d, ttft, fin
+
+
+LINK_FIELDS = ("total_bytes", "peak_bytes", "peak_t_us", "n_impulses")
+
+
+def link_demand(trace, ch, window_us: int = 1_000_000, bytes_per_token=None,
+                bytes_per_member_step=None):
+    """Peak link bandwidth demand of one chain (oracle_link_demand): dict with
+    total_bytes, peak_bytes (max bytes issued in any [t, t + window_us)),
+    peak_t_us (earliest impulse time attaining it, -1 if none), n_impulses, and
+    the chain's stats under "stats".  Payload sizes default to the chain tables'."""
+    L = lib()
+    a = _c(trace.arrival_us, np.int64)
+    p = _c(trace.prompt_len, np.uint32)
+    o = _c(trace.output_len, np.uint32)
+    s, keep = make_chain(ch)
+    bpt = ch.tables.link_bytes_per_token if bytes_per_token is None else bytes_per_token
+    pm = ch.tables.link_bytes_per_member_step if bytes_per_member_step is None \
+        else bytes_per_member_step
+    st = OrStats()
+    out = (C.c_int64 * 4)()
+    status = L.oracle_link_demand(_ptr(a), _ptr(p), _ptr(o), a.shape[0], C.byref(s), int(bpt),
+                                  int(pm), int(window_us), C.byref(st), out)
+    del keep
+    d = {f: int(out[i]) for i, f in enumerate(LINK_FIELDS)}
+    d["stats"] = {f: getattr(st, f) for f in STAT_FIELDS}
+    d["status"] = int(status)
+    return d
 
 
 def _stats_struct(d) -> OrStats:

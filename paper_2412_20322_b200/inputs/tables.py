@@ -141,6 +141,13 @@ class ChainTables:
     step_e_new_uj: np.ndarray    # int64
     step_e_old_uj: np.ndarray    # int64
     label: str = ""
+    # GPU-GPU link payloads (bandwidth demand, NEXT #2, R45-R47): a request's
+    # stage-2 payload is link_bytes_per_token * (p + 1) bytes (DPD: its KV, R11;
+    # DSD: its prompt IDs, R12); a decode iteration at batch b puts
+    # b * link_bytes_per_member_step bytes on the link (DSD: draft IDs, probs and
+    # accepted IDs of every member, R21).  Zero where nothing crosses the link.
+    link_bytes_per_token: int = 0
+    link_bytes_per_member_step: int = 0
 
     @property
     def max_prompt(self) -> int:
@@ -181,7 +188,15 @@ def dpd_tables(new: str, old: str, model: str, cap: int, bw_gbps: float = 16.0,
     zero_b = np.zeros(cap + 1, dtype=np.int64)
     return ChainTables(_i32(t1), e1, _i32(t2), _i32(zero_p), zero_p.copy(),
                        _i32(step), _i32(zero_b), _i32(step), zero_b.copy(), ed,
-                       f"DPD {model} {new}->{old} {bw_gbps}Gbps cap{cap}")
+                       f"DPD {model} {new}->{old} {bw_gbps}Gbps cap{cap}",
+                       link_bytes_per_token=m.kv_bytes_per_token, link_bytes_per_member_step=0)
+
+
+def dsd_member_step_bytes(gamma: int) -> int:
+    """Link bytes one member puts on the link per speculative step (R21, Fig. 7):
+    gamma draft token IDs (4 B), gamma probability vectors (VOCAB fp16), and the
+    gamma+1 accepted / bonus token IDs returned."""
+    return 4 * gamma + gamma * VOCAB * BYTES_PER_PROB + 4 * (gamma + 1)
 
 
 def dsd_tables(new: str, old: str, target: str, draft: str, gamma: int, cap: int,
@@ -223,7 +238,9 @@ def dsd_tables(new: str, old: str, target: str, draft: str, gamma: int, cap: int
         arr[0] = 0
     return ChainTables(_i32(t1), e1, _i32(t2), _i32(b2), e2,
                        _i32(step), _i32(busy_new), _i32(busy_old), se_new, se_old,
-                       f"DSD {target}/{draft} {new}+{old} g{gamma} {bw_gbps}Gbps cap{cap}")
+                       f"DSD {target}/{draft} {new}+{old} g{gamma} {bw_gbps}Gbps cap{cap}",
+                       link_bytes_per_token=4,
+                       link_bytes_per_member_step=dsd_member_step_bytes(gamma))
 
 
 def standalone_tables(gpu: str, model: str, cap: int, max_prompt: int = 4096) -> ChainTables:

@@ -45,9 +45,13 @@ def mix64(j, ttft, finish):
     return z ^ (z >> 31)
 
 
-def tick_simulate(trace, ch, t_max=10**6):
+def tick_simulate(trace, ch, t_max=10**6, link=None):
+    """``link`` = (bytes_per_token, bytes_per_member_step) records the link
+    impulses (R45-R47) as (time, bytes) pairs under "impulses"."""
     if ch.mode >= 2:
         return tick_simulate_colo(trace, ch, t_max)
+    bpt, pm = link if link is not None else (0, 0)
+    impulses = []
     a = [int(x) for x in trace.arrival_us]
     p = [int(x) for x in trace.prompt_len]
     o = [int(x) for x in trace.output_len]
@@ -83,6 +87,8 @@ def tick_simulate(trace, ch, t_max=10**6):
                 pf_cur = None
                 if o[j] > 1:
                     s2_queue.append(j)
+                    if bpt > 0:
+                        impulses.append((t, bpt * (p[j] + 1)))
                 else:
                     fin[j] = t
                     done += 1
@@ -126,6 +132,8 @@ def tick_simulate(trace, ch, t_max=10**6):
             if batch:
                 b = len(batch)
                 it_end, it_b = t + int(tb.step_us[b]), b
+                if pm > 0:
+                    impulses.append((t, b * pm))
                 busy_new += int(tb.step_busy_new_us[b])
                 busy_old += int(tb.step_busy_old_us[b])
                 e_new += int(tb.step_e_new_uj[b])
@@ -138,8 +146,22 @@ def tick_simulate(trace, ch, t_max=10**6):
             ok += 1
     return dict(ttft=ttft, finish=fin, ready=r, c=c, slo_ok=ok, busy_new_us=busy_new,
                 busy_old_us=busy_old, e_new_uj=e_new, e_old_uj=e_old, tokens=sum(o),
-                makespan_us=max(fin),
+                makespan_us=max(fin), impulses=impulses,
                 req_hash=sum(mix64(i, ttft[i], fin[i]) for i in range(n)) & M64)
+
+
+def window_peak_bruteforce(impulses, window_us):
+    """Max over EVERY integer t of the bytes issued in [t, t + window_us), and
+    the earliest impulse time whose window attains it (-1 without impulses)."""
+    if not impulses:
+        return 0, 0, -1
+    ts = [t for t, _ in impulses]
+    best = 0
+    for t0 in range(min(ts) - window_us, max(ts) + 1):
+        v = sum(w for t, w in impulses if t0 <= t < t0 + window_us)
+        best = max(best, v)
+    at = min(t for t in ts if sum(w for u, w in impulses if t <= u < t + window_us) == best)
+    return sum(w for _, w in impulses), best, at
 
 
 def tick_simulate_colo(trace, ch, t_max=10**6):
