@@ -211,6 +211,45 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces,
                            gl_chain_stats *stats_host, double *carbon_host,
                            int32_t *choice_host, uint8_t *via_fallback_host, void *stream);
 
+/* ---- Link bandwidth demand (Fig. 4, "bandwidth
+ * requirement"; "peak bandwidth demand over a 1 s sliding window").
+ * Readings R45-R47: every payload the timing model puts on the
+ * GPU-GPU link is an impulse of bytes at its ISSUE time --
+ *   a request with o > 1: bytes_per_token * (p + 1) at its prefill completion
+ *     c = a + TTFT (DPD: its KV cache, R11; DSD: its prompt IDs, R12);
+ *   a decode iteration at batch b: b * bytes_per_member_step at its start (DSD:
+ *     draft IDs, probabilities and accepted IDs of every member, R21; DPD: 0).
+ * demand(t) = bytes issued in [t, t + window_us); peak = max over t (attained at
+ * an impulse time); peak_t_us = the earliest impulse time attaining it.  The
+ * co-located modes have no link: all zero, peak_t_us = -1. */
+typedef struct {
+    int64_t bytes_per_token;        /* >= 0 */
+    int64_t bytes_per_member_step;  /* >= 0 */
+} gl_link_params;
+
+typedef struct {
+    int64_t total_bytes;   /* all payload bytes (SPEC S:372's bandwidth accounting) */
+    int64_t peak_bytes;    /* max bytes issued in one window (x 8 / window = peak bits/s) */
+    int64_t peak_t_us;     /* earliest impulse time whose window attains the peak, -1 if none */
+    int64_t n_impulses;    /* payloads with a positive size */
+} gl_link_stats;           /* 32 B */
+
+/*
+ * Simulate every chain exactly as gl_eval_grid does (one leader warp per chain,
+ * no speculation, recording the decode batch-size changes) and compute its link
+ * demand.  Stream-ordered like gl_eval_grid.
+ *   traces, chains   as for gl_eval_grid (HOST descriptors, DEVICE data)
+ *   params           HOST [n_chains] payload sizes
+ *   window_us        >= 1 (1,000,000 = SPEC's 1 s window)
+ *   stats_out        DEVICE [n_chains] or NULL (the same statistics gl_eval_grid writes)
+ *   link_out         DEVICE [n_chains]
+ * Errors: as gl_eval_grid; GL_E_INVALID for window_us < 1 or a NULL params /
+ * link_out, GL_E_DOMAIN for a negative payload size.
+ */
+gl_status gl_link_demand(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
+                         int32_t n_chains, const gl_link_params *params, int64_t window_us,
+                         gl_chain_stats *stats_out, gl_link_stats *link_out, void *stream);
+
 /* Number of CUDA kernels the last successful call on this thread enqueued. */
 int32_t gl_last_launch_count(void);
 

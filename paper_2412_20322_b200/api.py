@@ -105,6 +105,29 @@ def eval_grid(dg: DeviceGrid, chain_lo: int = 0, chain_hi: int | None = None, st
     return stats, pr
 
 
+def link_demand(dg: DeviceGrid, window_us: int = 1_000_000, chain_lo: int = 0,
+                chain_hi: int | None = None, params=None, stream=None):
+    """Link bandwidth demand of chains [chain_lo, chain_hi) (gl_link_demand; NEXT #2)
+    -> (stats uint8 tensor [k, 80], link uint8 tensor [k, 32]).  ``params`` =
+    [(bytes_per_token, bytes_per_member_step)] per chain, default the chain tables'."""
+    hi = dg.n_chains if chain_hi is None else chain_hi
+    chains = dg.gl_chains[chain_lo:hi]
+    k = len(chains)
+    if params is None:
+        params = [(c.tables.link_bytes_per_token, c.tables.link_bytes_per_member_step)
+                  for c in dg.grid.chains[chain_lo:hi]]
+    stats = torch.empty((k, N.STATS_DTYPE.itemsize), dtype=torch.uint8, device=dg.device)
+    link = torch.empty((k, N.LINK_DTYPE.itemsize), dtype=torch.uint8, device=dg.device)
+    dg.last_launches = N.link_demand(dg.gl_traces, chains, params, window_us, stats.data_ptr(),
+                                     link.data_ptr(), _stream_ptr(stream))
+    return stats, link
+
+
+def link_numpy(link: torch.Tensor) -> np.ndarray:
+    """Device link tensor -> numpy structured array (gl_link_stats fields)."""
+    return link.detach().cpu().numpy().view(N.LINK_DTYPE).reshape(-1)
+
+
 def argmin_feasible(dg: DeviceGrid, stats: torch.Tensor, want_carbon: bool = True, stream=None):
     """Alg. 1 over the grid -> (carbon f64 [rows, cols] or None, choice int32 [rows],
     via_fallback uint8 [rows]) as device tensors."""

@@ -39,6 +39,8 @@ struct DChainX {
     int32_t nseg;        // idle-point candidates, set by k_segments
     int32_t leader_pos;  // candidate the leader is at (helpers skip and abort below)
     int32_t next_seg;    // helper work counter
+    int32_t n_ev;        // LOG launches: batch-size log entries written
+    int32_t pad[3];
 };
 
 // one timing chain as the kernels see it (built by the host from gl_chain + gl_trace)
@@ -62,6 +64,7 @@ struct DChain {
     int32_t *seg_start; // [nseg + 1] candidate starts (q), seg_start[nseg] = M
     DSegOut *seg_out;   // [nseg]
     DChainX *x;
+    longlong2 *ev;      // LOG launches: batch-size log [2 M + 8] of (T, b) (k_link.cuh)
     int64_t n;
     int64_t ttft_slo, tpot_slo;
     int64_t out_off;  // first row of this chain in the per-request (ttft, finish) array

@@ -21,6 +21,9 @@
  *                                    speculative decode event loops
  *   k_finalize    (k_decode.cuh)     whole GPU over (chain, request): SLO, hash
  *   k_argmin      (k_argmin.cuh)     one warp per Alg. 1 row
+ * gl_link_demand (NEXT #2) runs the same simulation with a leader-only
+ * k_decode<.., LOG> that records batch-size changes, then
+ *   k_link_scan / k_link_window / k_link_reduce (k_link.cuh).
  * No tensor cores: nothing on this path is a contraction.
  */
 #include <cuda_runtime.h>
@@ -40,6 +43,7 @@
 #include "k_decode.cuh"
 #include "k_stages.cuh"
 #include "k_dsd_demand.cuh"
+#include "k_link.cuh"
 
 namespace {
 
@@ -148,22 +152,28 @@ gl_status validate_chain(const gl_chain &c, int32_t n_traces)
 
 gl_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GL_OK : GL_E_CUDA; }
 
-}  // namespace
+// the extra work of gl_link_demand
+struct LinkReq {
+    const gl_link_params *params;  // host [n_chains]
+    int64_t window;
+    gl_link_stats *out;            // device [n_chains]
+};
 
-// ---------------------------------------------------------------- C ABI
-extern "C" {
-
-gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
-                       int32_t n_chains, gl_chain_stats *stats_out, int64_t *per_request_out,
-                       void *stream_)
+gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
+                    int32_t n_chains, gl_chain_stats *stats_out, int64_t *per_request_out,
+                    cudaStream_t stream, const LinkReq *lk)
 {
-    g_last_launches = 0;
-    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     gl_status st = validate_traces(traces, n_traces);
     if (st) return st;
-    if (!chains || n_chains <= 0 || !stats_out) return GL_E_INVALID;
+    if (!chains || n_chains <= 0 || (!stats_out && !lk)) return GL_E_INVALID;
     for (int32_t i = 0; i < n_chains; ++i)
         if ((st = validate_chain(chains[i], n_traces))) return st;
+    if (lk) {
+        if (!lk->params || !lk->out || lk->window < 1) return GL_E_INVALID;
+        for (int32_t i = 0; i < n_chains; ++i)
+            if (lk->params[i].bytes_per_token < 0 || lk->params[i].bytes_per_member_step < 0)
+                return GL_E_DOMAIN;
+    }
     if ((st = device_check())) return st;
 
     // DSD demand groups: equal (output_len, n, gamma, thresholds, seed) share K
@@ -238,11 +248,37 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     // (capped at 8 GiB of scratch)
     int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
     while (extra > 0 && (size_t)dec_total * 2 * extra * sizeof(int64_t) > ((size_t)8 << 30)) --extra;
+    if (lk) extra = 0;  // the batch-size log needs one sequential run per chain
     const size_t off_spec = total;
     // (co-located chains keep two columns per helper: finish and TTFT)
     total += align256(sizeof(int64_t) * (size_t)dec_total * 2 * (size_t)std::max(extra, 1));
     const size_t off_segs = total;
     total += align256(sizeof(int32_t) * (size_t)seg_total);
+    // gl_link_demand: batch-size logs [2 n + 8], prefix sums, per-block partials, stats
+    std::vector<int64_t> ev_off(n_chains, 0), rq_off(n_chains, 0);
+    int64_t ev_total = 0, rq_total = 0;
+    size_t off_ev = 0, off_itpre = 0, off_rqpre = 0, off_links = 0, off_part = 0, off_lstats = 0;
+    if (lk) {
+        for (int32_t i = 0; i < n_chains; ++i) {
+            const int64_t n = traces[chains[i].trace_idx].n;
+            ev_off[i] = ev_total;
+            ev_total += 2 * n + 16;
+            rq_off[i] = rq_total;
+            rq_total += n + 8;
+        }
+        off_ev = total;
+        total += align256(sizeof(longlong2) * (size_t)ev_total);
+        off_itpre = total;
+        total += align256(sizeof(int64_t) * (size_t)ev_total);
+        off_rqpre = total;
+        total += align256(sizeof(int64_t) * (size_t)rq_total);
+        off_links = total;
+        total += align256(sizeof(gl::DLink) * (size_t)n_chains);
+        off_part = total;
+        total += align256(sizeof(longlong2) * gl::LINK_BLOCKS * (size_t)n_chains);
+        off_lstats = total;
+        if (!stats_out) total += align256(sizeof(gl_chain_stats) * (size_t)n_chains);
+    }
     const size_t off_zero = total;
     const size_t off_segout = total;
     total += align256(sizeof(gl::DSegOut) * (size_t)seg_total);
@@ -253,6 +289,8 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
         return st;
     int64_t *rows = per_request_out ? per_request_out : reinterpret_cast<int64_t *>(scratch + off_rows);
+    if (!stats_out) stats_out = reinterpret_cast<gl_chain_stats *>(scratch + off_lstats);
+    std::vector<gl::DLink> dl(lk ? n_chains : 0);
     for (size_t g = 0; g < groups.size(); ++g)
         groups[g].K = reinterpret_cast<uint32_t *>(scratch + k_off[g]);
 
@@ -285,6 +323,16 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
         d.seg_start = reinterpret_cast<int32_t *>(scratch + off_segs) + seg_off[i];
         d.seg_out = reinterpret_cast<gl::DSegOut *>(scratch + off_segout) + seg_off[i];
         d.x = reinterpret_cast<gl::DChainX *>(scratch + off_x) + i;
+        d.ev = lk ? reinterpret_cast<longlong2 *>(scratch + off_ev) + ev_off[i] : nullptr;
+        if (lk) {
+            gl::DLink &L = dl[i];
+            L.bpt = lk->params[i].bytes_per_token;
+            L.pm = lk->params[i].bytes_per_member_step;
+            L.it_pre = reinterpret_cast<int64_t *>(scratch + off_itpre) + ev_off[i];
+            L.req_pre = reinterpret_cast<int64_t *>(scratch + off_rqpre) + rq_off[i];
+            L.part = reinterpret_cast<longlong2 *>(scratch + off_part) + (size_t)gl::LINK_BLOCKS * i;
+            L.ev_cap = 2 * tr.n + 16;
+        }
         d.n = tr.n;
         d.ttft_slo = c.ttft_slo_us;
         d.tpot_slo = c.tpot_slo_us;
@@ -300,6 +348,9 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
                                     cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess && !groups.empty())
         e = cudaMemcpyAsync(scratch + off_groups, groups.data(), sizeof(DGroup) * groups.size(),
+                            cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess && lk)
+        e = cudaMemcpyAsync(scratch + off_links, dl.data(), sizeof(gl::DLink) * n_chains,
                             cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(scratch + off_zero, 0, zero_bytes, stream);
     int launches = 0;
@@ -346,7 +397,16 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
             return r;
         };
         // disaggregated chains, then co-located ones (each launch skips the others)
-        if (has_disg) {
+        if (has_disg && lk) {  // leader-only runs that log the batch size
+            if (max_cap <= 31)
+                e = launch(gl::k_decode<1, false, true>, "k_decode_log");
+            else if (max_cap <= 64)
+                e = launch(gl::k_decode<2, false, true>, "k_decode_log");
+            else if (max_cap <= 128)
+                e = launch(gl::k_decode<4, false, true>, "k_decode_log");
+            else
+                e = launch(gl::k_decode<8, false, true>, "k_decode_log");
+        } else if (has_disg) {
             if (max_cap <= 31)  // the one-row fast paths need b < 32
                 e = launch(gl::k_decode<1, false>, "k_decode");
             else if (max_cap <= 64)
@@ -376,11 +436,59 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
         prof_end(stream);
         ++launches;
     }
+    if (e == cudaSuccess && lk) {
+        const gl::DLink *dlk = reinterpret_cast<const gl::DLink *>(scratch + off_links);
+        prof_begin("k_link_scan", stream);
+        gl::k_link_scan<<<dim3((unsigned)n_chains, 2), 1024, 0, stream>>>(dc, dlk);
+        e = cudaGetLastError();
+        prof_end(stream);
+        ++launches;
+        if (e == cudaSuccess) {
+            prof_begin("k_link_window", stream);
+            gl::k_link_window<<<dim3(gl::LINK_BLOCKS, (unsigned)n_chains), gl::LINK_THREADS, 0,
+                                stream>>>(dc, dlk, rows, lk->window);
+            e = cudaGetLastError();
+            prof_end(stream);
+            ++launches;
+        }
+        if (e == cudaSuccess) {
+            prof_begin("k_link_reduce", stream);
+            gl::k_link_reduce<<<(unsigned)n_chains, 32, 0, stream>>>(dc, dlk, lk->out, n_chains);
+            e = cudaGetLastError();
+            prof_end(stream);
+            ++launches;
+        }
+    }
     cudaError_t ef = cudaFreeAsync(scratch, stream);
     if (e == cudaSuccess) e = ef;
     if (e != cudaSuccess) return GL_E_CUDA;
     g_last_launches = launches;
     return GL_OK;
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- C ABI
+extern "C" {
+
+gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
+                       int32_t n_chains, gl_chain_stats *stats_out, int64_t *per_request_out,
+                       void *stream_)
+{
+    g_last_launches = 0;
+    if (!stats_out) return GL_E_INVALID;
+    return eval_impl(traces, n_traces, chains, n_chains, stats_out, per_request_out,
+                     static_cast<cudaStream_t>(stream_), nullptr);
+}
+
+gl_status gl_link_demand(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
+                         int32_t n_chains, const gl_link_params *params, int64_t window_us,
+                         gl_chain_stats *stats_out, gl_link_stats *link_out, void *stream_)
+{
+    g_last_launches = 0;
+    const LinkReq lk{params, window_us, link_out};
+    return eval_impl(traces, n_traces, chains, n_chains, stats_out, nullptr,
+                     static_cast<cudaStream_t>(stream_), &lk);
 }
 
 gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains, const gl_chain *chains,

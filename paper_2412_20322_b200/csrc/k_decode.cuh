@@ -124,6 +124,7 @@ struct RingW {
 
 struct RunOut {
     int64_t mk;       // last finish time of the run (0 if nothing finished)
+    int32_t ne;       // LOG: batch-size log entries written so far (chain total)
     int64_t sums[4];  // decode busy_new, busy_old, e_new, e_old
     int32_t stop_seg; // candidate the run stopped at (idle there; nseg = end), -1 aborted
 };
@@ -137,6 +138,7 @@ struct RunCtx {
     int cap, lane;
     int32_t nseg;
     int32_t hid;  // helper index (buffer), -1 for the leader
+    longlong2 *ev;  // LOG: the chain's batch-size log (T, b after the change)
 };
 
 // kept out of line so the decode loops stay free of memory-ordering operations
@@ -179,8 +181,12 @@ __device__ __forceinline__ void run_sums(const RunCtx &cx, const uint64_t (&iter
 //          on the GPU (T += pf, its first token at T: the TTFT is written here), and a
 //          request with no decode demand (o = 1) finishes there without joining.
 //          Uses the general loop (the one-row fast paths assume free joins).
-template <int SPL, bool ROWS, bool COLO>
-__device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t k0, bool pub)
+//   LOG    (leader-only launches, link bandwidth demand) every change of the batch
+//          size b appends (T, b) to cx.ev at index ne (ne0 on entry): between two
+//          entries b is constant and iterations run back to back from the first.
+template <int SPL, bool ROWS, bool COLO, bool LOG = false>
+__device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t k0, bool pub,
+                             int32_t ne0 = 0)
 {
     constexpr bool to_rows = ROWS;
     const DChain &ch = *cx.ch;
@@ -258,6 +264,14 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
     int64_t T = 0, mk = 0;
     uint32_t I = 0;
     int b = 0;
+    int32_t ne = ne0;
+    longlong2 *const evp = cx.ev;
+    auto log_b = [&]() {
+        if constexpr (LOG) {
+            if (lane == 0) evp[ne] = make_longlong2(T, (int64_t)b);
+            ++ne;
+        }
+    };
     uint64_t iters[SPL + 1];
 #pragma unroll
     for (int s = 0; s <= SPL; ++s) iters[s] = 0;
@@ -313,6 +327,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                 }
                 fmin = min(fmin, fnew);
                 ++b;
+                log_b();
                 shift_up();
                 advance();
             }
@@ -351,6 +366,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         if (lv) Fm = F_EMPTY;
                         fr |= lm;
                         b -= __popc(lm);
+                        log_b();
                         fmin = __reduce_min_sync(FULL, Fm);
                         break;
                     }
@@ -395,6 +411,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         }
                         fmin = min(fmin, fnew);
                         ++b;
+                        log_b();
                         shift_up();
                         advance();
                         if (b == cap || h_r <= T) break;
@@ -411,6 +428,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         fr |= lm;
                         const int nl = __popc(lm);
                         b -= nl;
+                        log_b();
                         mk = T;
                         fmin = __reduce_min_sync(FULL, Fm);
                         if (nl == 1) shift_down();
@@ -451,6 +469,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
             fr |= lm;
             const int nl = __popc(lm);
             b -= nl;
+            log_b();
             mk = T;
             fmin = __reduce_min_sync(FULL, Fm);
             if (nl == 1) shift_down();
@@ -518,6 +537,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                     }
                 }
                 ++b;
+                if constexpr (!COLO) log_b();
                 advance();
             }
             if (b == 0) {  // idle (R17)
@@ -570,12 +590,16 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                 nl += __popc(lm);
             }
             b -= nl;
-            if (nl) mk = T;
+            if (nl) {
+                mk = T;
+                if constexpr (!COLO) log_b();
+            }
         }
 #pragma unroll
         for (int s = 0; s <= SPL; ++s) iters[s] += cnt[s];
     }
     res.mk = mk;
+    res.ne = ne;
     run_sums<SPL>(cx, iters, res.sums);
     return res;
 }
@@ -624,11 +648,14 @@ __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
 // Leader + helpers (see the file comment).  One warp per block: blocks
 // [0, n_chains) are the leaders of chain blockIdx.x, blocks >= n_chains are
 // helpers of chain blockIdx.x % n_chains.
-template <int SPL, bool COLO>
+//   LOG: leader-only launch (no helper blocks) that also writes the batch-size
+//   log of every disaggregated chain (link bandwidth demand, k_link.cuh).
+template <int SPL, bool COLO, bool LOG = false>
 __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     k_decode(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
              int64_t *__restrict__ perreq, int32_t n_chains)
 {
+    static_assert(!(LOG && COLO), "the co-located modes have no link");
     extern __shared__ __align__(16) unsigned char smem[];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int c = blockIdx.x % n_chains;
@@ -664,7 +691,7 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     const int32_t nseg = ch.x->nseg;
     const int32_t hid = leader ? -1 : (int32_t)(blockIdx.x / n_chains) - 1;
     RunCtx cx{&ch, steps, magic, perreq + 2 * ch.out_off + 1,
-              ch.spec_fin + (int64_t)max(hid, 0) * ch.spec_stride, cap, lane, nseg, hid};
+              ch.spec_fin + (int64_t)max(hid, 0) * ch.spec_stride, cap, lane, nseg, hid, ch.ev};
     RingW ring;
     ring.r = ring_r;
     ring.dj = ring_dj;
@@ -674,10 +701,13 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     ring.gpf = COLO ? ch.dec_pf : nullptr;
     ring.fill_next = ring.ready_to = 0;
 
-    if (!leader) {
-        helper_loop<SPL, COLO>(cx, ring);
-        return;
+    if constexpr (!LOG) {
+        if (!leader) {
+            helper_loop<SPL, COLO>(cx, ring);
+            return;
+        }
     }
+    int32_t ne = 0;
     // The leader hops from idle point to idle point: candidate 0 is one, and a run
     // from an idle point is the true run, so where it stops is the next one.
     int64_t acc[4] = {0, 0, 0, 0};
@@ -697,7 +727,8 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
         st = __shfl_sync(FULL, st, 0);
         if (st < 0) {  // nobody has run k: simulate it here, into the rows
             ring.q_end = M;
-            const RunOut ro = decode_run<SPL, true, COLO>(cx, ring, ch.seg_start[k], k, true);
+            const RunOut ro = decode_run<SPL, true, COLO, LOG>(cx, ring, ch.seg_start[k], k, true, ne);
+            ne = ro.ne;
             for (int i = 0; i < 4; ++i) acc[i] += ro.sums[i];
             mk = max(mk, ro.mk);
             k = ro.stop_seg;
@@ -751,6 +782,7 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
         k = m;
     }
     if (lane == 0) {
+        if (LOG) ch.x->n_ev = ne;
         st_release_gpu(&ch.x->leader_pos, nseg);
         gl_chain_stats &s = stats[c];
         s.busy_new_us += acc[0];

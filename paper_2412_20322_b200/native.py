@@ -54,9 +54,19 @@ STATS_DTYPE = np.dtype([("n", "<i8"), ("slo_ok", "<i8"), ("tokens", "<i8"),
                         ("e_old_uj", "<i8"), ("makespan_us", "<i8"), ("req_hash", "<u8"),
                         ("status", "<u4"), ("capacity_ok", "<u4")])
 assert STATS_DTYPE.itemsize == 80
+# gl_link_stats (32 B)
+LINK_DTYPE = np.dtype([("total_bytes", "<i8"), ("peak_bytes", "<i8"), ("peak_t_us", "<i8"),
+                       ("n_impulses", "<i8")])
+assert LINK_DTYPE.itemsize == 32
+
+
+class GlLinkParams(C.Structure):
+    _fields_ = [("bytes_per_token", C.c_int64), ("bytes_per_member_step", C.c_int64)]
+
+
 SCEN_DTYPE = np.dtype([("ci", "<f8"), ("lt_new", "<f8"), ("lt_old", "<f8")])
 
-EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_last_launch_count",
+EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_link_demand", "gl_last_launch_count",
            "gl_profile_enable", "gl_kernel_times", "gl_strerror", "gl_version")
 
 _lib = None
@@ -86,6 +96,9 @@ def lib():
         L.gl_evaluate_host.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
                                        C.POINTER(GlScenario), i32, C.POINTER(GlGrid), i32, i32,
                                        i32, i32, vp, vp, vp, vp, vp]
+        L.gl_link_demand.restype = i32
+        L.gl_link_demand.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
+                                     C.POINTER(GlLinkParams), C.c_int64, vp, vp, vp]
         L.gl_last_launch_count.restype = i32
         L.gl_last_launch_count.argtypes = []
         L.gl_profile_enable.restype = i32
@@ -110,6 +123,17 @@ def eval_grid(traces, chains, stats_ptr: int, per_request_ptr: int | None, strea
     c_arr = (GlChain * len(chains))(*chains)
     check(lib().gl_eval_grid(t_arr, len(traces), c_arr, len(chains), stats_ptr,
                              per_request_ptr or None, stream or None), "gl_eval_grid")
+    return lib().gl_last_launch_count()
+
+
+def link_demand(traces, chains, params, window_us: int, stats_ptr: int | None, link_ptr: int,
+                stream: int):
+    """params: [(bytes_per_token, bytes_per_member_step)] per chain."""
+    t_arr = (GlTrace * len(traces))(*traces)
+    c_arr = (GlChain * len(chains))(*chains)
+    p_arr = (GlLinkParams * len(chains))(*[GlLinkParams(int(a), int(b)) for a, b in params])
+    check(lib().gl_link_demand(t_arr, len(traces), c_arr, len(chains), p_arr, int(window_us),
+                               stats_ptr or None, link_ptr, stream or None), "gl_link_demand")
     return lib().gl_last_launch_count()
 
 

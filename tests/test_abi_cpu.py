@@ -27,7 +27,8 @@ def declared_functions():
 
 def test_header_declares_expected_calls():
     assert declared_functions() == sorted(["gl_eval_grid", "gl_argmin_feasible",
-                                           "gl_evaluate_host", "gl_last_launch_count",
+                                           "gl_evaluate_host", "gl_link_demand",
+                                           "gl_last_launch_count",
                                            "gl_profile_enable", "gl_kernel_times",
                                            "gl_strerror", "gl_version"])
 
@@ -62,6 +63,8 @@ int main(void){
  printf("%zu %zu %zu %zu\n", offsetof(gl_chain, alpha), offsetof(gl_chain, t1_us),
         offsetof(gl_chain, ttft_slo_us), offsetof(gl_chain, ce_old_g));
  printf("%zu %zu\n", offsetof(gl_chain_stats, req_hash), offsetof(gl_chain_stats, status));
+ printf("%zu %zu %zu\n", sizeof(gl_link_params), sizeof(gl_link_stats),
+        offsetof(gl_link_stats, peak_t_us));
  return 0;}
 """
     import tempfile
@@ -80,6 +83,9 @@ int main(void){
                     N.GlChain.ce_old_g.offset]
     so = list(map(int, lines[2].split()))
     assert so == [N.STATS_DTYPE.fields["req_hash"][1], N.STATS_DTYPE.fields["status"][1]]
+    lo = list(map(int, lines[3].split()))
+    assert lo == [C.sizeof(N.GlLinkParams), N.LINK_DTYPE.itemsize,
+                  N.LINK_DTYPE.fields["peak_t_us"][1]]
 
 
 def test_calls_fail_loudly_without_gpu(built):
@@ -97,6 +103,16 @@ def test_calls_fail_loudly_without_gpu(built):
         setattr(ch, f, 16)
     with pytest.raises(built.GreenLLMError):
         built.eval_grid([tr], [ch], 16, None, 0)
+    with pytest.raises(built.GreenLLMError):
+        built.link_demand([tr], [ch], [(4, 100)], 1_000_000, None, 16, 0)
+    # host validation precedes the device check: a bad window is GL_E_INVALID, a
+    # negative payload GL_E_DOMAIN
+    with pytest.raises(built.GreenLLMError) as ei:
+        built.link_demand([tr], [ch], [(4, 100)], 0, None, 16, 0)
+    assert ei.value.status == built.GL_E_INVALID
+    with pytest.raises(built.GreenLLMError) as ei:
+        built.link_demand([tr], [ch], [(-1, 100)], 10, None, 16, 0)
+    assert ei.value.status == built.GL_E_DOMAIN
 
 
 def test_oracle_and_product_share_no_code():
