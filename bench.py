@@ -40,6 +40,7 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--n", type=int, default=100_000, help="requests per trace")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-analysis", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
     return ap.parse_args()
 
@@ -304,6 +305,10 @@ def run_ours(args):
     else:
         e2e = e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush, dev)
 
+    analysis = None
+    if world == 1 and not args.no_analysis:
+        analysis = {"link_demand": link_demand_bench(dg, grid, flush)}
+
     if rank != 0:
         if world > 1:
             dist.destroy_process_group()
@@ -374,11 +379,52 @@ def run_ours(args):
         "e2e": e2e,
         "gpu_launches": launches,
         "clocks": clocks,
+        "analysis": analysis,
     }
     print(json.dumps(out))
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def link_demand_bench(dg, grid, flush, reps=3):
+    """NEXT #2 (not part of the timed step): gl_link_demand over all chains of the
+    workload -- the same simulation run leader-only with the batch-size log, then the
+    1 s sliding-window peak (k_link_*).  Device time with CUDA events; per-kernel
+    times from gl_kernel_times."""
+    import torch
+
+    from paper_2412_20322_b200 import api
+    from paper_2412_20322_b200 import native as N
+    stream = torch.cuda.current_stream()
+    api.link_demand(dg)
+    torch.cuda.synchronize()
+    N.profile_enable(True)
+    N.kernel_times()
+    ms = []
+    for i in range(reps):
+        flush.fill_(i & 0xFF)
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record(stream)
+        _, link = api.link_demand(dg)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        ms.append(e0.elapsed_time(e1))
+    kt = {}
+    for name, t in N.kernel_times():
+        kt.setdefault(name, []).append(t)
+    N.profile_enable(False)
+    lk = api.link_numpy(link)
+    gbps = {}
+    for ci, ch in enumerate(grid.chains):
+        kind = {0: "dpd", 1: "dsd"}.get(ch.mode)
+        if kind:
+            gbps.setdefault(kind, []).append(float(lk[ci]["peak_bytes"]) * 8 / 1e9)
+    return {"ms": sum(ms) / len(ms), "window_us": 1_000_000,
+            "kernel_ms": {k: sum(v) / len(v) for k, v in kt.items()},
+            "peak_gbps_range": {k: [min(v), max(v)] for k, v in gbps.items()},
+            "note": "peak link demand of every chain (R45-R47); leader-only decode + "
+                    "k_link_scan/window/reduce; outside the timed step"}
 
 
 def e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush, dev):

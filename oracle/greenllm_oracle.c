@@ -368,6 +368,35 @@ void oracle_carbon(const or_stats *st, double ce_new_g, double ce_old_g, double 
     out[2] = op + emb;
 }
 
+/*
+ * §5 carbon-efficiency analysis for one
+ * (Case 2 = disaggregated chain d, Case 1 = Standalone chain s) pair under one
+ * scenario (carbon intensity alpha = ci, lifetimes T_A = lt_new, T_B = lt_old).
+ * Case totals are Eqs. 1-3 with the fixed expression of R34 (oracle_carbon):
+ *   out[0] ratio     = (O_A' + E_A' + O_B + E_B) / (O_A + E_A)   (Eq. 5, first line)
+ *   out[1] op_saved  = O_A - (O_A' + O_B)      grams (Fig. 9 right / Fig. 14 split)
+ *   out[2] emb_saved = E_A - (E_A' + E_B)      grams
+ *   out[3] eq6_term  = (t_B/T_B * B) / (N_A * alpha + (t_A'/T_A) * A)   (Eq. 6 as printed,
+ *                      R49: its index slip kept -- an approximation, never the decision)
+ * and *eq4 = (N_A > N_A' + N_B) on integer energies (Eq. 4 with E read as energy N, G1).
+ */
+void oracle_savings(const or_stats *d, double ce_new_d, double ce_old_d, const or_stats *s,
+                    double ce_new_s, double ce_old_s, double ci, double lt_new_s, double lt_old_s,
+                    double out[4], int32_t *eq4)
+{
+    double cd[3], cs[3];
+    oracle_carbon(d, ce_new_d, ce_old_d, ci, lt_new_s, lt_old_s, cd);
+    oracle_carbon(s, ce_new_s, ce_old_s, ci, lt_new_s, lt_old_s, cs);
+    out[0] = cd[2] / cs[2];
+    out[1] = cs[0] - cd[0];
+    out[2] = cs[1] - cd[1];
+    double n_a = (double)s->e_new_uj / 3.6e12 + (double)s->e_old_uj / 3.6e12;
+    double e_b = ((double)d->busy_old_us / 1e6) / lt_old_s * ce_old_d;
+    double e_a2 = ((double)d->busy_new_us / 1e6) / lt_new_s * ce_new_d;
+    out[3] = e_b / (n_a * ci + e_a2);
+    *eq4 = (s->e_new_uj + s->e_old_uj) > (d->e_new_uj + d->e_old_uj);
+}
+
 /* attainment comparison by cross-multiplication: sign(ok1/n1 - ok2/n2) */
 static int or_cmp_att(int64_t ok1, int64_t n1, int64_t ok2, int64_t n2)
 {

@@ -74,6 +74,11 @@ def lib():
             L.oracle_carbon.restype = None
             L.oracle_carbon.argtypes = [C.POINTER(OrStats), C.c_double, C.c_double, C.c_double,
                                         C.c_double, C.c_double, C.POINTER(C.c_double)]
+            L.oracle_savings.restype = None
+            L.oracle_savings.argtypes = [C.POINTER(OrStats), C.c_double, C.c_double,
+                                         C.POINTER(OrStats), C.c_double, C.c_double,
+                                         C.c_double, C.c_double, C.c_double,
+                                         C.POINTER(C.c_double), C.POINTER(C.c_int32)]
             L.oracle_alg1.restype = None
             L.oracle_alg1.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
@@ -185,6 +190,43 @@ def carbon(stats: dict, ce_new_g: float, ce_old_g: float, ci: float, lt_new_s: f
     lib().oracle_carbon(C.byref(_stats_struct(stats)), ce_new_g, ce_old_g, ci, lt_new_s,
                         lt_old_s, out)
     return out[0], out[1], out[2]
+
+
+def savings(stats_d: dict, ce_d, stats_s: dict, ce_s, ci: float, lt_new_s: float,
+            lt_old_s: float):
+    """§5 analysis for one (disaggregated d, Standalone s) pair and scenario:
+    dict(ratio, op_saved_g, emb_saved_g, eq6_term, eq4).  ce_d / ce_s = (ce_new, ce_old)."""
+    out = (C.c_double * 4)()
+    eq4 = C.c_int32()
+    lib().oracle_savings(C.byref(_stats_struct(stats_d)), ce_d[0], ce_d[1],
+                         C.byref(_stats_struct(stats_s)), ce_s[0], ce_s[1], ci, lt_new_s,
+                         lt_old_s, out, C.byref(eq4))
+    return dict(ratio=out[0], op_saved_g=out[1], emb_saved_g=out[2], eq6_term=out[3],
+                eq4=int(eq4.value))
+
+
+def savings_surface(grid, pairs, stats=None):
+    """Oracle surfaces over (pair, scenario): arrays [P, S] of ratio, op_saved_g,
+    emb_saved_g, eq6_term (f64) and eq4 (int32).  ``stats`` = {chain: stats dict}
+    (simulated here when absent)."""
+    need = sorted({c for pr in pairs for c in pr})
+    if stats is None:
+        stats = {}
+    for ci in need:
+        if ci not in stats:
+            ch = grid.chains[ci]
+            stats[ci] = simulate_chain(grid.traces[ch.trace_idx], ch, per_request=False)[0]
+    P, S = len(pairs), len(grid.scenarios)
+    out = {k: np.zeros((P, S)) for k in ("ratio", "op_saved_g", "emb_saved_g", "eq6_term")}
+    out["eq4"] = np.zeros((P, S), np.int32)
+    for i, (d, s) in enumerate(pairs):
+        cd, cs = grid.chains[d], grid.chains[s]
+        for j, sc in enumerate(grid.scenarios):
+            r = savings(stats[d], (cd.ce_new_g, cd.ce_old_g), stats[s], (cs.ce_new_g, cs.ce_old_g),
+                        float(sc[0]), float(sc[1]), float(sc[2]))
+            for k in out:
+                out[k][i, j] = r[k]
+    return out
 
 
 def alg1(total, ok, n, present, cap_ok, slo_num=9, slo_den=10, priority=0, default_col=-1):

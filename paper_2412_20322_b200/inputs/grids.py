@@ -254,6 +254,14 @@ def config6(n: int = 100_000, cap: int = 16, rates=RATES8) -> GridSpec:
                     workload="chat")
 
 
+def savings_pairs(grid: GridSpec):
+    """§5 analysis pairs (NEXT #3): every non-Standalone chain (Case 2) with the
+    Standalone chain on the same trace (Case 1)."""
+    base = {c.trace_idx: i for i, c in enumerate(grid.chains) if c.mode == MODE_STANDALONE}
+    return [(i, base[c.trace_idx]) for i, c in enumerate(grid.chains)
+            if c.mode != MODE_STANDALONE and c.trace_idx in base]
+
+
 CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5, 6: config6}
 
 
