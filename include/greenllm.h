@@ -250,6 +250,40 @@ gl_status gl_link_demand(const gl_trace *traces, int32_t n_traces, const gl_chai
                          int32_t n_chains, const gl_link_params *params, int64_t window_us,
                          gl_chain_stats *stats_out, gl_link_stats *link_out, void *stream);
 
+/* ---- §5 carbon-efficiency analysis surfaces.
+ * Case 1 (Standalone): the service on the new GPU A alone; Case 2
+ * (disaggregation): the same trace on A and an old GPU B (or any other
+ * candidate chain).  Per (pair, scenario), with Case totals from Eqs. 1-3 in the
+ * fixed R34 order (bit-identical to gl_argmin_feasible's carbon):
+ *   ratio       Eq. 5 first line (O_A' + E_A' + O_B + E_B) / (O_A + E_A);
+ *               carbon savings = 1 - ratio
+ *   op_saved_g  O_A - (O_A' + O_B);  emb_saved_g  E_A - (E_A' + E_B)  (grams)
+ *   eq6_term    (t_B/T_B * B) / (N_A * alpha + (t_A'/T_A) * A), Eq. 6's variable
+ *               term exactly as printed (R49: an approximation; never decisive)
+ *   eq4_energy_less  1 iff N_A > N_A' + N_B (Eq. 4, integer energies) */
+typedef struct {
+    int32_t disagg_chain;      /* Case 2 chain index */
+    int32_t standalone_chain;  /* Case 1 chain index */
+} gl_savings_pair;
+
+typedef struct {
+    double ratio, op_saved_g, emb_saved_g, eq6_term;
+    int32_t eq4_energy_less, pad;
+} gl_savings;              /* 40 B */
+
+/*
+ *   stats      DEVICE [n_chains] (e.g. from gl_eval_grid)
+ *   chains     HOST [n_chains] (ce_new_g, ce_old_g are read)
+ *   pairs      HOST [n_pairs];  scen HOST [n_scen]
+ *   out        DEVICE [n_pairs * n_scen], pair-major (out[p * n_scen + s])
+ * Errors: GL_E_INVALID for NULL / non-positive counts, GL_E_LOOKUP for a chain
+ * index out of range, GL_E_DOMAIN as gl_argmin_feasible for scenarios and Ce.
+ */
+gl_status gl_savings_surface(const gl_chain_stats *stats, int32_t n_chains,
+                             const gl_chain *chains, const gl_savings_pair *pairs,
+                             int32_t n_pairs, const gl_scenario *scen, int32_t n_scen,
+                             gl_savings *out, void *stream);
+
 /* Number of CUDA kernels the last successful call on this thread enqueued. */
 int32_t gl_last_launch_count(void);
 

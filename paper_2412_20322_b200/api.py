@@ -123,6 +123,28 @@ def link_demand(dg: DeviceGrid, window_us: int = 1_000_000, chain_lo: int = 0,
     return stats, link
 
 
+def savings_surface(dg: DeviceGrid, stats: torch.Tensor, pairs=None, scenarios=None,
+                    stream=None):
+    """§5 analysis surfaces (gl_savings_surface; NEXT #3) over (pair, scenario):
+    uint8 tensor [P, S, 40] of gl_savings records.  ``pairs`` defaults to every
+    non-Standalone chain against the Standalone chain on its trace."""
+    from .inputs import savings_pairs
+    pairs = savings_pairs(dg.grid) if pairs is None else pairs
+    scen = dg.grid.scenarios if scenarios is None else scenarios
+    S = len(np.asarray(scen).reshape(-1, 3))
+    out = torch.empty((len(pairs), S, N.SAVINGS_DTYPE.itemsize), dtype=torch.uint8,
+                      device=dg.device)
+    dg.last_launches = N.savings_surface(stats.data_ptr(), dg.gl_chains, pairs, scen,
+                                         out.data_ptr(), _stream_ptr(stream))
+    return out
+
+
+def savings_numpy(out: torch.Tensor) -> np.ndarray:
+    """Device savings tensor [P, S, 40] -> numpy structured array [P, S]."""
+    x = out.detach().cpu().numpy()
+    return x.reshape(x.shape[0], -1).view(N.SAVINGS_DTYPE).reshape(x.shape[0], x.shape[1])
+
+
 def link_numpy(link: torch.Tensor) -> np.ndarray:
     """Device link tensor -> numpy structured array (gl_link_stats fields)."""
     return link.detach().cpu().numpy().view(N.LINK_DTYPE).reshape(-1)

@@ -44,6 +44,7 @@
 #include "k_stages.cuh"
 #include "k_dsd_demand.cuh"
 #include "k_link.cuh"
+#include "k_savings.cuh"
 
 namespace {
 
@@ -275,7 +276,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         off_links = total;
         total += align256(sizeof(gl::DLink) * (size_t)n_chains);
         off_part = total;
-        total += align256(sizeof(longlong2) * gl::LINK_BLOCKS * (size_t)n_chains);
+        total += align256(sizeof(longlong2) * (gl::LINK_BLOCKS + 1) * (size_t)n_chains);
         off_lstats = total;
         if (!stats_out) total += align256(sizeof(gl_chain_stats) * (size_t)n_chains);
     }
@@ -330,7 +331,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             L.pm = lk->params[i].bytes_per_member_step;
             L.it_pre = reinterpret_cast<int64_t *>(scratch + off_itpre) + ev_off[i];
             L.req_pre = reinterpret_cast<int64_t *>(scratch + off_rqpre) + rq_off[i];
-            L.part = reinterpret_cast<longlong2 *>(scratch + off_part) + (size_t)gl::LINK_BLOCKS * i;
+            L.part = reinterpret_cast<longlong2 *>(scratch + off_part) + (size_t)(gl::LINK_BLOCKS + 1) * i;
             L.ev_cap = 2 * tr.n + 16;
         }
         d.n = tr.n;
@@ -556,6 +557,61 @@ gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains, cons
             reinterpret_cast<const int32_t *>(scratch + o_rows),
             reinterpret_cast<const int32_t *>(scratch + o_cells), (int32_t)rows, (int32_t)cols,
             slo_num, slo_den, priority, default_col, carbon_out, choice_out, via_fallback_out);
+        e = cudaGetLastError();
+        prof_end(stream);
+    }
+    cudaError_t ef = cudaFreeAsync(scratch, stream);
+    if (e == cudaSuccess) e = ef;
+    if (e != cudaSuccess) return GL_E_CUDA;
+    g_last_launches = 1;
+    return GL_OK;
+}
+
+gl_status gl_savings_surface(const gl_chain_stats *stats, int32_t n_chains,
+                             const gl_chain *chains, const gl_savings_pair *pairs,
+                             int32_t n_pairs, const gl_scenario *scen, int32_t n_scen,
+                             gl_savings *out, void *stream_)
+{
+    g_last_launches = 0;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    if (!stats || n_chains <= 0 || !chains || !pairs || n_pairs <= 0 || !scen || n_scen <= 0 ||
+        !out)
+        return GL_E_INVALID;
+    for (int32_t i = 0; i < n_scen; ++i) {
+        const gl_scenario &s = scen[i];
+        if (!(std::isfinite(s.ci_g_per_kwh) && s.ci_g_per_kwh >= 0.0)) return GL_E_DOMAIN;
+        if (!(std::isfinite(s.lt_new_s) && s.lt_new_s > 0.0)) return GL_E_DOMAIN;
+        if (!(std::isfinite(s.lt_old_s) && s.lt_old_s > 0.0)) return GL_E_DOMAIN;
+    }
+    std::vector<gl::DPairC> pc(n_pairs);
+    for (int32_t i = 0; i < n_pairs; ++i) {
+        const int32_t d = pairs[i].disagg_chain, sa = pairs[i].standalone_chain;
+        if (d < 0 || d >= n_chains || sa < 0 || sa >= n_chains) return GL_E_LOOKUP;
+        for (int32_t c : {d, sa}) {
+            if (!(std::isfinite(chains[c].ce_new_g) && chains[c].ce_new_g > 0.0)) return GL_E_DOMAIN;
+            if (!(std::isfinite(chains[c].ce_old_g) && chains[c].ce_old_g >= 0.0)) return GL_E_DOMAIN;
+        }
+        pc[i] = gl::DPairC{d, sa, chains[d].ce_new_g, chains[d].ce_old_g, chains[sa].ce_new_g,
+                           chains[sa].ce_old_g};
+    }
+    gl_status st = device_check();
+    if (st) return st;
+    const size_t o_scen = align256(sizeof(gl::DPairC) * n_pairs);
+    const size_t total = o_scen + align256(sizeof(gl_scenario) * n_scen);
+    unsigned char *scratch = nullptr;
+    if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
+        return st;
+    cudaError_t e = cudaMemcpyAsync(scratch, pc.data(), sizeof(gl::DPairC) * n_pairs,
+                                    cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess)
+        e = cudaMemcpyAsync(scratch + o_scen, scen, sizeof(gl_scenario) * n_scen,
+                            cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess) {
+        const int64_t cells = (int64_t)n_pairs * n_scen;
+        prof_begin("k_savings", stream);
+        gl::k_savings<<<(unsigned)((cells + 255) / 256), 256, 0, stream>>>(
+            stats, reinterpret_cast<const gl::DPairC *>(scratch),
+            reinterpret_cast<const gl_scenario *>(scratch + o_scen), n_pairs, n_scen, out);
         e = cudaGetLastError();
         prof_end(stream);
     }

@@ -29,7 +29,7 @@ struct DLink {
     int64_t bpt, pm;     // bytes per prompt token (+1), bytes per member-step
     int64_t *req_pre;    // [n + 1] exclusive prefix of request payload bytes
     int64_t *it_pre;     // [ev_cap + 1] exclusive prefix of iteration payload bytes
-    longlong2 *part;     // [LINK_BLOCKS] per-block (peak, t)
+    longlong2 *part;     // [LINK_BLOCKS + 1] per-block (peak, t); [LINK_BLOCKS].x = iteration impulses
     int64_t ev_cap;
 };
 
@@ -90,13 +90,18 @@ __global__ void __launch_bounds__(1024)
     const int32_t ne = ch.x->n_ev;
     const int64_t n = req ? ch.n : (int64_t)ne;
     int64_t *out = req ? lk.req_pre : lk.it_pre;
-    int64_t carry = 0;
+    int64_t carry = 0, cnt = 0;
     for (int64_t base = 0; base < n; base += 1024) {
         const int64_t i = base + threadIdx.x;
         int64_t v = 0;
         if (i < n) {
-            if (req) v = link_req_bytes(ch, lk, i);
-            else v = link_iters(ch, ch.ev, ne, (int32_t)i) * ch.ev[i].y * lk.pm;
+            if (req) {
+                v = link_req_bytes(ch, lk, i);
+            } else {
+                const int64_t k = link_iters(ch, ch.ev, ne, (int32_t)i);
+                v = k * ch.ev[i].y * lk.pm;
+                cnt += v > 0 ? k : 0;  // iteration impulses with a payload
+            }
         }
         int64_t tot;
         const int64_t ex = block_excl_scan(v, tot, sw);
@@ -104,6 +109,11 @@ __global__ void __launch_bounds__(1024)
         carry += tot;
     }
     if (threadIdx.x == 0) out[n] = carry;
+    if (!req) {
+        int64_t tot;
+        block_excl_scan(cnt, tot, sw);
+        if (threadIdx.x == 0) lk.part[LINK_BLOCKS] = make_longlong2(tot, 0);
+    }
 }
 
 // first index in [lo, hi) whose key >= x (keys non-decreasing)
@@ -227,12 +237,9 @@ __global__ void k_link_reduce(const DChain *__restrict__ chains, const DLink *__
             const int64_t v = __shfl_xor_sync(FULL, bv, o), t = __shfl_xor_sync(FULL, bt, o);
             link_better(bv, bt, v, t);
         }
-        // impulse count: requests with a payload, iteration starts with one
+        // impulse count: requests with a payload, iteration starts with one (k_link_scan)
         const int32_t ne = ch.x->n_ev;
-        int64_t cnt = 0;
-        for (int32_t e = lane; e < ne; e += 32)
-            if (ch.ev[e].y * lk.pm > 0) cnt += link_iters(ch, ch.ev, ne, e);
-        cnt = warp_sum_i64(cnt);
+        const int64_t cnt = lk.part[LINK_BLOCKS].x;
         const int64_t nreq = lk.bpt > 0 ? (int64_t)ch.x->M : 0;
         r.total_bytes = lk.req_pre[ch.n] + lk.it_pre[ne];
         r.n_impulses = nreq + cnt;

@@ -64,9 +64,20 @@ class GlLinkParams(C.Structure):
     _fields_ = [("bytes_per_token", C.c_int64), ("bytes_per_member_step", C.c_int64)]
 
 
+# gl_savings (40 B) and gl_savings_pair
+SAVINGS_DTYPE = np.dtype([("ratio", "<f8"), ("op_saved_g", "<f8"), ("emb_saved_g", "<f8"),
+                          ("eq6_term", "<f8"), ("eq4_energy_less", "<i4"), ("pad", "<i4")])
+assert SAVINGS_DTYPE.itemsize == 40
+
+
+class GlSavingsPair(C.Structure):
+    _fields_ = [("disagg_chain", C.c_int32), ("standalone_chain", C.c_int32)]
+
+
 SCEN_DTYPE = np.dtype([("ci", "<f8"), ("lt_new", "<f8"), ("lt_old", "<f8")])
 
-EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_link_demand", "gl_last_launch_count",
+EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_link_demand",
+           "gl_savings_surface", "gl_last_launch_count",
            "gl_profile_enable", "gl_kernel_times", "gl_strerror", "gl_version")
 
 _lib = None
@@ -99,6 +110,9 @@ def lib():
         L.gl_link_demand.restype = i32
         L.gl_link_demand.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
                                      C.POINTER(GlLinkParams), C.c_int64, vp, vp, vp]
+        L.gl_savings_surface.restype = i32
+        L.gl_savings_surface.argtypes = [vp, i32, C.POINTER(GlChain), C.POINTER(GlSavingsPair),
+                                         i32, C.POINTER(GlScenario), i32, vp, vp]
         L.gl_last_launch_count.restype = i32
         L.gl_last_launch_count.argtypes = []
         L.gl_profile_enable.restype = i32
@@ -134,6 +148,16 @@ def link_demand(traces, chains, params, window_us: int, stats_ptr: int | None, l
     p_arr = (GlLinkParams * len(chains))(*[GlLinkParams(int(a), int(b)) for a, b in params])
     check(lib().gl_link_demand(t_arr, len(traces), c_arr, len(chains), p_arr, int(window_us),
                                stats_ptr or None, link_ptr, stream or None), "gl_link_demand")
+    return lib().gl_last_launch_count()
+
+
+def savings_surface(stats_ptr: int, chains, pairs, scen: np.ndarray, out_ptr: int, stream: int):
+    c_arr = (GlChain * len(chains))(*chains)
+    p_arr = (GlSavingsPair * len(pairs))(*[GlSavingsPair(int(d), int(s)) for d, s in pairs])
+    sc = np.ascontiguousarray(scen, dtype=np.float64).reshape(-1, 3)
+    s_arr = (GlScenario * len(sc))(*[GlScenario(*map(float, x)) for x in sc])
+    check(lib().gl_savings_surface(stats_ptr, len(chains), c_arr, p_arr, len(pairs), s_arr,
+                                   len(sc), out_ptr, stream or None), "gl_savings_surface")
     return lib().gl_last_launch_count()
 
 

@@ -27,7 +27,7 @@ def declared_functions():
 
 def test_header_declares_expected_calls():
     assert declared_functions() == sorted(["gl_eval_grid", "gl_argmin_feasible",
-                                           "gl_evaluate_host", "gl_link_demand",
+                                           "gl_evaluate_host", "gl_link_demand", "gl_savings_surface",
                                            "gl_last_launch_count",
                                            "gl_profile_enable", "gl_kernel_times",
                                            "gl_strerror", "gl_version"])
@@ -65,6 +65,8 @@ int main(void){
  printf("%zu %zu\n", offsetof(gl_chain_stats, req_hash), offsetof(gl_chain_stats, status));
  printf("%zu %zu %zu\n", sizeof(gl_link_params), sizeof(gl_link_stats),
         offsetof(gl_link_stats, peak_t_us));
+ printf("%zu %zu %zu\n", sizeof(gl_savings_pair), sizeof(gl_savings),
+        offsetof(gl_savings, eq4_energy_less));
  return 0;}
 """
     import tempfile
@@ -86,6 +88,9 @@ int main(void){
     lo = list(map(int, lines[3].split()))
     assert lo == [C.sizeof(N.GlLinkParams), N.LINK_DTYPE.itemsize,
                   N.LINK_DTYPE.fields["peak_t_us"][1]]
+    sv = list(map(int, lines[4].split()))
+    assert sv == [C.sizeof(N.GlSavingsPair), N.SAVINGS_DTYPE.itemsize,
+                  N.SAVINGS_DTYPE.fields["eq4_energy_less"][1]]
 
 
 def test_calls_fail_loudly_without_gpu(built):
@@ -112,6 +117,16 @@ def test_calls_fail_loudly_without_gpu(built):
     assert ei.value.status == built.GL_E_INVALID
     with pytest.raises(built.GreenLLMError) as ei:
         built.link_demand([tr], [ch], [(-1, 100)], 10, None, 16, 0)
+    assert ei.value.status == built.GL_E_DOMAIN
+    ch.ce_new_g, ch.ce_old_g = 1.0, 0.0
+    scen = [[261.0, 1.0, 1.0]]
+    with pytest.raises(built.GreenLLMError):  # no device
+        built.savings_surface(16, [ch], [(0, 0)], scen, 16, 0)
+    with pytest.raises(built.GreenLLMError) as ei:
+        built.savings_surface(16, [ch], [(0, 1)], scen, 16, 0)
+    assert ei.value.status == built.GL_E_LOOKUP
+    with pytest.raises(built.GreenLLMError) as ei:
+        built.savings_surface(16, [ch], [(0, 0)], [[261.0, 0.0, 1.0]], 16, 0)
     assert ei.value.status == built.GL_E_DOMAIN
 
 
