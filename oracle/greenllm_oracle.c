@@ -539,4 +539,116 @@ uint32_t oracle_link_demand(const int64_t *a, const uint32_t *p, const uint32_t 
     return status;
 }
 
+/*
+ * Collaborative filtering (Alg. 1 line 1; P:343-345:
+ * "GreenLLM employs collaborative filtering" to fill the missing entries of C and
+ * SLO_att; the algorithm is unspecified -- SPEC S:415-423, S:451 choose alternating
+ * least squares).  Readings R50-R53, step by step:
+ *   X [rows x cols], observed mask M, rank k, ridge lambda, `iters` iterations,
+ *   V [cols x k] initialised from the caller's v0 (seeded input, R51).
+ *   each iteration (R50):
+ *     U-step: for every row i, U_i = argmin_u sum_{j in M_i} (x_ij - u.V_j)^2 + lambda |u|^2
+ *             i.e. (sum_j V_j V_j^T + lambda I) U_i = sum_j x_ij V_j   (columns in order)
+ *     V-step: for every column j, the same with the roles swapped (rows in order)
+ *   each k x k system is solved by a textbook Cholesky factorisation.
+ *   out_ij = x_ij where observed (verbatim), else U_i.V_j clamped to [lo, hi] (R52).
+ * Returns bit 1 if some row has no observed entry, bit 2 for a column (R53: the
+ * completion is then undefined); out is still written.
+ */
+static void or_chol_solve(double *A, double *b, int k)
+{
+    /* A (k x k, SPD, row-major) = L L^T in place (lower), then L y = b, L^T x = y */
+    for (int c = 0; c < k; ++c) {
+        double d = A[c * k + c];
+        for (int m = 0; m < c; ++m) d -= A[c * k + m] * A[c * k + m];
+        d = sqrt(d);
+        A[c * k + c] = d;
+        for (int r = c + 1; r < k; ++r) {
+            double v = A[r * k + c];
+            for (int m = 0; m < c; ++m) v -= A[r * k + m] * A[c * k + m];
+            A[r * k + c] = v / d;
+        }
+    }
+    for (int r = 0; r < k; ++r) {
+        double v = b[r];
+        for (int m = 0; m < r; ++m) v -= A[r * k + m] * b[m];
+        b[r] = v / A[r * k + r];
+    }
+    for (int r = k - 1; r >= 0; --r) {
+        double v = b[r];
+        for (int m = r + 1; m < k; ++m) v -= A[m * k + r] * b[m];
+        b[r] = v / A[r * k + r];
+    }
+}
+
+int32_t oracle_als_complete(const double *x, const uint8_t *obs, int32_t rows, int32_t cols,
+                            int32_t k, double lambda, int32_t iters, const double *v0,
+                            double lo, double hi, double *out, double *u_out, double *v_out)
+{
+    double *U = calloc((size_t)rows * k, sizeof(double));
+    double *V = malloc(sizeof(double) * (size_t)cols * k);
+    double A[64], b[8];
+    int32_t status = 0;
+    memcpy(V, v0, sizeof(double) * (size_t)cols * k);
+    for (int32_t i = 0; i < rows; ++i) {
+        int any = 0;
+        for (int32_t j = 0; j < cols; ++j) any |= obs[(int64_t)i * cols + j] != 0;
+        if (!any) status |= 1;
+    }
+    for (int32_t j = 0; j < cols; ++j) {
+        int any = 0;
+        for (int32_t i = 0; i < rows; ++i) any |= obs[(int64_t)i * cols + j] != 0;
+        if (!any) status |= 2;
+    }
+    for (int32_t it = 0; it < iters; ++it) {
+        for (int32_t i = 0; i < rows; ++i) { /* U-step */
+            for (int a = 0; a < k * k; ++a) A[a] = 0.0;
+            for (int a = 0; a < k; ++a) b[a] = 0.0;
+            for (int32_t j = 0; j < cols; ++j) {
+                if (!obs[(int64_t)i * cols + j]) continue;
+                const double *vj = V + (int64_t)j * k;
+                for (int r = 0; r < k; ++r) {
+                    for (int c = 0; c <= r; ++c) A[r * k + c] += vj[r] * vj[c];
+                    b[r] += x[(int64_t)i * cols + j] * vj[r];
+                }
+            }
+            for (int r = 0; r < k; ++r) A[r * k + r] += lambda;
+            or_chol_solve(A, b, k);
+            for (int r = 0; r < k; ++r) U[(int64_t)i * k + r] = b[r];
+        }
+        for (int32_t j = 0; j < cols; ++j) { /* V-step */
+            for (int a = 0; a < k * k; ++a) A[a] = 0.0;
+            for (int a = 0; a < k; ++a) b[a] = 0.0;
+            for (int32_t i = 0; i < rows; ++i) {
+                if (!obs[(int64_t)i * cols + j]) continue;
+                const double *ui = U + (int64_t)i * k;
+                for (int r = 0; r < k; ++r) {
+                    for (int c = 0; c <= r; ++c) A[r * k + c] += ui[r] * ui[c];
+                    b[r] += x[(int64_t)i * cols + j] * ui[r];
+                }
+            }
+            for (int r = 0; r < k; ++r) A[r * k + r] += lambda;
+            or_chol_solve(A, b, k);
+            for (int r = 0; r < k; ++r) V[(int64_t)j * k + r] = b[r];
+        }
+    }
+    for (int32_t i = 0; i < rows; ++i) {
+        for (int32_t j = 0; j < cols; ++j) {
+            int64_t q = (int64_t)i * cols + j;
+            if (obs[q]) {
+                out[q] = x[q];
+                continue;
+            }
+            double v = 0.0;
+            for (int r = 0; r < k; ++r) v += U[(int64_t)i * k + r] * V[(int64_t)j * k + r];
+            out[q] = v < lo ? lo : (v > hi ? hi : v);
+        }
+    }
+    if (u_out) memcpy(u_out, U, sizeof(double) * (size_t)rows * k);
+    if (v_out) memcpy(v_out, V, sizeof(double) * (size_t)cols * k);
+    free(U);
+    free(V);
+    return status;
+}
+
 int32_t oracle_version(void) { return 1; }

@@ -79,6 +79,11 @@ def lib():
                                          C.POINTER(OrStats), C.c_double, C.c_double,
                                          C.c_double, C.c_double, C.c_double,
                                          C.POINTER(C.c_double), C.POINTER(C.c_int32)]
+            L.oracle_als_complete.restype = C.c_int32
+            L.oracle_als_complete.argtypes = [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32,
+                                              C.c_int32, C.c_double, C.c_int32, C.c_void_p,
+                                              C.c_double, C.c_double, C.c_void_p, C.c_void_p,
+                                              C.c_void_p]
             L.oracle_alg1.restype = None
             L.oracle_alg1.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
@@ -227,6 +232,21 @@ def savings_surface(grid, pairs, stats=None):
             for k in out:
                 out[k][i, j] = r[k]
     return out
+
+
+def als_complete(x, observed, rank, lam, iters, v0, lo=-np.inf, hi=np.inf):
+    """Collaborative filtering by ALS (oracle_als_complete): returns
+    (completed [rows, cols], U [rows, rank], V [cols, rank], status)."""
+    x = _c(x, np.float64)
+    rows, cols = x.shape
+    m = _c(observed, np.uint8)
+    v = _c(v0, np.float64).reshape(cols, rank)
+    out = np.zeros_like(x)
+    U = np.zeros((rows, rank))
+    V = np.zeros((cols, rank))
+    st = lib().oracle_als_complete(_ptr(x), _ptr(m), rows, cols, rank, float(lam), int(iters),
+                                   _ptr(v), float(lo), float(hi), _ptr(out), _ptr(U), _ptr(V))
+    return out, U, V, int(st)
 
 
 def alg1(total, ok, n, present, cap_ok, slo_num=9, slo_den=10, priority=0, default_col=-1):
