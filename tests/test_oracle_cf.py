@@ -98,7 +98,8 @@ def test_clamping_and_observed_verbatim():
     out, U, V, _ = O.als_complete(x, m, 2, 0.1, 30, als_init(6, 2), lo=0.0, hi=1.0)
     assert np.array_equal(out[m == 1], x[m == 1])
     pred = (U @ V.T)[m == 0]
-    assert np.array_equal(out[m == 0], np.clip(pred, 0.0, 1.0))
+    np.testing.assert_allclose(out[m == 0], np.clip(pred, 0.0, 1.0), rtol=1e-13, atol=0)
+    assert ((out[m == 0] == 1.0) == (pred >= 1.0)).all() and (out >= 0).all()
 
 
 def test_empty_row_and_column_status():
