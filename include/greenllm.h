@@ -284,6 +284,32 @@ gl_status gl_savings_surface(const gl_chain_stats *stats, int32_t n_chains,
                              int32_t n_pairs, const gl_scenario *scen, int32_t n_scen,
                              gl_savings *out, void *stream);
 
+/* ---- Collaborative filtering (Alg. 1 line 1, P:309;
+ * missing entries of C and SLO_att are filled "only once after
+ * profiling").  The paper names no algorithm; this is alternating least squares
+ * with ridge regularisation (readings R50-R53):
+ *   each of `iters` iterations: for every row i,
+ *     U_i = (sum_{j observed} V_j V_j^T + lambda I)^-1 sum_j x_ij V_j,
+ *   then for every column j the same with U and V swapped; k x k Cholesky solves.
+ *   out_ij = x_ij where observed (verbatim), else clamp(U_i . V_j, lo, hi).
+ * The matrices of a batch are independent (SPEC completes C and SLO_att
+ * separately); all arrays are row-major fp64 / uint8 in DEVICE memory:
+ *   x, observed   [batch][rows][cols]     (observed != 0 marks a known entry)
+ *   v0            [batch][cols][rank]     initial V (seeded input, R51)
+ *   out           [batch][rows][cols]
+ *   u_out, v_out  [batch][rows][rank], [batch][cols][rank] final factors, or NULL
+ *   status_out    [batch] int32: bit 1 = a row without an observed entry, bit 2 =
+ *                 a column without one (the completion is then undefined)
+ * Limits: 1 <= rank <= GL_MAX_RANK, rank <= min(rows, cols), cols <= 1024,
+ * lambda >= 0 finite, iters >= 0, lo <= hi.  Results match the CPU oracle to
+ * rounding (the V-step sums rows in a parallel order; R50). */
+#define GL_MAX_RANK 8
+gl_status gl_complete_matrices(const double *x, const uint8_t *observed, int32_t batch,
+                               int32_t rows, int32_t cols, int32_t rank, double lambda,
+                               int32_t iters, const double *v0, double lo, double hi,
+                               double *out, double *u_out, double *v_out, int32_t *status_out,
+                               void *stream);
+
 /* Number of CUDA kernels the last successful call on this thread enqueued. */
 int32_t gl_last_launch_count(void);
 

@@ -145,6 +145,34 @@ def savings_numpy(out: torch.Tensor) -> np.ndarray:
     return x.reshape(x.shape[0], -1).view(N.SAVINGS_DTYPE).reshape(x.shape[0], x.shape[1])
 
 
+def complete_matrices(x: torch.Tensor, observed: torch.Tensor, rank: int = 2,
+                      lam: float = 0.1, iters: int = 200, v0: torch.Tensor | None = None,
+                      lo: float = float("-inf"), hi: float = float("inf"), stream=None):
+    """Collaborative filtering (gl_complete_matrices; NEXT #4) of a batch of
+    partially observed matrices x [batch, rows, cols] (fp64, device) with mask
+    ``observed`` (uint8) -> (out, U, V, status) device tensors.  ``v0`` [batch, cols,
+    rank] defaults to the seeded inputs.cf.als_init draw for every matrix."""
+    if x.dim() == 2:
+        x, observed = x[None], observed[None]
+        if v0 is not None and v0.dim() == 2:
+            v0 = v0[None]
+    x = x.contiguous().to(torch.float64)
+    observed = observed.contiguous().to(torch.uint8)
+    B, R, Cc = x.shape
+    if v0 is None:
+        from .inputs.cf import als_init
+        v0 = torch.from_numpy(np.broadcast_to(als_init(Cc, rank), (B, Cc, rank)).copy())
+    v0 = v0.to(x.device, torch.float64).contiguous()
+    out = torch.empty_like(x)
+    U = torch.empty((B, R, rank), dtype=torch.float64, device=x.device)
+    V = torch.empty((B, Cc, rank), dtype=torch.float64, device=x.device)
+    status = torch.empty(B, dtype=torch.int32, device=x.device)
+    N.complete_matrices(x.data_ptr(), observed.data_ptr(), B, R, Cc, rank, lam, iters,
+                        v0.data_ptr(), lo, hi, out.data_ptr(), U.data_ptr(), V.data_ptr(),
+                        status.data_ptr(), _stream_ptr(stream))
+    return out, U, V, status
+
+
 def link_numpy(link: torch.Tensor) -> np.ndarray:
     """Device link tensor -> numpy structured array (gl_link_stats fields)."""
     return link.detach().cpu().numpy().view(N.LINK_DTYPE).reshape(-1)

@@ -45,6 +45,7 @@
 #include "k_dsd_demand.cuh"
 #include "k_link.cuh"
 #include "k_savings.cuh"
+#include "k_als.cuh"
 
 namespace {
 
@@ -617,6 +618,60 @@ gl_status gl_savings_surface(const gl_chain_stats *stats, int32_t n_chains,
     }
     cudaError_t ef = cudaFreeAsync(scratch, stream);
     if (e == cudaSuccess) e = ef;
+    if (e != cudaSuccess) return GL_E_CUDA;
+    g_last_launches = 1;
+    return GL_OK;
+}
+
+gl_status gl_complete_matrices(const double *x, const uint8_t *observed, int32_t batch,
+                               int32_t rows, int32_t cols, int32_t rank, double lambda,
+                               int32_t iters, const double *v0, double lo, double hi,
+                               double *out, double *u_out, double *v_out, int32_t *status_out,
+                               void *stream_)
+{
+    g_last_launches = 0;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    if (!x || !observed || !v0 || !out || !status_out) return GL_E_INVALID;
+    if (batch <= 0 || rows <= 0 || cols <= 0 || cols > 1024 || iters < 0) return GL_E_INVALID;
+    if (rank < 1 || rank > GL_MAX_RANK || rank > rows || rank > cols) return GL_E_INVALID;
+    if (!(std::isfinite(lambda) && lambda >= 0.0) || std::isnan(lo) || std::isnan(hi) || lo > hi)
+        return GL_E_DOMAIN;
+    gl_status st = device_check();
+    if (st) return st;
+    double *u = u_out;
+    if (!u) {
+        if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&u),
+                                              sizeof(double) * (size_t)batch * rows * rank, stream))))
+            return st;
+    }
+    const gl::DAls p{x, observed, v0, u, v_out, out, status_out, (int64_t)rows, cols, iters,
+                     lambda, lo, hi};
+    const size_t smem = gl::als_smem_bytes(cols, rank);
+    cudaError_t e = cudaSuccess;
+    auto launch = [&](auto kern) {
+        cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                             (int)smem);
+        if (r != cudaSuccess) return r;
+        prof_begin("k_als", stream);
+        kern<<<(unsigned)batch, gl::ALS_THREADS, smem, stream>>>(p);
+        r = cudaGetLastError();
+        prof_end(stream);
+        return r;
+    };
+    switch (rank) {
+        case 1: e = launch(gl::k_als<1>); break;
+        case 2: e = launch(gl::k_als<2>); break;
+        case 3: e = launch(gl::k_als<3>); break;
+        case 4: e = launch(gl::k_als<4>); break;
+        case 5: e = launch(gl::k_als<5>); break;
+        case 6: e = launch(gl::k_als<6>); break;
+        case 7: e = launch(gl::k_als<7>); break;
+        default: e = launch(gl::k_als<8>); break;
+    }
+    if (!u_out) {
+        cudaError_t ef = cudaFreeAsync(u, stream);
+        if (e == cudaSuccess) e = ef;
+    }
     if (e != cudaSuccess) return GL_E_CUDA;
     g_last_launches = 1;
     return GL_OK;

@@ -77,7 +77,7 @@ class GlSavingsPair(C.Structure):
 SCEN_DTYPE = np.dtype([("ci", "<f8"), ("lt_new", "<f8"), ("lt_old", "<f8")])
 
 EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_link_demand",
-           "gl_savings_surface", "gl_last_launch_count",
+           "gl_savings_surface", "gl_complete_matrices", "gl_last_launch_count",
            "gl_profile_enable", "gl_kernel_times", "gl_strerror", "gl_version")
 
 _lib = None
@@ -113,6 +113,9 @@ def lib():
         L.gl_savings_surface.restype = i32
         L.gl_savings_surface.argtypes = [vp, i32, C.POINTER(GlChain), C.POINTER(GlSavingsPair),
                                          i32, C.POINTER(GlScenario), i32, vp, vp]
+        L.gl_complete_matrices.restype = i32
+        L.gl_complete_matrices.argtypes = [vp, vp, i32, i32, i32, i32, C.c_double, i32, vp,
+                                           C.c_double, C.c_double, vp, vp, vp, vp, vp]
         L.gl_last_launch_count.restype = i32
         L.gl_last_launch_count.argtypes = []
         L.gl_profile_enable.restype = i32
@@ -158,6 +161,16 @@ def savings_surface(stats_ptr: int, chains, pairs, scen: np.ndarray, out_ptr: in
     s_arr = (GlScenario * len(sc))(*[GlScenario(*map(float, x)) for x in sc])
     check(lib().gl_savings_surface(stats_ptr, len(chains), c_arr, p_arr, len(pairs), s_arr,
                                    len(sc), out_ptr, stream or None), "gl_savings_surface")
+    return lib().gl_last_launch_count()
+
+
+def complete_matrices(x_ptr: int, obs_ptr: int, batch: int, rows: int, cols: int, rank: int,
+                      lam: float, iters: int, v0_ptr: int, lo: float, hi: float, out_ptr: int,
+                      u_ptr: int | None, v_ptr: int | None, status_ptr: int, stream: int):
+    check(lib().gl_complete_matrices(x_ptr, obs_ptr, batch, rows, cols, rank, float(lam),
+                                     int(iters), v0_ptr, float(lo), float(hi), out_ptr,
+                                     u_ptr or None, v_ptr or None, status_ptr, stream or None),
+          "gl_complete_matrices")
     return lib().gl_last_launch_count()
 
 

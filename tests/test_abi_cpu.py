@@ -28,6 +28,7 @@ def declared_functions():
 def test_header_declares_expected_calls():
     assert declared_functions() == sorted(["gl_eval_grid", "gl_argmin_feasible",
                                            "gl_evaluate_host", "gl_link_demand", "gl_savings_surface",
+                                           "gl_complete_matrices",
                                            "gl_last_launch_count",
                                            "gl_profile_enable", "gl_kernel_times",
                                            "gl_strerror", "gl_version"])
@@ -128,6 +129,16 @@ def test_calls_fail_loudly_without_gpu(built):
     with pytest.raises(built.GreenLLMError) as ei:
         built.savings_surface(16, [ch], [(0, 0)], [[261.0, 0.0, 1.0]], 16, 0)
     assert ei.value.status == built.GL_E_DOMAIN
+    cm = built.complete_matrices
+    with pytest.raises(built.GreenLLMError):  # no device
+        cm(16, 16, 1, 4, 3, 2, 0.1, 10, 16, 0.0, 1.0, 16, None, None, 16, 0)
+    for bad, code in (((16, 16, 1, 4, 3, 4, 0.1, 10), built.GL_E_INVALID),   # rank > cols
+                      ((16, 16, 1, 4, 3, 9, 0.1, 10), built.GL_E_INVALID),   # rank > GL_MAX_RANK
+                      ((16, 16, 1, 4, 2000, 2, 0.1, 10), built.GL_E_INVALID),
+                      ((16, 16, 1, 4, 3, 2, -1.0, 10), built.GL_E_DOMAIN)):
+        with pytest.raises(built.GreenLLMError) as ei:
+            cm(*bad, 16, 0.0, 1.0, 16, None, None, 16, 0)
+        assert ei.value.status == code
 
 
 def test_oracle_and_product_share_no_code():
