@@ -1,23 +1,32 @@
-"""Per-chain k_decode time of config 4 (one launch per chain)."""
-import sys, json
-import numpy as np, torch
+"""Per-chain decode time of config 4, one launch per chain: the speculative
+k_decode (gl_eval_grid) and the leader-only serial walk k_decode_log
+(gl_link_demand), plus the request count of the chain's decode stream."""
+import sys
+import numpy as np
+import torch
 sys.path.insert(0, '.')
 from paper_2412_20322_b200 import api, native as N
 from paper_2412_20322_b200.inputs import build_config
-from oracle import oracle as O
-g = build_config(4)
+cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+g = build_config(cfg)
 dg = api.DeviceGrid(g)
 N.profile_enable(True)
-out = []
 stats, _ = api.eval_grid(dg)
 torch.cuda.synchronize(); N.kernel_times()
+out = []
 for ci in range(len(g.chains)):
     st = torch.empty((1, 80), dtype=torch.uint8, device='cuda')
     api.eval_grid(dg, ci, ci + 1, stats=st)
     torch.cuda.synchronize()
     kt = dict(N.kernel_times())
-    s = api.stats_numpy(st)[0]
+    api.link_demand(dg, chain_lo=ci, chain_hi=ci + 1)
+    torch.cuda.synchronize()
+    kl = dict(N.kernel_times())
     ch = g.chains[ci]
-    out.append((kt['k_decode'], ci, ch.label, int(s['slo_ok']), int(s['makespan_us']), kt['k_stages']))
+    M = int((g.traces[ch.trace_idx].output_len > 1).sum())
+    dec = kt.get('k_decode', kt.get('k_decode_colo', 0.0))
+    walk = kl.get('k_decode_log', 0.0)
+    out.append((dec, walk, ci, ch.label, M))
 out.sort(reverse=True)
-for r in out: print("%.2f ms  chain %2d  %-50s ok=%d makespan=%.0fs  (k_stages %.2f ms)" % (r[0], r[1], r[2], r[3], r[4]/1e6, r[5]))
+for dec, walk, ci, lab, M in out:
+    print("%6.2f ms spec  %6.2f ms walk (%5.1f ns/request)  chain %2d  %s" % (dec, walk, 1e6 * walk / max(M, 1), ci, lab))
