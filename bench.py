@@ -307,7 +307,8 @@ def run_ours(args):
 
     analysis = None
     if world == 1 and not args.no_analysis:
-        analysis = {"link_demand": link_demand_bench(dg, grid, flush)}
+        analysis = {"link_demand": link_demand_bench(dg, grid, flush),
+                    **analysis_bench(dg, grid)}
 
     if rank != 0:
         if world > 1:
@@ -425,6 +426,53 @@ def link_demand_bench(dg, grid, flush, reps=3):
             "peak_gbps_range": {k: [min(v), max(v)] for k, v in gbps.items()},
             "note": "peak link demand of every chain (R45-R47); leader-only decode + "
                     "k_link_scan/window/reduce; outside the timed step"}
+
+
+def analysis_bench(dg, grid, reps=3):
+    """NEXT #3 / #4 (not part of the timed step), device time with CUDA events:
+    gl_savings_surface over config 6 (72 pairs x 1,024 scenarios) and
+    gl_complete_matrices on this workload's Alg. 1 matrices (carbon, attainment;
+    30% of the cells hidden; rank 2, lambda 0.1, 200 iterations)."""
+    import torch
+
+    from paper_2412_20322_b200 import api
+    from paper_2412_20322_b200.inputs import build_config
+    from paper_2412_20322_b200.inputs.cf import observation_mask
+
+    def timed(fn):
+        fn()
+        torch.cuda.synchronize()
+        ms = []
+        for _ in range(reps):
+            e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+            e0.record()
+            fn()
+            e1.record()
+            torch.cuda.synchronize()
+            ms.append(e0.elapsed_time(e1))
+        return sum(ms) / len(ms)
+
+    g6 = build_config(6, n=grid.traces[0].n)
+    dg6 = api.DeviceGrid(g6, dg.device)
+    stats6, _ = api.eval_grid(dg6)
+    sav_ms = timed(lambda: api.savings_surface(dg6, stats6))
+    stats, _ = api.eval_grid(dg)
+    carbon, _, _ = api.argmin_feasible(dg, stats)
+    st = api.stats_numpy(stats)
+    att = torch.from_numpy((st["slo_ok"] / st["n"])[grid.cell_chain]
+                           .reshape(grid.rows, grid.cols)).to(dg.device)
+    m = torch.from_numpy(observation_mask(grid.rows, grid.cols, 0.3, seed=42)).to(dg.device)
+    x, mm = torch.stack([carbon, att]), torch.stack([m, m])
+    cf_ms = timed(lambda: api.complete_matrices(x, mm, 2, 0.1, 200, lo=0.0))
+    return {"savings_surface": {"ms": sav_ms, "cells": len(api_pairs(g6)) * len(g6.scenarios),
+                                "workload": "cfg6: 72 (Case 2, Standalone) pairs x 1,024 (CI, T_A, T_B)"},
+            "complete_matrices": {"ms": cf_ms, "matrices": 2, "shape": [grid.rows, grid.cols],
+                                  "rank": 2, "iters": 200, "hidden": 0.3}}
+
+
+def api_pairs(g):
+    from paper_2412_20322_b200.inputs import savings_pairs
+    return savings_pairs(g)
 
 
 def e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush, dev):
