@@ -648,6 +648,63 @@ gl_status gl_complete_matrices(const double *x, const uint8_t *observed, int32_t
                      lambda, lo, hi};
     const size_t smem = gl::als_smem_bytes(cols, rank);
     cudaError_t e = cudaSuccess;
+    // small batches: P CTAs per matrix with a grid-wide barrier per iteration
+    // (cooperative launch), so the whole GPU works on a handful of matrices
+    int dev = 0, n_sm = 0, coop = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&n_sm, cudaDevAttrMultiProcessorCount, dev);
+    cudaDeviceGetAttribute(&coop, cudaDevAttrCooperativeLaunch, dev);
+    const size_t smem_c = sizeof(double) * (size_t)cols * rank;
+    auto launch_coop = [&](auto kern) -> cudaError_t {
+        int per_sm = 0;
+        cudaError_t r = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern,
+                                                                      gl::ALSC_THREADS, smem_c);
+        if (r != cudaSuccess) return r;
+        const int64_t fit = (int64_t)per_sm * n_sm;
+        int P = (int)std::min<int64_t>(fit / batch, (rows + 63) / 64);
+        P = std::min(P, 2 * n_sm);
+        if (P < 2) return cudaErrorNotSupported;  // the one-CTA kernel below
+        const int ns = rank * (rank + 1) / 2 + rank;
+        const int cw = (cols + 31) / 32;
+        const size_t part_b = sizeof(double) * 2 * (size_t)batch * P * cols * ns;
+        const size_t mask_b = sizeof(uint32_t) * (size_t)batch * cw + sizeof(int32_t) * batch;
+        unsigned char *scr = nullptr;
+        r = cudaMallocAsync(reinterpret_cast<void **>(&scr), align256(part_b) + mask_b, stream);
+        if (r != cudaSuccess) return r;
+        double *part = reinterpret_cast<double *>(scr);
+        uint32_t *cmask = reinterpret_cast<uint32_t *>(scr + align256(part_b));
+        int32_t *rflag = reinterpret_cast<int32_t *>(cmask + (size_t)batch * cw);
+        r = cudaMemsetAsync(cmask, 0, mask_b, stream);
+        if (r == cudaSuccess) {
+            gl::DAls pp = p;
+            int Pv = P;
+            void *args[] = {&pp, &part, &cmask, &rflag, &Pv};
+            prof_begin("k_als", stream);
+            r = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(kern),
+                                            dim3((unsigned)(batch * P)), dim3(gl::ALSC_THREADS),
+                                            args, smem_c, stream);
+            prof_end(stream);
+        }
+        cudaError_t rf = cudaFreeAsync(scr, stream);
+        return r != cudaSuccess ? r : rf;
+    };
+    bool done = false;
+    if (coop && smem_c <= 48 * 1024) {
+        cudaError_t r;
+        switch (rank) {
+            case 1: r = launch_coop(gl::k_als_coop<1>); break;
+            case 2: r = launch_coop(gl::k_als_coop<2>); break;
+            case 3: r = launch_coop(gl::k_als_coop<3>); break;
+            case 4: r = launch_coop(gl::k_als_coop<4>); break;
+            case 5: r = launch_coop(gl::k_als_coop<5>); break;
+            case 6: r = launch_coop(gl::k_als_coop<6>); break;
+            case 7: r = launch_coop(gl::k_als_coop<7>); break;
+            default: r = launch_coop(gl::k_als_coop<8>); break;
+        }
+        if (r == cudaSuccess) done = true;
+        else if (r != cudaErrorNotSupported) e = r;
+        cudaGetLastError();  // clear a NotSupported marker
+    }
     auto launch = [&](auto kern) {
         cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                              (int)smem);
@@ -658,7 +715,7 @@ gl_status gl_complete_matrices(const double *x, const uint8_t *observed, int32_t
         prof_end(stream);
         return r;
     };
-    switch (rank) {
+    if (!done && e == cudaSuccess) switch (rank) {
         case 1: e = launch(gl::k_als<1>); break;
         case 2: e = launch(gl::k_als<2>); break;
         case 3: e = launch(gl::k_als<3>); break;

@@ -16,6 +16,8 @@
 // Finally out = x where observed (verbatim), else clamp(U_i . V_j, lo, hi).
 #pragma once
 
+#include <cooperative_groups.h>
+
 #include "common.cuh"
 
 namespace gl {
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(ALS_THREADS, 1) k_als(const DAls p)
     const uint8_t *obs = p.obs + mo;
     double *u = p.u + (size_t)blockIdx.x * rows * K;
     for (int i = tid; i < cols * K; i += ALS_THREADS) V[i] = p.v0[(size_t)blockIdx.x * cols * K + i];
+    for (int64_t i = tid; i < rows * K; i += ALS_THREADS) u[i] = 0.0;  // U = 0 before iteration 1
     if (tid == 0) s_flags = 0;
     __syncthreads();
 
@@ -241,6 +244,173 @@ __host__ __device__ inline size_t als_smem_bytes(int cols, int k)
 {
     const int ns = k * (k + 1) / 2 + k;
     return sizeof(double) * ((size_t)cols * k + (cols <= ALS_WARPS ? (size_t)ALS_WARPS * ns : 0));
+}
+
+// ---- multi-CTA ALS for small batches: P CTAs per matrix, one grid-wide barrier
+// per iteration (cooperative launch).  CTA p owns a contiguous block of rows: its
+// U-step, its partial V-step sums (warp per column, lanes striding its rows) into
+// a double-buffered global array; after the barrier EVERY CTA combines the P
+// partials of each column in order p = 0..P-1 and solves V itself (no second
+// barrier).  Fixed assignment and order => deterministic.
+
+constexpr int ALSC_THREADS = 256;
+constexpr int ALSC_WARPS = ALSC_THREADS / 32;
+
+template <int K>
+__global__ void __launch_bounds__(ALSC_THREADS)
+    k_als_coop(const DAls p, double *__restrict__ part, uint32_t *__restrict__ colmask,
+               int32_t *__restrict__ rowflag, int P)
+{
+    namespace cg = cooperative_groups;
+    cg::grid_group grid = cg::this_grid();
+    constexpr int NS = K * (K + 1) / 2 + K;
+    extern __shared__ __align__(16) double alsc_smem[];
+    double *V = alsc_smem;  // [cols][K]
+    const int mat = blockIdx.x / P, pi = blockIdx.x % P;
+    const int64_t rows = p.rows;
+    const int32_t cols = p.cols;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int64_t r0 = rows * pi / P, r1 = rows * (pi + 1) / P;
+    const size_t mo = (size_t)mat * (size_t)rows * cols;
+    const double *x = p.x + mo;
+    const uint8_t *obs = p.obs + mo;
+    double *u = p.u + (size_t)mat * rows * K;
+    const int cw = (cols + 31) / 32;
+    for (int i = tid; i < cols * K; i += ALSC_THREADS) V[i] = p.v0[(size_t)mat * cols * K + i];
+    for (int64_t i = r0 * K + tid; i < r1 * K; i += ALSC_THREADS) u[i] = 0.0;  // U = 0 before iteration 1
+
+    // R53 status: rows without an observed entry; columns observed somewhere
+    for (int64_t i = r0 + tid; i < r1; i += ALSC_THREADS) {
+        int any = 0;
+        for (int32_t j = 0; j < cols; ++j) any |= obs[i * cols + j];
+        if (!any) atomicOr(rowflag + mat, 1);
+    }
+    for (int32_t j = warp; j < cols; j += ALSC_WARPS) {
+        int any = 0;
+        for (int64_t i = r0 + lane; i < r1; i += 32) any |= obs[i * cols + j];
+        if (__any_sync(FULL, any) && lane == 0) atomicOr(colmask + (size_t)mat * cw + j / 32, 1u << (j & 31));
+    }
+    __syncthreads();
+
+    for (int it = 0; it < p.iters; ++it) {
+        // U-step over this CTA's rows (the oracle's order within a row)
+        for (int64_t i = r0 + tid; i < r1; i += ALSC_THREADS) {
+            double A[K * K], b[K];
+#pragma unroll
+            for (int a = 0; a < K * K; ++a) A[a] = 0.0;
+#pragma unroll
+            for (int a = 0; a < K; ++a) b[a] = 0.0;
+            for (int32_t j = 0; j < cols; ++j) {
+                if (!obs[i * cols + j]) continue;
+                const double xv = x[i * cols + j];
+                double vj[K];
+#pragma unroll
+                for (int r = 0; r < K; ++r) vj[r] = V[j * K + r];
+#pragma unroll
+                for (int r = 0; r < K; ++r) {
+#pragma unroll
+                    for (int c = 0; c <= r; ++c) A[r * K + c] = dfma_free(A[r * K + c], vj[r], vj[c]);
+                    b[r] = dfma_free(b[r], xv, vj[r]);
+                }
+            }
+#pragma unroll
+            for (int r = 0; r < K; ++r) A[r * K + r] = __dadd_rn(A[r * K + r], p.lambda);
+            chol_solve<K>(A, b);
+#pragma unroll
+            for (int r = 0; r < K; ++r) u[i * K + r] = b[r];
+        }
+        __syncthreads();
+        // partial V-step sums of this CTA's rows: warp per column
+        double *pb = part + (((size_t)(it & 1) * gridDim.x + blockIdx.x) * cols) * NS;
+        for (int32_t j = warp; j < cols; j += ALSC_WARPS) {
+            double s[NS];
+#pragma unroll
+            for (int a = 0; a < NS; ++a) s[a] = 0.0;
+            for (int64_t i = r0 + lane; i < r1; i += 32) {
+                if (!obs[i * cols + j]) continue;
+                const double xv = x[i * cols + j];
+                double ui[K];
+#pragma unroll
+                for (int r = 0; r < K; ++r) ui[r] = u[i * K + r];
+                int a = 0;
+#pragma unroll
+                for (int r = 0; r < K; ++r)
+#pragma unroll
+                    for (int c = 0; c <= r; ++c) {
+                        s[a] = dfma_free(s[a], ui[r], ui[c]);
+                        ++a;
+                    }
+#pragma unroll
+                for (int r = 0; r < K; ++r) s[a + r] = dfma_free(s[a + r], xv, ui[r]);
+            }
+#pragma unroll
+            for (int a = 0; a < NS; ++a)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) s[a] = __dadd_rn(s[a], __shfl_xor_sync(FULL, s[a], o));
+            if (lane == 0)
+#pragma unroll
+                for (int a = 0; a < NS; ++a) pb[(size_t)j * NS + a] = s[a];
+        }
+        grid.sync();
+        // every CTA combines its matrix's P partials per column (warp per column: lane
+        // l sums partials l, l+32, ... in order, then a fixed shuffle tree) and solves V
+        const double *pa = part + ((size_t)(it & 1) * gridDim.x + (size_t)mat * P) * cols * NS;
+        for (int32_t j = warp; j < cols; j += ALSC_WARPS) {
+            double s[NS];
+#pragma unroll
+            for (int a = 0; a < NS; ++a) s[a] = 0.0;
+            for (int q = lane; q < P; q += 32)
+#pragma unroll
+                for (int a = 0; a < NS; ++a)
+                    s[a] = __dadd_rn(s[a], __ldcg(pa + ((size_t)q * cols + j) * NS + a));
+#pragma unroll
+            for (int a = 0; a < NS; ++a)
+#pragma unroll
+                for (int o = 16; o; o >>= 1) s[a] = __dadd_rn(s[a], __shfl_xor_sync(FULL, s[a], o));
+            if (lane != 0) continue;
+            double A[K * K], b[K];
+            int a = 0;
+#pragma unroll
+            for (int r = 0; r < K; ++r)
+#pragma unroll
+                for (int c = 0; c <= r; ++c) A[r * K + c] = s[a++];
+#pragma unroll
+            for (int r = 0; r < K; ++r) {
+                b[r] = s[a + r];
+                A[r * K + r] = __dadd_rn(A[r * K + r], p.lambda);
+            }
+            chol_solve<K>(A, b);
+#pragma unroll
+            for (int r = 0; r < K; ++r) V[j * K + r] = b[r];
+        }
+        __syncthreads();
+    }
+    if (p.iters == 0) grid.sync();  // the status flags below need every CTA's pre-pass
+
+    // completion of this CTA's rows
+    double *out = p.out + mo;
+    for (int64_t q = r0 * cols + tid; q < r1 * cols; q += ALSC_THREADS) {
+        if (obs[q]) {
+            out[q] = x[q];
+            continue;
+        }
+        const int64_t i = q / cols;
+        const int32_t j = (int32_t)(q - i * cols);
+        double v = 0.0;
+#pragma unroll
+        for (int r = 0; r < K; ++r) v = dfma_free(v, u[i * K + r], V[j * K + r]);
+        out[q] = v < p.lo ? p.lo : (v > p.hi ? p.hi : v);
+    }
+    if (pi == 0) {
+        if (p.v_out)
+            for (int i = tid; i < cols * K; i += ALSC_THREADS) p.v_out[(size_t)mat * cols * K + i] = V[i];
+        if (tid == 0) {
+            int32_t f = __ldcg(rowflag + mat) ? 1 : 0;
+            for (int32_t j = 0; j < cols; ++j)
+                if (!((__ldcg(colmask + (size_t)mat * cw + j / 32) >> (j & 31)) & 1u)) f |= 2;
+            p.status[mat] = f;
+        }
+    }
 }
 
 }  // namespace gl

@@ -94,3 +94,23 @@ def test_alg1_matrices_of_config4():
     print(f"config-4 Alg. 1 matrices: max |gpu - oracle| / scale = {w:.3e}")
     out, _, _, _ = run_batch([ok], [m], 2, 0.1, 200, [als_init(g.cols, 2)], 0.0, 1.0)
     assert ((out >= 0) & (out <= 1)).all()
+
+
+def test_large_batch_one_cta_per_matrix():
+    # >= one wave of matrices: the one-CTA-per-matrix kernel (small batches use the
+    # cooperative multi-CTA kernel); both must match the oracle
+    xs, ms, vs = [], [], []
+    for s in range(320):
+        xs.append(low_rank_matrix(40, 6, 2, seed=5000 + s))
+        ms.append(observation_mask(40, 6, 0.3, seed=5000 + s))
+        vs.append(als_init(6, 2, seed=s))
+    compare(xs, ms, 2, 0.1, 30, vs)
+
+
+def test_iters_zero_and_determinism():
+    x = low_rank_matrix(3000, 9, 2, seed=8)
+    m = observation_mask(3000, 9, 0.3, seed=8)
+    compare([x], [m], 2, 0.1, 0, [als_init(9, 2)])
+    a = run_batch([x], [m], 2, 0.1, 50, [als_init(9, 2)])
+    b = run_batch([x], [m], 2, 0.1, 50, [als_init(9, 2)])
+    assert all(np.array_equal(u, v) for u, v in zip(a, b))
