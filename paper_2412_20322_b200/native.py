@@ -12,7 +12,9 @@ import os
 import numpy as np
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "libgreenllm.so")
+# GL_LIB_PATH selects another build of the same library (A/B kernel experiments,
+# scripts/ab_build.py); the default is the in-tree build of __graft_entry__.build()
+LIB_PATH = os.environ.get("GL_LIB_PATH") or os.path.join(HERE, "libgreenllm.so")
 
 GL_OK, GL_E_INVALID, GL_E_DOMAIN, GL_E_LOOKUP, GL_E_CUDA, GL_E_UNSUPPORTED = 0, -1, -2, -3, -4, -5
 GL_MODE_DPD, GL_MODE_DSD, GL_MODE_STANDALONE, GL_MODE_SPEC_COLO = 0, 1, 2, 3
