@@ -257,6 +257,16 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
         n_r = rr[e1];
         n_dj = rdj[e1];
     };
+    // advance() when no ring maintenance is due ((nxt + 2) & 127 > 1): no
+    // convergent operations, so no reconvergence region in the loops using it
+    auto advance_fast = [&]() {
+        ++nxt;
+        h_r = n_r;
+        h_dj = n_dj;
+        const int e1 = (nxt + 1) & RING_MASK;
+        n_r = rr[e1];
+        n_dj = rdj[e1];
+    };
     auto fin_addr = [&](uint32_t j, int32_t q) -> int64_t * {
         return to_rows ? fin_rows + 2 * (int64_t)j : fin_spec + q;
     };
@@ -362,7 +372,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                     if (lv) *fa = T;
                     mk = T;
                     const bool one = (lm & (lm - 1u)) == 0u;
-                    if (!(one && h_r <= T && I < 0x80000000u)) {
+                    if (!(one && h_r <= T && I < 0x80000000u && ((nxt + 2) & 127) > 1)) {
                         if (lv) Fm = F_EMPTY;
                         fr |= lm;
                         b -= __popc(lm);
@@ -375,7 +385,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         fa = fin_addr(h_dj.y, nxt);
                     }
                     fmin = __reduce_min_sync(FULL, Fm);
-                    advance();
+                    advance_fast();
                 }
                 c_b += (lane == cap) ? it : 0u;
                 if (b == cap - 1) shift_down();
@@ -402,6 +412,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         T += (int64_t)kJ * st;
                         I += kJ;
                         c_b += (lane == b) ? kJ : 0u;
+                        if (((nxt + 2) & 127) <= 1) break;  // ring refill due: joins at the top
                         const unsigned bit = fr & (0u - fr);
                         fr ^= bit;
                         const uint32_t fnew = I + h_dj.x;
@@ -413,7 +424,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         ++b;
                         log_b();
                         shift_up();
-                        advance();
+                        advance_fast();
                         if (b == cap || h_r <= T) break;
                     } else {  // leave at iteration fmin (R16)
                         T += (int64_t)kL * st;

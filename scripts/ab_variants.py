@@ -42,3 +42,55 @@ VARIANTS = {
                         else load_nbr(b);
                         if (b == 0 || h_r <= T) break;''')],
 }
+
+_ADV_OLD = '''    auto fin_addr = [&](uint32_t j, int32_t q) -> int64_t * {'''
+_ADV_NEW = '''    // advance() when no ring maintenance is due ((nxt + 2) & 127 > 1): no
+    // convergent operations, so no reconvergence region in the loops using it
+    auto advance_fast = [&]() {
+        ++nxt;
+        h_r = n_r;
+        h_dj = n_dj;
+        const int e1 = (nxt + 1) & RING_MASK;
+        n_r = rr[e1];
+        n_dj = rdj[e1];
+    };
+    auto fin_addr = [&](uint32_t j, int32_t q) -> int64_t * {'''
+_SAT_OLD = '''                    const bool one = (lm & (lm - 1u)) == 0u;
+                    if (!(one && h_r <= T && I < 0x80000000u)) {'''
+_SAT_NEW = '''                    const bool one = (lm & (lm - 1u)) == 0u;
+                    if (!(one && h_r <= T && I < 0x80000000u && ((nxt + 2) & 127) > 1)) {'''
+_SAT_ADV_OLD = '''                    fmin = __reduce_min_sync(FULL, Fm);
+                    advance();
+                }
+                c_b += (lane == cap) ? it : 0u;'''
+_SAT_ADV_NEW = '''                    fmin = __reduce_min_sync(FULL, Fm);
+                    advance_fast();
+                }
+                c_b += (lane == cap) ? it : 0u;'''
+_LIGHT_OLD = '''                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;
+                        I += kJ;
+                        c_b += (lane == b) ? kJ : 0u;
+                        const unsigned bit = fr & (0u - fr);'''
+_LIGHT_NEW = '''                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;
+                        I += kJ;
+                        c_b += (lane == b) ? kJ : 0u;
+                        if (((nxt + 2) & 127) <= 1) break;  // ring refill due: joins at the top
+                        const unsigned bit = fr & (0u - fr);'''
+_LIGHT_ADV_OLD = '''                        ++b;
+                        log_b();
+                        shift_up();
+                        advance();
+                        if (b == cap || h_r <= T) break;'''
+_LIGHT_ADV_NEW = '''                        ++b;
+                        log_b();
+                        shift_up();
+                        advance_fast();
+                        if (b == cap || h_r <= T) break;'''
+VARIANTS["fastadv"] = [("k_decode.cuh", _ADV_OLD, _ADV_NEW), ("k_decode.cuh", _SAT_OLD, _SAT_NEW),
+                       ("k_decode.cuh", _SAT_ADV_OLD, _SAT_ADV_NEW),
+                       ("k_decode.cuh", _LIGHT_OLD, _LIGHT_NEW),
+                       ("k_decode.cuh", _LIGHT_ADV_OLD, _LIGHT_ADV_NEW)]
+VARIANTS["fastadv_sat"] = VARIANTS["fastadv"][:3]
+VARIANTS["fastadv_light"] = [VARIANTS["fastadv"][0]] + VARIANTS["fastadv"][3:]
