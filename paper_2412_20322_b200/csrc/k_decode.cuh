@@ -442,8 +442,11 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         log_b();
                         mk = T;
                         fmin = __reduce_min_sync(FULL, Fm);
-                        if (nl == 1) shift_down();
-                        else load_nbr(b);
+                        shift_down();
+                        if (nl != 1) {  // several members left at once: leave the loop
+                            load_nbr(b);
+                            break;
+                        }
                         if (b == 0 || h_r <= T) break;
                     }
                 }

@@ -94,3 +94,31 @@ VARIANTS["fastadv"] = [("k_decode.cuh", _ADV_OLD, _ADV_NEW), ("k_decode.cuh", _S
                        ("k_decode.cuh", _LIGHT_ADV_OLD, _LIGHT_ADV_NEW)]
 VARIANTS["fastadv_sat"] = VARIANTS["fastadv"][:3]
 VARIANTS["fastadv_light"] = [VARIANTS["fastadv"][0]] + VARIANTS["fastadv"][3:]
+
+# one branch decides leave vs (join or slow path); the slow test moves inside
+_MERGE_OLD = '''                    if (gap >= 0x80000000ll || I >= 0x80000000u) {
+                        slow = true;
+                        break;
+                    }
+                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;'''
+_MERGE_NEW = '''                    const bool far = gap >= 0x80000000ll || I >= 0x80000000u;
+                    if (far || kJ < kL) {  // the head joins at T + kJ * step[b]
+                        if (far) {
+                            slow = true;
+                            break;
+                        }
+                        T += (int64_t)kJ * st;'''
+VARIANTS["merge"] = [("k_decode.cuh", _MERGE_OLD, _MERGE_NEW)]
+# the leave branch's multi-leave test on the ballot (no popc) and predicated refill
+_NL_OLD = '''                        if (nl == 1) shift_down();
+                        else load_nbr(b);
+                        if (b == 0 || h_r <= T) break;'''
+_NL_NEW = '''                        shift_down();
+                        if (nl != 1) {  // several members left at once: leave the loop
+                            load_nbr(b);
+                            break;
+                        }
+                        if (b == 0 || h_r <= T) break;'''
+VARIANTS["nl"] = [("k_decode.cuh", _NL_OLD, _NL_NEW)]
+VARIANTS["merge_nl"] = VARIANTS["merge"] + VARIANTS["nl"]
