@@ -122,3 +122,36 @@ _NL_NEW = '''                        shift_down();
                         if (b == 0 || h_r <= T) break;'''
 VARIANTS["nl"] = [("k_decode.cuh", _NL_OLD, _NL_NEW)]
 VARIANTS["merge_nl"] = VARIANTS["merge"] + VARIANTS["nl"]
+
+# join/leave decided in the time domain: kJ < kL  <=>  gap <= (kL - 1) st; the
+# division is computed only on the join path
+_TDEC_OLD = '''                    const uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, M_c);
+                    if (gap >= 0x80000000ll || I >= 0x80000000u) {
+                        slow = true;
+                        break;
+                    }
+                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;'''
+_TDEC_NEW = '''                    if (gap >= 0x80000000ll || I >= 0x80000000u) {
+                        slow = true;
+                        break;
+                    }
+                    if (gap <= ((int64_t)kL - 1) * st) {  // the head joins at T + kJ * step[b]
+                        const uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, M_c);
+                        T += (int64_t)kJ * st;'''
+VARIANTS["tdec"] = [("k_decode.cuh", _TDEC_OLD, _TDEC_NEW)]
+# saturated loop: exit test without the popc / multi-leave combination on the chain
+_SATX_OLD = '''                    const bool one = (lm & (lm - 1u)) == 0u;
+                    if (!(one && h_r <= T && I < 0x80000000u && ((nxt + 2) & 127) > 1)) {'''
+_SATX_NEW = '''                    const bool one = lm == lane_bit_of_min;
+                    if (!(one && h_r <= T && I < 0x80000000u && ((nxt + 2) & 127) > 1)) {'''
+
+# a join that fills the batch stays in the light-load loop (the next event is then
+# a forced leave): near-saturated chains stop bouncing into the saturated loop
+VARIANTS["capjoin"] = [
+    ("k_decode.cuh", '''                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;''', '''                    if (kJ < kL && b < cap) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;'''),
+    ("k_decode.cuh", '''                        if (b == cap || h_r <= T) break;''',
+     '''                        if (h_r <= T && b < cap) break;'''),
+]
