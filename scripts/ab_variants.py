@@ -155,3 +155,8 @@ VARIANTS["capjoin"] = [
     ("k_decode.cuh", '''                        if (b == cap || h_r <= T) break;''',
      '''                        if (h_r <= T && b < cap) break;'''),
 ]
+
+# decision in the time domain while kJ is still computed before the branch
+VARIANTS["tdec2"] = [("k_decode.cuh", '''                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;''', '''                    if (gap <= ((int64_t)kL - 1) * st) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;''')]
