@@ -330,10 +330,13 @@ def run_ours(args):
     alg_bytes = algorithmic_bytes(grid, lo, hi)
     achieved = alg_bytes / (kdec_ms / 1e3) / 1e9 if kdec_ms > 0 else 0.0
     traffic = None
+    winst = None
     prof_path = os.path.join(ROOT, "profiles", "k_decode_dram_bytes.json")
     if os.path.exists(prof_path):
         try:
-            traffic = json.load(open(prof_path)).get("dram_bytes_per_launch")
+            pj = json.load(open(prof_path))
+            traffic = pj.get("dram_bytes_per_launch")
+            winst = pj.get("warp_inst_per_launch")
         except (OSError, ValueError):
             traffic = None
     step_total = {k: sum(v) / max(1, len(v)) for k, v in kt.items()}
@@ -373,6 +376,7 @@ def run_ours(args):
                      "bytes_per_unit": DECODE_BYTES_PER_REQUEST, "unit_name": "decode request",
                      "kernel_ms": kdec_ms,
                      "latency": latency,
+                     "alu_view": alu_view(winst, kdec_ms, sm_mhz, grid, lo, hi),
                      "note": "k_decode is bound by the dependent latency of the slowest chain's "
                              "serial decode event loop (busy periods cannot be split exactly), "
                              "not by HBM (DESIGN.md §5)"},
@@ -386,6 +390,22 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def alu_view(warp_inst, kernel_ms, sm_mhz, grid, lo, hi):
+    """The issue-rate view of k_decode: warp-instructions per
+    launch (ncu smsp__inst_executed.sum, profiles/k_decode_dram_bytes.json) over the
+    live kernel time, against 148 SMs x 4 schedulers x 1 warp-instruction per cycle
+    at the sampled SM clock."""
+    if not warp_inst or kernel_ms <= 0:
+        return None
+    peak = 148 * 4 * sm_mhz * 1e6
+    achieved = warp_inst / (kernel_ms / 1e3)
+    reqs = sum(g.n for g in [grid.traces[c.trace_idx] for c in grid.chains[lo:hi]])
+    return {"achieved": achieved, "peak": peak, "unit": "warp-inst/s", "frac": achieved / peak,
+            "warp_inst_per_chain_request": warp_inst / max(reqs, 1),
+            "note": "instruction count from the committed ncu capture; the kernel is bound by "
+                    "the slowest chain's dependent latency, so most SMs idle (warps_active ~3%)"}
 
 
 def link_demand_bench(dg, grid, flush, reps=3):

@@ -160,3 +160,34 @@ VARIANTS["capjoin"] = [
 VARIANTS["tdec2"] = [("k_decode.cuh", '''                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
                         T += (int64_t)kJ * st;''', '''                    if (gap <= ((int64_t)kL - 1) * st) {  // the head joins at T + kJ * step[b]
                         T += (int64_t)kJ * st;''')]
+
+# the light loop keeps fmin2 = the next distinct finish iteration above fmin, so a
+# leave sets fmin = fmin2 at once and the REDUX (for the new fmin2) leaves the chain
+VARIANTS["fmin2"] = [
+    ("k_decode.cuh", '''                bool slow = false;
+                for (;;) {
+                    const int64_t st = st_c;
+                    const uint32_t kL = fmin - I;''', '''                bool slow = false;
+                uint32_t fmin2 = __reduce_min_sync(FULL, Fm > fmin ? Fm : F_EMPTY);
+                for (;;) {
+                    const int64_t st = st_c;
+                    const uint32_t kL = fmin - I;'''),
+    ("k_decode.cuh", '''                        fmin = min(fmin, fnew);
+                        ++b;
+                        log_b();
+                        shift_up();
+                        advance_fast();''', '''                        fmin2 = fnew < fmin ? fmin : (fnew > fmin ? min(fmin2, fnew) : fmin2);
+                        fmin = min(fmin, fnew);
+                        ++b;
+                        log_b();
+                        shift_up();
+                        advance_fast();'''),
+    ("k_decode.cuh", '''                        mk = T;
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        shift_down();
+                        if (nl != 1) {  // several members left at once: leave the loop''', '''                        mk = T;
+                        fmin = fmin2;  // every member at the old minimum has left
+                        fmin2 = __reduce_min_sync(FULL, Fm > fmin ? Fm : F_EMPTY);
+                        shift_down();
+                        if (nl != 1) {  // several members left at once: leave the loop'''),
+]

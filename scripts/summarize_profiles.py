@@ -79,6 +79,7 @@ def num(n):
 
 dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
 json.dump({"round": tag, "kernel": kern, "dram_bytes_per_launch": dram,
+           "warp_inst_per_launch": num("smsp__inst_executed.sum"),
            "source": f"profiles/{tag}_{kern}_ncu.md"},
           open(os.path.join(out_dir, f"{kern}_dram_bytes.json"), "w"), indent=1)
 print(open(os.path.join(out_dir, f"{tag}_launches.md")).read())
