@@ -456,6 +456,7 @@ def analysis_bench(dg, grid, reps=3):
     import torch
 
     from paper_2412_20322_b200 import api
+    from paper_2412_20322_b200 import native as N
     from paper_2412_20322_b200.inputs import build_config
     from paper_2412_20322_b200.inputs.cf import observation_mask
 
@@ -476,6 +477,14 @@ def analysis_bench(dg, grid, reps=3):
     dg6 = api.DeviceGrid(g6, dg.device)
     stats6, _ = api.eval_grid(dg6)
     sav_ms = timed(lambda: api.savings_surface(dg6, stats6))
+    # NEXT #1: the whole config-6 step (cfg 4 + the Standalone and SpecDecode columns)
+    N.profile_enable(True)
+    N.kernel_times()
+    cfg6_ms = timed(lambda: (api.eval_grid(dg6), api.argmin_feasible(dg6, stats6)))
+    kt6 = {}
+    for name, t in N.kernel_times():
+        kt6.setdefault(name, []).append(t)
+    N.profile_enable(False)
     stats, _ = api.eval_grid(dg)
     carbon, _, _ = api.argmin_feasible(dg, stats)
     st = api.stats_numpy(stats)
@@ -484,7 +493,12 @@ def analysis_bench(dg, grid, reps=3):
     m = torch.from_numpy(observation_mask(grid.rows, grid.cols, 0.3, seed=42)).to(dg.device)
     x, mm = torch.stack([carbon, att]), torch.stack([m, m])
     cf_ms = timed(lambda: api.complete_matrices(x, mm, 2, 0.1, 200, lo=0.0))
-    return {"savings_surface": {"ms": sav_ms, "cells": len(api_pairs(g6)) * len(g6.scenarios),
+    return {"cfg6_step": {"ms": cfg6_ms, "timing_chains": len(g6.chains),
+                          "grid": [g6.rows, g6.cols],
+                          "kernel_ms": {k: sum(v) / len(v) for k, v in kt6.items()},
+                          "workload": "cfg6: cfg4 + Standalone and SpecDecode (A100) columns, "
+                                      "8,192 x 10 cells, 80 timing chains"},
+            "savings_surface": {"ms": sav_ms, "cells": len(api_pairs(g6)) * len(g6.scenarios),
                                 "workload": "cfg6: 72 (Case 2, Standalone) pairs x 1,024 (CI, T_A, T_B)"},
             "complete_matrices": {"ms": cf_ms, "matrices": 2, "shape": [grid.rows, grid.cols],
                                   "rank": 2, "iters": 200, "hidden": 0.3}}

@@ -21,7 +21,10 @@
  *  - The caller owns every buffer.  The library keeps no global state besides
  *    a cached device-capability check, allocates only stream-ordered scratch
  *    (cudaMallocAsync / cudaFreeAsync on `stream`) and never synchronises
- *    except in gl_evaluate_host.
+ *    except in gl_evaluate_host.  When one gl_eval_grid call holds both
+ *    disaggregated and co-located chains, it forks a temporary side stream from
+ *    `stream` (event record / wait) for the co-located decode launch and joins it
+ *    back before returning, so the call remains ordered on `stream`.
  *  - Calls are asynchronous and stream-ordered (except gl_evaluate_host):
  *    device buffers must stay valid until `stream` has passed the call; host
  *    descriptor arrays are consumed before the call returns.

@@ -387,17 +387,35 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     }
     if (e == cudaSuccess) {
         const unsigned blocks = (unsigned)(n_chains * (1 + extra));
+        cudaStream_t dec_stream = stream;  // the co-located launch may run on a side stream
         auto launch = [&](auto kern, const char *name) {
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem_dec);
             if (r != cudaSuccess) return r;
-            prof_begin(name, stream);
-            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, stream>>>(dc, stats_out, rows, (int32_t)n_chains);
+            prof_begin(name, dec_stream);
+            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, dec_stream>>>(dc, stats_out, rows,
+                                                                      (int32_t)n_chains);
             r = cudaGetLastError();
-            prof_end(stream);
+            prof_end(dec_stream);
             ++launches;
             return r;
         };
+        // Both families present (configuration 6): the co-located launch goes to a
+        // side stream forked from `stream` and joined back, so the two launches
+        // (disjoint chains) overlap; the call stays stream-ordered on `stream`.
+        cudaStream_t side = nullptr;
+        cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
+        if (has_disg && has_colo && !lk) {
+            if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess &&
+                cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) == cudaSuccess &&
+                cudaEventRecord(ev_fork, stream) == cudaSuccess &&
+                cudaStreamWaitEvent(side, ev_fork, 0) == cudaSuccess) {
+            } else {
+                e = cudaGetLastError();
+                if (e == cudaSuccess) e = cudaErrorUnknown;
+            }
+        }
         // disaggregated chains, then co-located ones (each launch skips the others)
         if (has_disg && lk) {  // leader-only runs that log the batch size
             if (max_cap <= 31)
@@ -419,6 +437,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                 e = launch(gl::k_decode<8, false>, "k_decode");
         }
         if (has_colo && e == cudaSuccess) {
+            if (side) dec_stream = side;
             if (max_cap <= 32)
                 e = launch(gl::k_decode<1, true>, "k_decode_colo");
             else if (max_cap <= 64)
@@ -427,7 +446,16 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                 e = launch(gl::k_decode<4, true>, "k_decode_colo");
             else
                 e = launch(gl::k_decode<8, true>, "k_decode_colo");
+            dec_stream = stream;
         }
+        if (side) {  // join the side stream back into `stream`
+            cudaError_t r = cudaEventRecord(ev_join, side);
+            if (r == cudaSuccess) r = cudaStreamWaitEvent(stream, ev_join, 0);
+            if (e == cudaSuccess) e = r;
+        }
+        if (ev_fork) cudaEventDestroy(ev_fork);
+        if (ev_join) cudaEventDestroy(ev_join);
+        if (side) cudaStreamDestroy(side);  // released once its work completes
     }
     if (e == cudaSuccess) {
         const int per_thread = 8;

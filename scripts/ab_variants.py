@@ -191,3 +191,102 @@ VARIANTS["fmin2"] = [
                         shift_down();
                         if (nl != 1) {  // several members left at once: leave the loop'''),
 ]
+
+# general loop (caps >= 32, co-located modes): fmin kept across join events (REDUX
+# only after leaves) and step[b +- 1] / reciprocals cached in registers
+VARIANTS["gen1"] = [
+    ("k_decode.cuh", '''#pragma unroll
+        for (int s = 0; s <= SPL; ++s) cnt[s] = 0;
+        for (;;) {
+            while (b < cap && h_r <= T) {  // FCFS joins (R16, R18)''', '''#pragma unroll
+        for (int s = 0; s <= SPL; ++s) cnt[s] = 0;
+        uint32_t fmin = F_EMPTY;  // min over members, kept across joins
+        int32_t g_st_d = 0, g_st_c = ld_step(0), g_st_u = ld_step(min(1, cap));
+        uint64_t g_M_d = 0, g_M_c = ld_magic(0), g_M_u = ld_magic(min(1, cap));
+        auto g_load = [&](int nbb) {
+            g_st_c = ld_step(nbb);
+            g_M_c = ld_magic(nbb);
+            g_st_u = ld_step(min(nbb + 1, cap));
+            g_M_u = ld_magic(min(nbb + 1, cap));
+            g_st_d = ld_step(max(nbb - 1, 0));
+            g_M_d = ld_magic(max(nbb - 1, 0));
+        };
+        for (;;) {
+            while (b < cap && h_r <= T) {  // FCFS joins (R16, R18)'''),
+    ("k_decode.cuh", '''                    for (int s = 0; s < SPL; ++s)
+                        if (F[s] != F_EMPTY) F[s] -= I;
+#pragma unroll
+                    for (int s = 0; s <= SPL; ++s) {''', '''                    for (int s = 0; s < SPL; ++s)
+                        if (F[s] != F_EMPTY) F[s] -= I;
+                    if (fmin != F_EMPTY) fmin -= I;
+#pragma unroll
+                    for (int s = 0; s <= SPL; ++s) {'''),
+    ("k_decode.cuh", '''                        if (lane_bit == bit) {
+                            F[s] = I + h_dj.x;
+                            fa[s] = fin_addr(h_dj.y, nxt);
+                        }
+                    }
+                }
+                ++b;
+                if constexpr (!COLO) log_b();
+                advance();''', '''                        if (lane_bit == bit) {
+                            F[s] = I + h_dj.x;
+                            fa[s] = fin_addr(h_dj.y, nxt);
+                        }
+                    }
+                }
+                fmin = min(fmin, I + h_dj.x);
+                ++b;
+                g_st_d = g_st_c;
+                g_M_d = g_M_c;
+                g_st_c = g_st_u;
+                g_M_c = g_M_u;
+                g_st_u = ld_step(min(b + 1, cap));
+                g_M_u = ld_magic(min(b + 1, cap));
+                if constexpr (!COLO) log_b();
+                advance();'''),
+    ("k_decode.cuh", '''            const int64_t st = ld_step(b);
+            uint32_t kJ = 0xFFFFFFFFu;
+            if (b < cap) {
+                const int64_t gap = h_r - T;
+                if (gap < 0x80000000ll) kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, ld_magic(b));
+                else if (h_r != INT64_MAX)
+                    kJ = (uint32_t)min((gap + st - 1) / st, (int64_t)0xFFFFFFFF);
+            }
+            uint32_t fmin = F[0];
+#pragma unroll
+            for (int s = 1; s < SPL; ++s) fmin = min(fmin, F[s]);
+            fmin = __reduce_min_sync(FULL, fmin);
+            const uint32_t kL = fmin - I;''', '''            const int64_t st = g_st_c;
+            uint32_t kJ = 0xFFFFFFFFu;
+            if (b < cap) {
+                const int64_t gap = h_r - T;
+                if (gap < 0x80000000ll) kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, g_M_c);
+                else if (h_r != INT64_MAX)
+                    kJ = (uint32_t)min((gap + st - 1) / st, (int64_t)0xFFFFFFFF);
+            }
+            const uint32_t kL = fmin - I;'''),
+    ("k_decode.cuh", '''            b -= nl;
+            if (nl) {
+                mk = T;
+                if constexpr (!COLO) log_b();
+            }''', '''            b -= nl;
+            if (nl) {
+                mk = T;
+                if constexpr (!COLO) log_b();
+                uint32_t f = F[0];
+#pragma unroll
+                for (int s = 1; s < SPL; ++s) f = min(f, F[s]);
+                fmin = __reduce_min_sync(FULL, f);
+                if (nl == 1) {
+                    g_st_u = g_st_c;
+                    g_M_u = g_M_c;
+                    g_st_c = g_st_d;
+                    g_M_c = g_M_d;
+                    g_st_d = ld_step(max(b - 1, 0));
+                    g_M_d = ld_magic(max(b - 1, 0));
+                } else {
+                    g_load(b);
+                }
+            }'''),
+]

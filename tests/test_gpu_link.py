@@ -111,3 +111,18 @@ def test_window_monotone_and_total_invariant():
             assert np.array_equal(lk["total_bytes"], prev["total_bytes"])
         prev = lk
     assert np.array_equal(prev["peak_bytes"], prev["total_bytes"])
+
+
+def test_config5_sampled_chains_full_size():
+    # 1M-request LongBench traces (DSD 70B/7B): the largest logs and windows
+    g = build_config(5)
+    link_parity(subset_chains(g, [0, 319]), 1_000_000, check_eval=False)
+
+
+def test_config3_bandwidth_axis():
+    # config 3 sweeps the link bandwidth (1-100 Gbps) for both modes, incl. the
+    # capacity-infeasible 13B DPD chains (still simulated, R38)
+    g = build_config(3, n=4000)
+    ids = list(range(0, 128, 9))
+    lk = link_parity(subset_chains(g, ids), 1_000_000, check_eval=False)
+    assert (lk["total_bytes"] > 0).all()
