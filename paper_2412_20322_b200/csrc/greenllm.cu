@@ -438,7 +438,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         }
         if (has_colo && e == cudaSuccess) {
             if (side) dec_stream = side;
-            if (max_cap <= 32)
+            if (max_cap <= 31)  // the one-row fast paths need b < 32
                 e = launch(gl::k_decode<1, true>, "k_decode_colo");
             else if (max_cap <= 64)
                 e = launch(gl::k_decode<2, true>, "k_decode_colo");

@@ -286,7 +286,21 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
 #pragma unroll
     for (int s = 0; s <= SPL; ++s) iters[s] = 0;
 
-    if constexpr (SPL == 1 && !COLO) {
+    if constexpr (SPL == 1) {
+        // caps <= 31, one member per lane.  Co-located modes (COLO, R41-R44) add, at
+        // every admission, the request's prefill run alone on the GPU (T += t1[p],
+        // its first token at T: the TTFT is written there); a request with no decode
+        // demand (o = 1) finishes at its first token without taking a slot -- the
+        // fast paths hand such heads to the admission loop.
+        auto prefill = [&]() {
+            if constexpr (COLO) {
+                T += (int64_t)rpf[nxt & RING_MASK];
+                if (lane == 0) {
+                    if (to_rows) fin_rows[2 * (int64_t)h_dj.y - 1] = T - h_r;
+                    else ttft_spec[nxt] = T - h_r;
+                }
+            }
+        };
         uint32_t Fm = F_EMPTY, fmin = F_EMPTY;
         int64_t *fa = fin_rows;
         unsigned fr = cap >= 32 ? FULL : ((1u << cap) - 1u);
@@ -327,6 +341,15 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                     iters[0] += c_b;
                     c_b = 0;
                     I = 0;
+                }
+                if constexpr (COLO) {
+                    prefill();
+                    if (h_dj.x == 0) {  // o = 1: done at its first token (R13)
+                        if (lane == 0) *fin_addr(h_dj.y, nxt) = T;
+                        mk = T;
+                        advance();
+                        continue;
+                    }
                 }
                 const unsigned bit = fr & (0u - fr);
                 fr ^= bit;
@@ -372,7 +395,8 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                     if (lv) *fa = T;
                     mk = T;
                     const bool one = (lm & (lm - 1u)) == 0u;
-                    if (!(one && h_r <= T && I < 0x80000000u && ((nxt + 2) & 127) > 1)) {
+                    if (!(one && h_r <= T && I < 0x80000000u && ((nxt + 2) & 127) > 1 &&
+                          (!COLO || h_dj.x != 0))) {
                         if (lv) Fm = F_EMPTY;
                         fr |= lm;
                         b -= __popc(lm);
@@ -384,6 +408,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         Fm = I + h_dj.x;
                         fa = fin_addr(h_dj.y, nxt);
                     }
+                    prefill();  // co-located: the freed slot's newcomer prefills first
                     fmin = __reduce_min_sync(FULL, Fm);
                     advance_fast();
                 }
@@ -413,6 +438,10 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                         I += kJ;
                         c_b += (lane == b) ? kJ : 0u;
                         if (((nxt + 2) & 127) <= 1) break;  // ring refill due: joins at the top
+                        if constexpr (COLO) {
+                            if (h_dj.x == 0) break;  // o = 1 head: admitted at the top
+                            prefill();
+                        }
                         const unsigned bit = fr & (0u - fr);
                         fr ^= bit;
                         const uint32_t fnew = I + h_dj.x;
