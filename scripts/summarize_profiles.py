@@ -44,7 +44,8 @@ raw = subprocess.run(["ncu", "-i", rep, "--page", "raw", "--csv"], capture_outpu
 rr = list(csv.reader(raw.splitlines()))
 names, units, vals = rr[0], rr[1], rr[2]
 want = ["gpu__time_duration.sum", "dram__bytes_read.sum", "dram__bytes_write.sum",
-        "lts__t_bytes.sum", "smsp__inst_executed.sum", "sm__inst_executed.sum",
+        "lts__t_bytes.sum", "lts__t_sectors.sum", "lts__t_requests.sum",
+        "smsp__inst_executed.sum", "sm__inst_executed.sum",
         "smsp__issue_active.avg.pct_of_peak_sustained_active",
         "sm__warps_active.avg.pct_of_peak_sustained_active", "launch__registers_per_thread",
         "launch__grid_size", "launch__block_size", "launch__shared_mem_per_block_dynamic",
