@@ -199,6 +199,9 @@ def test_iteration_rebase_and_far_gaps():
              15_000_000_000, 16_000_000_000]
         o = [1_000_000_000, 5, 7, 1_070_000_000, 600_000_000, 3, 300_000_000, 1000]
         pairs.append((custom_trace(a, [1, 2, 3, 4, 1, 2, 3, 4], o), ch))
+        if cap == 2:  # the co-located fast paths (prefill at every admission) rebase too
+            pairs.append((custom_trace(a, [1, 2, 3, 4, 1, 2, 3, 4], o),
+                          make_chain(tab, MODE_STANDALONE, cap, ttft_slo=100, tpot_slo=4)))
     assert_parity(grid_of(pairs))
 
 
