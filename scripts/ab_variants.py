@@ -290,3 +290,29 @@ VARIANTS["gen1"] = [
                 }
             }'''),
 ]
+
+# the one-leave path decrements b without waiting for popc(ballot)
+VARIANTS["nl2"] = [("k_decode.cuh", '''                        fr |= lm;
+                        const int nl = __popc(lm);
+                        b -= nl;
+                        log_b();
+                        mk = T;
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        shift_down();
+                        if (nl != 1) {  // several members left at once: leave the loop
+                            load_nbr(b);
+                            break;
+                        }
+                        if (b == 0 || h_r <= T) break;''', '''                        fr |= lm;
+                        mk = T;
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        if ((lm & (lm - 1u)) != 0u) {  // several left at once: leave the loop
+                            b -= __popc(lm);
+                            log_b();
+                            load_nbr(b);
+                            break;
+                        }
+                        --b;
+                        log_b();
+                        shift_down();
+                        if (b == 0 || h_r <= T) break;''')]
