@@ -359,7 +359,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     if (e == cudaSuccess && !groups.empty()) {
         int64_t gmax = 0;
         for (auto &g : groups) gmax = std::max(gmax, g.n);
-        dim3 grid((unsigned)((gmax + 255) / 256), (unsigned)groups.size());
+        dim3 grid((unsigned)((gmax * gl::DSD_QL + 255) / 256), (unsigned)groups.size());
         prof_begin("k_dsd_demand", stream);
         gl::k_dsd_demand<<<grid, 256, 0, stream>>>(
             reinterpret_cast<const DGroup *>(scratch + off_groups));

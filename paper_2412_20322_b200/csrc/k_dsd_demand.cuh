@@ -6,54 +6,109 @@
 // thr_c = floor(alpha^c 2^32) and u = Philox word (s mod 4) of counter
 // (s/4, j, ACCEPT_STREAM, 0) for request j's own step s.  Because the draw is keyed
 // by (request, its own step), K_j = min{k : sum_{s<k} acc_s >= o_j - 1} does not
-// depend on batching, so one thread per (group, request) computes it up front and
-// chains with equal (output lengths, gamma, alpha, seed) share it.
+// depend on batching, so chains with equal (output lengths, gamma, alpha, seed)
+// share it.
+//
+// Work split: QL = 4 lanes per request.  In round t lane l evaluates Philox call
+// 4t + l (steps 16t + 4l .. +3); the four calls' token counts are prefix-summed with
+// two shuffles and the crossing step is found without a serial walk, so a warp
+// waits on the longest of 8 requests (not 32) and each request finishes 4x sooner.
+// The gamma thresholds sit in registers (the kernel is instantiated per gamma;
+// the block's group picks the instance), compared as 64-bit (thr = 2^32 at alpha = 1).
 #pragma once
 
 #include "common.cuh"
 
 namespace gl {
 
-__global__ void __launch_bounds__(256) k_dsd_demand(const DGroup *__restrict__ groups)
+constexpr int DSD_QL = 4;  // lanes per request
+
+template <int G>
+__device__ __forceinline__ uint32_t accepted_tokens(uint32_t u, const uint64_t (&thr)[G])
 {
-    __shared__ uint64_t thr[GL_MAX_GAMMA];
-    __shared__ int32_t gamma_s;
-    __shared__ uint64_t seed_s;
-    const DGroup *g = groups + blockIdx.y;
-    if (threadIdx.x < GL_MAX_GAMMA) thr[threadIdx.x] = g->thr[threadIdx.x];
-    if (threadIdx.x == 0) {
-        gamma_s = g->gamma;
-        seed_s = g->seed;
-    }
-    __syncthreads();
-    const int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (j >= g->n) return;
-    uint32_t o = __ldg(g->o + j);
+    uint32_t acc = 1;
+#pragma unroll
+    for (int c = 0; c < G; ++c) acc += ((uint64_t)u < thr[c]) ? 1u : 0u;
+    return acc;
+}
+
+template <int G>
+__device__ __forceinline__ void dsd_demand_body(const DGroup *g)
+{
+    uint64_t thr[G];
+#pragma unroll
+    for (int c = 0; c < G; ++c) thr[c] = g->thr[c];
+    const int lane = threadIdx.x & 31, sub = lane & (DSD_QL - 1);
+    const unsigned gmask = 0xFu << (lane & ~(DSD_QL - 1));  // this request's 4 lanes
+    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / DSD_QL;
+    const bool valid = j < g->n;
+    uint32_t o = valid ? __ldg(g->o + j) : 1u;
     if (o >= O_LIMIT) o = O_LIMIT - 1;
     const int64_t need = (int64_t)o - 1;
-    uint32_t s = 0;
-    if (need > 0) {
-        const uint32_t k0 = (uint32_t)seed_s, k1 = (uint32_t)(seed_s >> 32);
-        const int gam = gamma_s;
-        int64_t tok = 0;
-        for (;;) {
-            const uint4 w = philox4x32_10(make_uint4(s >> 2, (uint32_t)j, ACCEPT_STREAM, 0u), k0, k1);
-            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-            bool done = false;
-#pragma unroll
-            for (int q = 0; q < 4; ++q) {
-                if (!done) {
-                    int acc = 1;
-                    for (int c = 0; c < gam; ++c) acc += ((uint64_t)ws[q] < thr[c]) ? 1 : 0;
-                    tok += acc;
-                    ++s;
-                    done = tok >= need;
-                }
+    const uint32_t k0 = (uint32_t)g->seed, k1 = (uint32_t)(g->seed >> 32);
+    int64_t tok = 0;  // tokens accepted before this round
+    uint32_t K = 0;
+    bool done = need <= 0;
+    for (uint32_t t = 0; !__all_sync(gmask, done); ++t) {
+        // this lane's call: steps s0 .. s0+3 of request j
+        const uint32_t call = DSD_QL * t + sub;
+        const uint4 w = philox4x32_10(make_uint4(call, (uint32_t)j, ACCEPT_STREAM, 0u), k0, k1);
+        const uint32_t a0 = accepted_tokens<G>(w.x, thr), a1 = accepted_tokens<G>(w.y, thr);
+        const uint32_t a2 = accepted_tokens<G>(w.z, thr), a3 = accepted_tokens<G>(w.w, thr);
+        const uint32_t mine = a0 + a1 + a2 + a3;
+        // inclusive prefix over the 4 lanes of this request
+        uint32_t inc = mine;
+        uint32_t y = __shfl_up_sync(gmask, inc, 1, DSD_QL);
+        if (sub >= 1) inc += y;
+        y = __shfl_up_sync(gmask, inc, 2, DSD_QL);
+        if (sub >= 2) inc += y;
+        const uint32_t round_tot = __shfl_sync(gmask, inc, DSD_QL - 1, DSD_QL);
+        if (!done) {
+            const int64_t before = tok + (inc - mine);  // tokens before this lane's call
+            // the crossing lies in this lane's call iff before < need <= before + mine
+            int64_t cum = before;
+            uint32_t ks = 0;
+            if (before < need && need <= before + mine) {
+                cum += a0;
+                ks = 1;
+                if (cum < need) { cum += a1; ks = 2; }
+                if (cum < need) { cum += a2; ks = 3; }
+                if (cum < need) { ks = 4; }
             }
-            if (done) break;
+            const unsigned hit = __ballot_sync(gmask, ks != 0) & gmask;
+            if (hit) {
+                const int src = __ffs(hit) - 1;
+                const uint32_t kk = __shfl_sync(gmask, ks, src & (32 - 1));
+                K = 4 * (DSD_QL * t + (uint32_t)(src & (DSD_QL - 1))) + kk;
+                done = true;
+            }
+            tok += round_tot;
         }
     }
-    g->K[j] = s;
+    if (valid && sub == 0) g->K[j] = K;
+}
+
+__global__ void __launch_bounds__(256) k_dsd_demand(const DGroup *__restrict__ groups)
+{
+    const DGroup *g = groups + blockIdx.y;
+    switch (g->gamma) {
+        case 1: dsd_demand_body<1>(g); break;
+        case 2: dsd_demand_body<2>(g); break;
+        case 3: dsd_demand_body<3>(g); break;
+        case 4: dsd_demand_body<4>(g); break;
+        case 5: dsd_demand_body<5>(g); break;
+        case 6: dsd_demand_body<6>(g); break;
+        case 7: dsd_demand_body<7>(g); break;
+        case 8: dsd_demand_body<8>(g); break;
+        case 9: dsd_demand_body<9>(g); break;
+        case 10: dsd_demand_body<10>(g); break;
+        case 11: dsd_demand_body<11>(g); break;
+        case 12: dsd_demand_body<12>(g); break;
+        case 13: dsd_demand_body<13>(g); break;
+        case 14: dsd_demand_body<14>(g); break;
+        case 15: dsd_demand_body<15>(g); break;
+        default: dsd_demand_body<16>(g); break;
+    }
 }
 
 }  // namespace gl
