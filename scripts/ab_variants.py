@@ -316,3 +316,54 @@ VARIANTS["nl2"] = [("k_decode.cuh", '''                        fr |= lm;
                         log_b();
                         shift_down();
                         if (b == 0 || h_r <= T) break;''')]
+
+# packed keys (F << 5 | lane) for DPD/DSD caps <= 31: one REDUX gives the leaver
+# (no ballot / popc), joins update kmin uniformly; ring refills hoisted
+_PK_BLOCK = open("/tmp/pk_variant_block.txt").read() if __import__("os").path.exists(
+    "/tmp/pk_variant_block.txt") else ""
+VARIANTS["packed"] = [
+    ("k_decode.cuh", '''constexpr int DEC_WARPS = 1;  // one warp per k_decode block (leader or helper)''',
+     '''constexpr int DEC_WARPS = 1;  // one warp per k_decode block (leader or helper)
+constexpr uint32_t KEY_INF = 0xFFFFFFFFu;  // packed-key decode loop (caps <= 31)
+constexpr uint32_t PK_REBASE = 1u << 25;   // keys hold F < 2^27: rebase I at 2^25
+constexpr uint32_t PK_MAXD = 1u << 25;     // ... which needs every demand < 2^25'''),
+    ("k_decode.cuh", '''        };
+        uint32_t Fm = F_EMPTY, fmin = F_EMPTY;
+        int64_t *fa = fin_rows;''', '''        };
+''' + _PK_BLOCK + '''        uint32_t Fm = F_EMPTY, fmin = F_EMPTY;
+        int64_t *fa = fin_rows;'''),
+    ("k_decode.cuh", '''        iters[0] += c_b;
+    } else {
+        // general loop, caps 32..256: SPL rows of 32 member slots per lane''', '''        iters[0] += c_b;
+        }
+    } else {
+        // general loop, caps 32..256: SPL rows of 32 member slots per lane'''),
+    ("common.cuh", '''    int32_t n_ev;        // LOG launches: batch-size log entries written
+    int32_t pad[3];''', '''    int32_t n_ev;        // LOG launches: batch-size log entries written
+    uint32_t maxd;       // largest decode demand of the chain (k_segments)
+    int32_t pad[2];'''),
+    ("k_stages.cuh", '''    __shared__ int32_t s_min_step;''', '''    __shared__ int32_t s_min_step;
+    __shared__ uint32_t s_maxd;'''),
+    ("k_stages.cuh", '''    if (threadIdx.x == 0) s_min_step = INT32_MAX;
+    __syncthreads();''', '''    if (threadIdx.x == 0) {
+        s_min_step = INT32_MAX;
+        s_maxd = 0;
+    }
+    __syncthreads();
+    uint32_t maxd = 0;'''),
+    ("k_stages.cuh", '''            for (int32_t q = lo + lane; q < hi; q += 32)
+                m = max(m, __ldg(ch.dec_r + q) + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
+                               (colo ? __ldg(ch.dec_pf + q) : 0));''', '''            for (int32_t q = lo + lane; q < hi; q += 32) {
+                const uint32_t dq = __ldg(&ch.dec_dj[q].x);
+                maxd = max(maxd, dq);
+                m = max(m, __ldg(ch.dec_r + q) + (int64_t)dq * smin +
+                               (colo ? __ldg(ch.dec_pf + q) : 0));
+            }'''),
+    ("k_stages.cuh", '''    if (threadIdx.x == 0) {
+        ch.seg_start[ncand] = M;''', '''    maxd = __reduce_max_sync(FULL, maxd);
+    if (lane == 0) atomicMax(&s_maxd, maxd);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        ch.x->maxd = s_maxd;
+        ch.seg_start[ncand] = M;'''),
+]
