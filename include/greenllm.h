@@ -199,7 +199,8 @@ gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains,
                              int32_t *choice_out, uint8_t *via_fallback_out, void *stream);
 
 /*
- * End to end from host buffers: copies the traces host->device, runs
+ * End to end from host buffers: copies the traces host->device (each distinct
+ * host array once -- traces sharing an array share its device copy), runs
  * gl_eval_grid and gl_argmin_feasible, copies the results device->host and
  * synchronises `stream` before returning.
  *   host_traces      HOST descriptors with HOST data pointers

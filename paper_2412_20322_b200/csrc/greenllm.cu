@@ -777,12 +777,25 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
         return GL_E_INVALID;
     if ((st = device_check())) return st;
     const int64_t rows = grid->rows, cols = grid->cols;
-    std::vector<size_t> off(n_traces);
+    // Each distinct host array is copied once: traces that share a host array
+    // (e.g. rate-independent lengths) share the device copy, and with it their DSD
+    // demand group in gl_eval_grid.
+    std::map<std::pair<const void *, size_t>, size_t> arr_off;  // (host ptr, bytes) -> offset
+    std::vector<std::pair<const void *, size_t>> arr_list;
     size_t total = 0;
+    auto place = [&](const void *h, size_t bytes) {
+        auto key = std::make_pair(h, bytes);
+        if (arr_off.find(key) == arr_off.end()) {
+            arr_off[key] = total;
+            arr_list.push_back(key);
+            total += align256(bytes);
+        }
+    };
     for (int32_t t = 0; t < n_traces; ++t) {
-        off[t] = total;
         const size_t n = (size_t)host_traces[t].n;
-        total += align256(8 * n) + 2 * align256(4 * n);
+        place(host_traces[t].arrival_us, 8 * n);
+        place(host_traces[t].prompt_len, 4 * n);
+        place(host_traces[t].output_len, 4 * n);
     }
     const size_t o_stats = total;
     total += align256(sizeof(gl_chain_stats) * n_chains);
@@ -796,22 +809,16 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&dev), total, stream)))) return st;
     std::vector<gl_trace> dtr(n_traces);
     cudaError_t e = cudaSuccess;
-    for (int32_t t = 0; t < n_traces && e == cudaSuccess; ++t) {
+    for (size_t k = 0; k < arr_list.size() && e == cudaSuccess; ++k)
+        e = cudaMemcpyAsync(dev + arr_off[arr_list[k]], arr_list[k].first, arr_list[k].second,
+                            cudaMemcpyHostToDevice, stream);
+    for (int32_t t = 0; t < n_traces; ++t) {
         const gl_trace &h = host_traces[t];
         const size_t n = (size_t)h.n;
-        unsigned char *base = dev + off[t];
-        dtr[t].arrival_us = reinterpret_cast<int64_t *>(base);
-        dtr[t].prompt_len = reinterpret_cast<uint32_t *>(base + align256(8 * n));
-        dtr[t].output_len = reinterpret_cast<uint32_t *>(base + align256(8 * n) + align256(4 * n));
+        dtr[t].arrival_us = reinterpret_cast<int64_t *>(dev + arr_off[{h.arrival_us, 8 * n}]);
+        dtr[t].prompt_len = reinterpret_cast<uint32_t *>(dev + arr_off[{h.prompt_len, 4 * n}]);
+        dtr[t].output_len = reinterpret_cast<uint32_t *>(dev + arr_off[{h.output_len, 4 * n}]);
         dtr[t].n = h.n;
-        e = cudaMemcpyAsync((void *)dtr[t].arrival_us, h.arrival_us, 8 * n, cudaMemcpyHostToDevice,
-                            stream);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync((void *)dtr[t].prompt_len, h.prompt_len, 4 * n,
-                                cudaMemcpyHostToDevice, stream);
-        if (e == cudaSuccess)
-            e = cudaMemcpyAsync((void *)dtr[t].output_len, h.output_len, 4 * n,
-                                cudaMemcpyHostToDevice, stream);
     }
     int launches = 0;
     if (e == cudaSuccess) {
