@@ -367,3 +367,23 @@ constexpr uint32_t PK_MAXD = 1u << 25;     // ... which needs every demand < 2^2
         ch.x->maxd = s_maxd;
         ch.seg_start[ncand] = M;'''),
 ]
+
+# each 4-lane unit walks a contiguous run of C requests: per-warp work is a sum over
+# 8 x C requests, so the long-tailed lengths average out
+VARIANTS["dsdC"] = [
+    ("k_dsd_demand.cuh", '''    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / DSD_QL;
+    const bool valid = j < g->n;''', '''  const int64_t unit = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / DSD_QL;
+  for (int64_t jj = 0; jj < DSD_C; ++jj) {
+    const int64_t j = unit * DSD_C + jj;
+    if (__all_sync(gmask, j >= g->n)) break;
+    const bool valid = j < g->n;'''),
+    ("k_dsd_demand.cuh", '''    if (valid && sub == 0) g->K[j] = K;
+}''', '''    if (valid && sub == 0) g->K[j] = K;
+  }
+}'''),
+    ("k_dsd_demand.cuh", '''constexpr int DSD_QL = 4;  // lanes per request''', '''constexpr int DSD_QL = 4;  // lanes per request
+constexpr int DSD_C = 16;  // requests per 4-lane unit'''),
+    ("greenllm.cu", '''        dim3 grid((unsigned)((gmax * gl::DSD_QL + 255) / 256), (unsigned)groups.size());''',
+     '''        dim3 grid((unsigned)(((gmax + gl::DSD_C - 1) / gl::DSD_C * gl::DSD_QL + 255) / 256),
+                  (unsigned)groups.size());'''),
+]
