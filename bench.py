@@ -410,7 +410,7 @@ def alu_view(warp_inst, kernel_ms, sm_mhz, grid, lo, hi):
 
 def link_demand_bench(dg, grid, flush, reps=3):
     """NEXT #2 (not part of the timed step): gl_link_demand over all chains of the
-    workload -- the same simulation run leader-only with the batch-size log, then the
+    workload -- the same speculative simulation recording batch-size logs, then the
     1 s sliding-window peak (k_link_*).  Device time with CUDA events; per-kernel
     times from gl_kernel_times."""
     import torch
@@ -444,7 +444,7 @@ def link_demand_bench(dg, grid, flush, reps=3):
     return {"ms": sum(ms) / len(ms), "window_us": 1_000_000,
             "kernel_ms": {k: sum(v) / len(v) for k, v in kt.items()},
             "peak_gbps_range": {k: [min(v), max(v)] for k, v in gbps.items()},
-            "note": "peak link demand of every chain (R45-R47); leader-only decode + "
+            "note": "peak link demand of every chain (R45-R47); logging decode + "
                     "k_link_scan/window/reduce; outside the timed step"}
 
 

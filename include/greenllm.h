@@ -239,9 +239,9 @@ typedef struct {
 } gl_link_stats;           /* 32 B */
 
 /*
- * Simulate every chain exactly as gl_eval_grid does (one leader warp per chain,
- * no speculation, recording the decode batch-size changes) and compute its link
- * demand.  Stream-ordered like gl_eval_grid.
+ * Simulate every chain exactly as gl_eval_grid does (recording the decode
+ * batch-size changes of every run) and compute its link demand.  Stream-ordered
+ * like gl_eval_grid.
  *   traces, chains   as for gl_eval_grid (HOST descriptors, DEVICE data)
  *   params           HOST [n_chains] payload sizes
  *   window_us        >= 1 (1,000,000 = SPEC's 1 s window)

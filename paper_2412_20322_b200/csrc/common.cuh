@@ -29,7 +29,7 @@ struct DSegOut {
     int32_t state;    // 0 unclaimed, 1 claimed, 2 published (release)
     int32_t next;     // candidate index at which the run stopped (idle there)
     int32_t helper;   // whose finish-time buffer holds the run
-    int32_t pad;
+    int32_t nev;      // LOG launches: batch-size log entries of the run (from 2 q0)
 };
 constexpr int32_t SEG_FREE = 0, SEG_CLAIMED = 1, SEG_DONE = 2;
 
@@ -64,7 +64,11 @@ struct DChain {
     int32_t *seg_start; // [nseg + 1] candidate starts (q), seg_start[nseg] = M
     DSegOut *seg_out;   // [nseg]
     DChainX *x;
-    longlong2 *ev;      // LOG launches: batch-size log [2 M + 8] of (T, b) (k_link.cuh)
+    longlong2 *ev;      // LOG launches: batch-size log [2 n + 16] of (T, b) (k_link.cuh);
+                        // a run from decode request q0 writes from position 2 q0, unused
+                        // positions keep the sentinel b = -1 (removed by k_link_scan)
+    longlong2 *ev_spec; // LOG launches: helpers' logs, helper h at ev_spec + h * ev_stride
+    int64_t ev_stride;
     int64_t n;
     int64_t ttft_slo, tpot_slo;
     int64_t out_off;  // first row of this chain in the per-request (ttft, finish) array

@@ -21,7 +21,7 @@
  *                                    speculative decode event loops
  *   k_finalize    (k_decode.cuh)     whole GPU over (chain, request): SLO, hash
  *   k_argmin      (k_argmin.cuh)     one warp per Alg. 1 row
- * gl_link_demand (NEXT #2) runs the same simulation with a leader-only
+ * gl_link_demand (NEXT #2) runs the same simulation with a
  * k_decode<.., LOG> that records batch-size changes, then
  *   k_link_scan / k_link_window / k_link_reduce (k_link.cuh).
  * No tensor cores: nothing on this path is a contraction.
@@ -249,17 +249,19 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     // SM in total; each helper keeps its finish times in a buffer of its own
     // (capped at 8 GiB of scratch)
     int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
-    while (extra > 0 && (size_t)dec_total * 2 * extra * sizeof(int64_t) > ((size_t)8 << 30)) --extra;
-    if (lk) extra = 0;  // the batch-size log needs one sequential run per chain
+    // (gl_link_demand: helpers also keep batch-size logs, 2 entries x 16 B per request)
+    const size_t per_helper_req = 2 * sizeof(int64_t) + (lk ? 2 * sizeof(longlong2) : 0);
+    while (extra > 0 && (size_t)dec_total * per_helper_req * extra > ((size_t)8 << 30)) --extra;
     const size_t off_spec = total;
     // (co-located chains keep two columns per helper: finish and TTFT)
     total += align256(sizeof(int64_t) * (size_t)dec_total * 2 * (size_t)std::max(extra, 1));
     const size_t off_segs = total;
     total += align256(sizeof(int32_t) * (size_t)seg_total);
     // gl_link_demand: batch-size logs [2 n + 8], prefix sums, per-block partials, stats
-    std::vector<int64_t> ev_off(n_chains, 0), rq_off(n_chains, 0);
-    int64_t ev_total = 0, rq_total = 0;
+    std::vector<int64_t> ev_off(n_chains, 0), rq_off(n_chains, 0), evs_off(n_chains, 0);
+    int64_t ev_total = 0, rq_total = 0, evs_total = 0;
     size_t off_ev = 0, off_itpre = 0, off_rqpre = 0, off_links = 0, off_part = 0, off_lstats = 0;
+    size_t off_evd = 0, off_evs = 0;
     if (lk) {
         for (int32_t i = 0; i < n_chains; ++i) {
             const int64_t n = traces[chains[i].trace_idx].n;
@@ -267,9 +269,15 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             ev_total += 2 * n + 16;
             rq_off[i] = rq_total;
             rq_total += n + 8;
+            evs_off[i] = evs_total;
+            evs_total += (2 * n + 16) * std::max(extra, 1);
         }
         off_ev = total;
         total += align256(sizeof(longlong2) * (size_t)ev_total);
+        off_evd = total;  // compacted logs
+        total += align256(sizeof(longlong2) * (size_t)ev_total);
+        off_evs = total;  // helpers' logs
+        total += align256(sizeof(longlong2) * (size_t)evs_total);
         off_itpre = total;
         total += align256(sizeof(int64_t) * (size_t)ev_total);
         off_rqpre = total;
@@ -326,6 +334,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         d.seg_out = reinterpret_cast<gl::DSegOut *>(scratch + off_segout) + seg_off[i];
         d.x = reinterpret_cast<gl::DChainX *>(scratch + off_x) + i;
         d.ev = lk ? reinterpret_cast<longlong2 *>(scratch + off_ev) + ev_off[i] : nullptr;
+        d.ev_spec = lk ? reinterpret_cast<longlong2 *>(scratch + off_evs) + evs_off[i] : nullptr;
+        d.ev_stride = 2 * tr.n + 16;
         if (lk) {
             gl::DLink &L = dl[i];
             L.bpt = lk->params[i].bytes_per_token;
@@ -334,6 +344,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             L.req_pre = reinterpret_cast<int64_t *>(scratch + off_rqpre) + rq_off[i];
             L.part = reinterpret_cast<longlong2 *>(scratch + off_part) + (size_t)(gl::LINK_BLOCKS + 1) * i;
             L.ev_cap = 2 * tr.n + 16;
+            L.ev = reinterpret_cast<longlong2 *>(scratch + off_evd) + ev_off[i];
         }
         d.n = tr.n;
         d.ttft_slo = c.ttft_slo_us;
@@ -355,6 +366,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         e = cudaMemcpyAsync(scratch + off_links, dl.data(), sizeof(gl::DLink) * n_chains,
                             cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(scratch + off_zero, 0, zero_bytes, stream);
+    if (e == cudaSuccess && lk)  // log sentinels: every byte 0xFF -> (T, b) = (-1, -1)
+        e = cudaMemsetAsync(scratch + off_ev, 0xFF, sizeof(longlong2) * (size_t)ev_total, stream);
     int launches = 0;
     if (e == cudaSuccess && !groups.empty()) {
         int64_t gmax = 0;
@@ -417,7 +430,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             }
         }
         // disaggregated chains, then co-located ones (each launch skips the others)
-        if (has_disg && lk) {  // leader-only runs that log the batch size
+        if (has_disg && lk) {  // runs that also log the batch size
             if (max_cap <= 31)
                 e = launch(gl::k_decode<1, false, true>, "k_decode_log");
             else if (max_cap <= 64)

@@ -181,9 +181,10 @@ __device__ __forceinline__ void run_sums(const RunCtx &cx, const uint64_t (&iter
 //          on the GPU (T += pf, its first token at T: the TTFT is written here), and a
 //          request with no decode demand (o = 1) finishes there without joining.
 //          Uses the general loop (the one-row fast paths assume free joins).
-//   LOG    (leader-only launches, link bandwidth demand) every change of the batch
-//          size b appends (T, b) to cx.ev at index ne (ne0 on entry): between two
-//          entries b is constant and iterations run back to back from the first.
+//   LOG    (link bandwidth demand) every change of the batch size b appends (T, b)
+//          to cx.ev at index ne (ne0 = 2 q0 on entry: a run over decode requests
+//          [q0, q1) has at most 2 (q1 - q0) changes); between two entries b is
+//          constant and iterations run back to back from the first.
 template <int SPL, bool ROWS, bool COLO, bool LOG = false>
 __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t k0, bool pub,
                              int32_t ne0 = 0)
@@ -654,7 +655,7 @@ __device__ __forceinline__ void backoff() { __nanosleep(64); }
 // A helper's runs write disjoint stretches of its buffer: it skips candidates
 // inside its previous run (if that run was the true one they are not idle points;
 // if not, the leader runs them itself).
-template <int SPL, bool COLO>
+template <int SPL, bool COLO, bool LOG>
 __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
 {
     const DChain &ch = *cx.ch;
@@ -673,7 +674,8 @@ __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
         if (k >= nseg) break;
         if (k < 0) continue;
         ring.q_end = ch.x->M;
-        const RunOut ro = decode_run<SPL, false, COLO>(cx, ring, ch.seg_start[k], k, false);
+        const int32_t q0 = ch.seg_start[k];
+        const RunOut ro = decode_run<SPL, false, COLO, LOG>(cx, ring, q0, k, false, 2 * q0);
         if (ro.stop_seg < 0) continue;  // aborted: the leader passed k (moot values)
         k_end = ro.stop_seg;
         if (lane == 0) {
@@ -682,6 +684,7 @@ __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
             for (int i = 0; i < 4; ++i) so.sums[i] = ro.sums[i];
             so.next = ro.stop_seg;
             so.helper = cx.hid;
+            so.nev = ro.ne - 2 * q0;
             __threadfence();
             st_release_gpu(&so.state, SEG_DONE);
         }
@@ -691,8 +694,9 @@ __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
 // Leader + helpers (see the file comment).  One warp per block: blocks
 // [0, n_chains) are the leaders of chain blockIdx.x, blocks >= n_chains are
 // helpers of chain blockIdx.x % n_chains.
-//   LOG: leader-only launch (no helper blocks) that also writes the batch-size
-//   log of every disaggregated chain (link bandwidth demand, k_link.cuh).
+//   LOG: also writes the batch-size log of every disaggregated chain (link bandwidth
+//   demand, k_link.cuh): the leader's runs into the chain's log, helper runs into
+//   their own logs, copied by the leader with the finish times when accepted.
 template <int SPL, bool COLO, bool LOG = false>
 __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     k_decode(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
@@ -734,7 +738,8 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     const int32_t nseg = ch.x->nseg;
     const int32_t hid = leader ? -1 : (int32_t)(blockIdx.x / n_chains) - 1;
     RunCtx cx{&ch, steps, magic, perreq + 2 * ch.out_off + 1,
-              ch.spec_fin + (int64_t)max(hid, 0) * ch.spec_stride, cap, lane, nseg, hid, ch.ev};
+              ch.spec_fin + (int64_t)max(hid, 0) * ch.spec_stride, cap, lane, nseg, hid,
+              leader ? ch.ev : ch.ev_spec + (int64_t)max(hid, 0) * ch.ev_stride};
     RingW ring;
     ring.r = ring_r;
     ring.dj = ring_dj;
@@ -744,13 +749,10 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     ring.gpf = COLO ? ch.dec_pf : nullptr;
     ring.fill_next = ring.ready_to = 0;
 
-    if constexpr (!LOG) {
-        if (!leader) {
-            helper_loop<SPL, COLO>(cx, ring);
-            return;
-        }
+    if (!leader) {
+        helper_loop<SPL, COLO, LOG>(cx, ring);
+        return;
     }
-    int32_t ne = 0;
     // The leader hops from idle point to idle point: candidate 0 is one, and a run
     // from an idle point is the true run, so where it stops is the next one.
     int64_t acc[4] = {0, 0, 0, 0};
@@ -770,8 +772,8 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
         st = __shfl_sync(FULL, st, 0);
         if (st < 0) {  // nobody has run k: simulate it here, into the rows
             ring.q_end = M;
-            const RunOut ro = decode_run<SPL, true, COLO, LOG>(cx, ring, ch.seg_start[k], k, true, ne);
-            ne = ro.ne;
+            const RunOut ro = decode_run<SPL, true, COLO, LOG>(cx, ring, ch.seg_start[k], k, true,
+                                                              2 * ch.seg_start[k]);
             for (int i = 0; i < 4; ++i) acc[i] += ro.sums[i];
             mk = max(mk, ro.mk);
             k = ro.stop_seg;
@@ -822,10 +824,15 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
                 }
             }
         }
+        if constexpr (LOG) {  // the run's batch-size log, at the same positions
+            const int64_t p0 = 2 * (int64_t)ch.seg_start[k];
+            const int32_t nev = __ldcg(&so.nev);
+            const longlong2 *src = ch.ev_spec + (int64_t)__ldcg(&so.helper) * ch.ev_stride;
+            for (int32_t e = lane; e < nev; e += 32) ch.ev[p0 + e] = __ldcg(src + p0 + e);
+        }
         k = m;
     }
     if (lane == 0) {
-        if (LOG) ch.x->n_ev = ne;
         st_release_gpu(&ch.x->leader_pos, nseg);
         gl_chain_stats &s = stats[c];
         s.busy_new_us += acc[0];

@@ -7,13 +7,16 @@
 // iteration's start.  demand(t) = bytes issued in [t, t + W); the peak is its
 // maximum over t, attained at an impulse time; peak_t is the earliest such time.
 //
-// The decode iterations come from the batch-size log k_decode<.., LOG> writes:
+// The decode iterations come from the batch-size log k_decode<.., LOG> writes
+// (runs write from position 2 q0, sentinels b = -1 elsewhere; k_link_scan compacts
+// it, in order, into DLink::ev):
 // between entries e and e+1 the batch size b_e is constant and iterations start
 // at T_e, T_e + s_e, ..., k_e = (T_{e+1} - T_e) / s_e of them (s_e = step[b_e]).
 // With C(x) = bytes issued before x (prefix sums over requests and over log
 // entries), demand(t) = C(t + W) - C(t).
 //   k_link_scan    exclusive prefix sums: per request (bytes) and per log entry
-//                  (k_e * b_e * pm), one 1024-thread block per (chain, side)
+//                  (k_e * b_e * pm, after compacting the log), one 1024-thread block
+//                  per (chain, side)
 //   k_link_window  every candidate start: a request impulse (binary searches), or
 //                  the k_e iteration starts of one log entry (binary search once,
 //                  then two pointers that only move forward); per-block best
@@ -30,6 +33,7 @@ struct DLink {
     int64_t *req_pre;    // [n + 1] exclusive prefix of request payload bytes
     int64_t *it_pre;     // [ev_cap + 1] exclusive prefix of iteration payload bytes
     longlong2 *part;     // [LINK_BLOCKS + 1] per-block (peak, t); [LINK_BLOCKS].x = iteration impulses
+    longlong2 *ev;       // [ev_cap] the compacted batch-size log (k_link_scan)
     int64_t ev_cap;
 };
 
@@ -87,6 +91,21 @@ __global__ void __launch_bounds__(1024)
     if (ch.mode != GL_MODE_DPD && ch.mode != GL_MODE_DSD) return;
     const DLink &lk = links[blockIdx.x];
     const bool req = blockIdx.y == 0;
+    if (!req) {  // compact the log (drop the b = -1 sentinels), keeping the order
+        int64_t kept = 0;
+        for (int64_t base = 0; base < lk.ev_cap; base += 1024) {
+            const int64_t i = base + threadIdx.x;
+            longlong2 v = make_longlong2(0, -1);
+            if (i < lk.ev_cap) v = ch.ev[i];
+            const int64_t f = v.y >= 0 ? 1 : 0;
+            int64_t tot;
+            const int64_t ex = block_excl_scan(f, tot, sw);
+            if (f) lk.ev[kept + ex] = v;
+            kept += tot;
+        }
+        if (threadIdx.x == 0) ch.x->n_ev = (int32_t)kept;
+        __syncthreads();
+    }
     const int32_t ne = ch.x->n_ev;
     const int64_t n = req ? ch.n : (int64_t)ne;
     int64_t *out = req ? lk.req_pre : lk.it_pre;
@@ -98,8 +117,8 @@ __global__ void __launch_bounds__(1024)
             if (req) {
                 v = link_req_bytes(ch, lk, i);
             } else {
-                const int64_t k = link_iters(ch, ch.ev, ne, (int32_t)i);
-                v = k * ch.ev[i].y * lk.pm;
+                const int64_t k = link_iters(ch, lk.ev, ne, (int32_t)i);
+                v = k * lk.ev[i].y * lk.pm;
                 cnt += v > 0 ? k : 0;  // iteration impulses with a payload
             }
         }
@@ -148,7 +167,7 @@ __global__ void __launch_bounds__(LINK_THREADS)
     if (ch.mode == GL_MODE_DPD || ch.mode == GL_MODE_DSD) {
         const int64_t n = ch.n;
         const int32_t ne = ch.x->n_ev;
-        const longlong2 *ev = ch.ev;
+        const longlong2 *ev = lk.ev;
         const int64_t *ttft = perreq + 2 * ch.out_off;  // (ttft, finish) rows
         auto c_of = [&](int64_t i) { return __ldg(ch.a + i) + ttft[2 * i]; };
         // bytes issued before x: requests with c < x, and iteration starts < x
