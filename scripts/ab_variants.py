@@ -387,3 +387,35 @@ constexpr int DSD_C = 16;  // requests per 4-lane unit'''),
      '''        dim3 grid((unsigned)(((gmax + gl::DSD_C - 1) / gl::DSD_C * gl::DSD_QL + 255) / 256),
                   (unsigned)groups.size());'''),
 ]
+
+VARIANTS["st32"] = [("k_stages.cuh", "constexpr int ST_WARPS = 16;", "constexpr int ST_WARPS = 32;")]
+
+# 32-bit threshold compares: u < thr with thr <= 2^32 is u < min(thr, 2^32 - 1) except
+# u = 2^32 - 1 against thr = 2^32 (alpha = 1), counted separately
+VARIANTS["thr32"] = [("k_dsd_demand.cuh", '''template <int G>
+__device__ __forceinline__ uint32_t accepted_tokens(uint32_t u, const uint64_t (&thr)[G])
+{
+    uint32_t acc = 1;
+#pragma unroll
+    for (int c = 0; c < G; ++c) acc += ((uint64_t)u < thr[c]) ? 1u : 0u;
+    return acc;
+}''', '''template <int G>
+__device__ __forceinline__ uint32_t accepted_tokens(uint32_t u, const uint32_t (&thr)[G],
+                                                    uint32_t nfull)
+{
+    uint32_t acc = 1 + (u == 0xFFFFFFFFu ? nfull : 0u);
+#pragma unroll
+    for (int c = 0; c < G; ++c) acc += (u < thr[c]) ? 1u : 0u;
+    return acc;
+}'''), ("k_dsd_demand.cuh", '''    uint64_t thr[G];
+#pragma unroll
+    for (int c = 0; c < G; ++c) thr[c] = g->thr[c];''', '''    uint32_t thr[G];
+    uint32_t nfull = 0;  // thresholds equal to 2^32 (always accepted)
+#pragma unroll
+    for (int c = 0; c < G; ++c) {
+        const uint64_t t = g->thr[c];
+        thr[c] = t >= 0xFFFFFFFFull ? 0xFFFFFFFFu : (uint32_t)t;
+        nfull += t > 0xFFFFFFFFull ? 1u : 0u;
+    }'''), ("k_dsd_demand.cuh", '''        const uint32_t a0 = accepted_tokens<G>(w.x, thr), a1 = accepted_tokens<G>(w.y, thr);
+        const uint32_t a2 = accepted_tokens<G>(w.z, thr), a3 = accepted_tokens<G>(w.w, thr);''', '''        const uint32_t a0 = accepted_tokens<G>(w.x, thr, nfull), a1 = accepted_tokens<G>(w.y, thr, nfull);
+        const uint32_t a2 = accepted_tokens<G>(w.z, thr, nfull), a3 = accepted_tokens<G>(w.w, thr, nfull);''')]
