@@ -419,3 +419,27 @@ __device__ __forceinline__ uint32_t accepted_tokens(uint32_t u, const uint32_t (
     }'''), ("k_dsd_demand.cuh", '''        const uint32_t a0 = accepted_tokens<G>(w.x, thr), a1 = accepted_tokens<G>(w.y, thr);
         const uint32_t a2 = accepted_tokens<G>(w.z, thr), a3 = accepted_tokens<G>(w.w, thr);''', '''        const uint32_t a0 = accepted_tokens<G>(w.x, thr, nfull), a1 = accepted_tokens<G>(w.y, thr, nfull);
         const uint32_t a2 = accepted_tokens<G>(w.z, thr, nfull), a3 = accepted_tokens<G>(w.w, thr, nfull);''')]
+
+# a head that is already ready joins inside the light loop (kJ = 0) instead of
+# leaving to the admission loop
+VARIANTS["nohr"] = [
+    ("k_decode.cuh", '''                    const int64_t gap = h_r - T;
+                    const uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, M_c);
+                    if (gap >= 0x80000000ll || I >= 0x80000000u) {''', '''                    const int64_t gap = h_r - T;
+                    const uint32_t kJ = ceil_div_magic((uint32_t)max(gap, (int64_t)0), (uint32_t)st, M_c);
+                    if (gap >= 0x80000000ll || I >= 0x80000000u) {'''),
+    ("k_decode.cuh", '''                        advance_fast();
+                        if (b == cap || h_r <= T) break;''', '''                        advance_fast();
+                        if (b == cap) break;'''),
+    ("k_decode.cuh", '''                        shift_down();
+                        if (nl != 1) {  // several members left at once: leave the loop
+                            load_nbr(b);
+                            break;
+                        }
+                        if (b == 0 || h_r <= T) break;''', '''                        shift_down();
+                        if (nl != 1) {  // several members left at once: leave the loop
+                            load_nbr(b);
+                            break;
+                        }
+                        if (b == 0) break;'''),
+]
