@@ -63,8 +63,23 @@ class DeviceGrid:
                 *[x.data_ptr() for x in tabs], int(ch.ttft_slo_us), int(ch.tpot_slo_us),
                 float(ch.ce_new_g), float(ch.ce_old_g)))
         self.n_chains = len(self.gl_chains)
+        self._arr_cache = {}  # ctypes descriptor arrays, built once per (kind, lo, hi)
         self.chain_n = np.array([grid.traces[c.trace_idx].n for c in grid.chains], np.int64)
         self.last_launches = 0
+
+    def chain_arr(self, lo: int = 0, hi: int | None = None):
+        """gl_chain[lo:hi] as a cached ctypes array (the descriptors never change)."""
+        hi = self.n_chains if hi is None else hi
+        key = ("c", lo, hi)
+        if key not in self._arr_cache:
+            items = self.gl_chains[lo:hi]
+            self._arr_cache[key] = (N.GlChain * len(items))(*items)
+        return self._arr_cache[key]
+
+    def trace_arr(self):
+        if "t" not in self._arr_cache:
+            self._arr_cache["t"] = (N.GlTrace * len(self.gl_traces))(*self.gl_traces)
+        return self._arr_cache["t"]
 
     # ------------------------------------------------------------ host copies
     def pinned_traces(self):
@@ -92,7 +107,7 @@ def eval_grid(dg: DeviceGrid, chain_lo: int = 0, chain_hi: int | None = None, st
     """Simulate chains [chain_lo, chain_hi) -> (stats uint8 tensor [k, 80], per-request
     int64 tensor [sum n, 2] or None).  ``stats`` may be a preallocated view."""
     hi = dg.n_chains if chain_hi is None else chain_hi
-    chains = dg.gl_chains[chain_lo:hi]
+    chains = dg.chain_arr(chain_lo, hi)
     k = len(chains)
     if stats is None:
         stats = torch.empty((k, N.STATS_DTYPE.itemsize), dtype=torch.uint8, device=dg.device)
@@ -100,7 +115,7 @@ def eval_grid(dg: DeviceGrid, chain_lo: int = 0, chain_hi: int | None = None, st
     if per_request:
         tot = int(dg.chain_n[chain_lo:hi].sum())
         pr = torch.empty((tot, 2), dtype=torch.int64, device=dg.device)
-    dg.last_launches = N.eval_grid(dg.gl_traces, chains, stats.data_ptr(),
+    dg.last_launches = N.eval_grid(dg.trace_arr(), chains, stats.data_ptr(),
                                    pr.data_ptr() if pr is not None else None, _stream_ptr(stream))
     return stats, pr
 
@@ -187,7 +202,7 @@ def argmin_feasible(dg: DeviceGrid, stats: torch.Tensor, want_carbon: bool = Tru
     choice = torch.empty(g.rows, dtype=torch.int32, device=dg.device)
     fb = torch.empty(g.rows, dtype=torch.uint8, device=dg.device)
     dg.last_launches = N.argmin_feasible(
-        stats.data_ptr(), dg.gl_chains, g.scenarios, g.rows, g.cols, g.row_scenario,
+        stats.data_ptr(), dg.chain_arr(), g.scenarios, g.rows, g.cols, g.row_scenario,
         g.cell_chain, g.slo_num, g.slo_den, g.priority, g.default_col,
         carbon.data_ptr() if carbon is not None else None, choice.data_ptr(), fb.data_ptr(),
         _stream_ptr(stream))
@@ -218,7 +233,7 @@ def evaluate_host(dg: DeviceGrid, host_traces, want_carbon: bool = False, stream
                          pinned(g.rows * g.cols * 8).view(np.float64).reshape(g.rows, g.cols)
                          if want_carbon else None,
                          pinned(g.rows * 4).view(np.int32), pinned(g.rows), 0, 0, 0)
-    out.launches = N.evaluate_host(gl_tr, dg.gl_chains, g.scenarios, g.rows, g.cols,
+    out.launches = N.evaluate_host(gl_tr, dg.chain_arr(), g.scenarios, g.rows, g.cols,
                                    g.row_scenario, g.cell_chain, g.slo_num, g.slo_den, g.priority,
                                    g.default_col, out.stats, out.carbon, out.choice,
                                    out.via_fallback, _stream_ptr(stream))

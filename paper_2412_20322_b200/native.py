@@ -137,9 +137,20 @@ def check(status: int, where: str):
         raise GreenLLMError(status, where)
 
 
+def _arr(kind, items):
+    """ctypes array of `kind` from a list (or a prebuilt array, passed through)."""
+    return items if isinstance(items, C.Array) else (kind * len(items))(*items)
+
+
+def _scen_arr(scen):
+    """[S, 3] float64 scenarios viewed in place as gl_scenario[S] (same layout)."""
+    s = np.ascontiguousarray(scen, dtype=np.float64).reshape(-1, 3)
+    return s, s.ctypes.data_as(C.POINTER(GlScenario))
+
+
 def eval_grid(traces, chains, stats_ptr: int, per_request_ptr: int | None, stream: int):
-    t_arr = (GlTrace * len(traces))(*traces)
-    c_arr = (GlChain * len(chains))(*chains)
+    t_arr = _arr(GlTrace, traces)
+    c_arr = _arr(GlChain, chains)
     check(lib().gl_eval_grid(t_arr, len(traces), c_arr, len(chains), stats_ptr,
                              per_request_ptr or None, stream or None), "gl_eval_grid")
     return lib().gl_last_launch_count()
@@ -148,8 +159,8 @@ def eval_grid(traces, chains, stats_ptr: int, per_request_ptr: int | None, strea
 def link_demand(traces, chains, params, window_us: int, stats_ptr: int | None, link_ptr: int,
                 stream: int):
     """params: [(bytes_per_token, bytes_per_member_step)] per chain."""
-    t_arr = (GlTrace * len(traces))(*traces)
-    c_arr = (GlChain * len(chains))(*chains)
+    t_arr = _arr(GlTrace, traces)
+    c_arr = _arr(GlChain, chains)
     p_arr = (GlLinkParams * len(chains))(*[GlLinkParams(int(a), int(b)) for a, b in params])
     check(lib().gl_link_demand(t_arr, len(traces), c_arr, len(chains), p_arr, int(window_us),
                                stats_ptr or None, link_ptr, stream or None), "gl_link_demand")
@@ -157,10 +168,9 @@ def link_demand(traces, chains, params, window_us: int, stats_ptr: int | None, l
 
 
 def savings_surface(stats_ptr: int, chains, pairs, scen: np.ndarray, out_ptr: int, stream: int):
-    c_arr = (GlChain * len(chains))(*chains)
+    c_arr = _arr(GlChain, chains)
     p_arr = (GlSavingsPair * len(pairs))(*[GlSavingsPair(int(d), int(s)) for d, s in pairs])
-    sc = np.ascontiguousarray(scen, dtype=np.float64).reshape(-1, 3)
-    s_arr = (GlScenario * len(sc))(*[GlScenario(*map(float, x)) for x in sc])
+    sc, s_arr = _scen_arr(scen)
     check(lib().gl_savings_surface(stats_ptr, len(chains), c_arr, p_arr, len(pairs), s_arr,
                                    len(sc), out_ptr, stream or None), "gl_savings_surface")
     return lib().gl_last_launch_count()
@@ -180,9 +190,8 @@ def argmin_feasible(stats_ptr: int, chains, scen: np.ndarray, rows: int, cols: i
                     row_scenario: np.ndarray, cell_chain: np.ndarray, slo_num: int, slo_den: int,
                     priority: int, default_col: int, carbon_ptr: int | None, choice_ptr: int,
                     fb_ptr: int, stream: int):
-    c_arr = (GlChain * len(chains))(*chains)
-    s = np.ascontiguousarray(scen, dtype=np.float64).reshape(-1, 3)
-    s_arr = (GlScenario * len(s))(*[GlScenario(*map(float, x)) for x in s])
+    c_arr = _arr(GlChain, chains)
+    s, s_arr = _scen_arr(scen)
     rs = np.ascontiguousarray(row_scenario, dtype=np.int32)
     cc = np.ascontiguousarray(cell_chain, dtype=np.int32)
     g = GlGrid(rows, cols, rs.ctypes.data, cc.ctypes.data)
@@ -195,10 +204,9 @@ def argmin_feasible(stats_ptr: int, chains, scen: np.ndarray, rows: int, cols: i
 def evaluate_host(host_traces, chains, scen, rows, cols, row_scenario, cell_chain, slo_num,
                   slo_den, priority, default_col, stats_out: np.ndarray, carbon_out,
                   choice_out: np.ndarray, fb_out: np.ndarray, stream: int):
-    t_arr = (GlTrace * len(host_traces))(*host_traces)
-    c_arr = (GlChain * len(chains))(*chains)
-    s = np.ascontiguousarray(scen, dtype=np.float64).reshape(-1, 3)
-    s_arr = (GlScenario * len(s))(*[GlScenario(*map(float, x)) for x in s])
+    t_arr = _arr(GlTrace, host_traces)
+    c_arr = _arr(GlChain, chains)
+    s, s_arr = _scen_arr(scen)
     rs = np.ascontiguousarray(row_scenario, dtype=np.int32)
     cc = np.ascontiguousarray(cell_chain, dtype=np.int32)
     g = GlGrid(rows, cols, rs.ctypes.data, cc.ctypes.data)
