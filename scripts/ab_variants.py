@@ -443,3 +443,41 @@ VARIANTS["nohr"] = [
                         }
                         if (b == 0) break;'''),
 ]
+
+# packed keys only for chains k_segments flags as overloaded (rho >= 1.2): the
+# saturated loop wins there, the near-saturated / light chains keep the base loops
+def _pksel():
+    v = []
+    for f, old, new in VARIANTS["packed"]:
+        if f == "k_decode.cuh" and "pk_done = true" in new:
+            new = new.replace("if (xx->maxd < PK_MAXD) {", "if (xx->maxd < PK_MAXD && xx->pk) {", 1)
+        if f == "common.cuh":
+            new = new.replace('''    uint32_t maxd;       // largest decode demand of the chain (k_segments)
+    int32_t pad[2];''', '''    uint32_t maxd;       // largest decode demand of the chain (k_segments)
+    int32_t pk;          // 1: overloaded chain, packed-key loops (k_segments)
+    int32_t pad;''')
+        if f == "k_stages.cuh" and "s_maxd = 0;" in new:
+            new = new.replace("    uint32_t maxd = 0;", "    uint32_t maxd = 0;\n    unsigned long long sumd = 0;")
+            new = new.replace("        s_maxd = 0;", "        s_maxd = 0;\n        s_sumd = 0;")
+        if f == "k_stages.cuh" and "__shared__ uint32_t s_maxd;" in new:
+            new = new + "\n    __shared__ unsigned long long s_sumd;"
+        if f == "k_stages.cuh" and "maxd = max(maxd, dq);" in new:
+            new = new.replace("maxd = max(maxd, dq);", "maxd = max(maxd, dq);\n                sumd += dq;")
+        if f == "k_stages.cuh" and "ch.x->maxd = s_maxd;" in new:
+            new = new.replace('''    maxd = __reduce_max_sync(FULL, maxd);
+    if (lane == 0) atomicMax(&s_maxd, maxd);''', '''    maxd = __reduce_max_sync(FULL, maxd);
+    for (int o = 16; o; o >>= 1) sumd += __shfl_xor_sync(FULL, sumd, o);
+    if (lane == 0) {
+        atomicMax(&s_maxd, maxd);
+        atomicAdd(&s_sumd, sumd);
+    }''')
+            new = new.replace('''        ch.x->maxd = s_maxd;''', '''        ch.x->maxd = s_maxd;
+        // offered decode load at a full batch: rho = sum(d) step[cap] / (cap span)
+        const int64_t span = M > 1 ? __ldg(ch.dec_r + M - 1) - __ldg(ch.dec_r) : 0;
+        const double work = (double)s_sumd * (double)__ldg(ch.step + ch.cap);
+        ch.x->pk = (!colo && M > 1 && work >= 1.2 * (double)ch.cap * (double)span) ? 1 : 0;''')
+        v.append((f, old, new))
+    return v
+
+
+VARIANTS["pksel"] = _pksel()
