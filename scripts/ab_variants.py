@@ -319,8 +319,8 @@ VARIANTS["nl2"] = [("k_decode.cuh", '''                        fr |= lm;
 
 # packed keys (F << 5 | lane) for DPD/DSD caps <= 31: one REDUX gives the leaver
 # (no ballot / popc), joins update kmin uniformly; ring refills hoisted
-_PK_BLOCK = open("/tmp/pk_variant_block.txt").read() if __import__("os").path.exists(
-    "/tmp/pk_variant_block.txt") else ""
+_PK_BLOCK = open(__import__("os").path.join(__import__("os").path.dirname(__file__), "ab_blocks",
+                                            "packed_spl1.txt")).read()
 VARIANTS["packed"] = [
     ("k_decode.cuh", '''constexpr int DEC_WARPS = 1;  // one warp per k_decode block (leader or helper)''',
      '''constexpr int DEC_WARPS = 1;  // one warp per k_decode block (leader or helper)
