@@ -1,4 +1,11 @@
-"""Source edits for scripts/ab_build.py: name -> [(file, old, new), ...]."""
+"""Source edits for scripts/ab_build.py: name -> [(file, old, new), ...].
+
+The record of the round's same-box A/B experiments (results in DESIGN.md §10).
+Variants in MERGED were adopted and are part of the current source, so their
+edits no longer apply; the others were measured against the source of their time
+and may need the old text to build."""
+
+MERGED = {"fastadv", "nl"}
 
 LIGHT_HEAD_OLD = '''                    const int64_t gap = h_r - T;
                     const uint32_t kJ = ceil_div_magic((uint32_t)gap, (uint32_t)st, M_c);
