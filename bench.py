@@ -460,7 +460,7 @@ def analysis_bench(dg, grid, reps=3):
     from paper_2412_20322_b200.inputs import build_config
     from paper_2412_20322_b200.inputs.cf import observation_mask
 
-    def timed(fn):
+    def timed(fn, reps=reps):
         fn()
         torch.cuda.synchronize()
         ms = []
@@ -493,7 +493,25 @@ def analysis_bench(dg, grid, reps=3):
     m = torch.from_numpy(observation_mask(grid.rows, grid.cols, 0.3, seed=42)).to(dg.device)
     x, mm = torch.stack([carbon, att]), torch.stack([m, m])
     cf_ms = timed(lambda: api.complete_matrices(x, mm, 2, 0.1, 200, lo=0.0))
-    return {"cfg6_step": {"ms": cfg6_ms, "timing_chains": len(g6.chains),
+    # the other BASELINE configurations, one device-timed step each (inputs resident)
+    others = {}
+    for k in (1, 2, 3, 5):
+        gk = build_config(k)
+        dk = api.DeviceGrid(gk, dg.device)
+        sk, _ = api.eval_grid(dk)
+        N.profile_enable(True)
+        N.kernel_times()
+        ms_k = timed(lambda: api.argmin_feasible(dk, api.eval_grid(dk, stats=sk)[0]), reps=2)
+        ktk = {}
+        for name, t in N.kernel_times():
+            ktk.setdefault(name, []).append(t)
+        N.profile_enable(False)
+        others[f"cfg{k}"] = {"ms": ms_k, "timing_chains": len(gk.chains),
+                             "requests_per_trace": gk.traces[0].n, "grid": [gk.rows, gk.cols],
+                             "kernel_ms": {n: sum(v) / len(v) for n, v in ktk.items()}}
+        del dk, sk
+    return {"other_configs": others,
+            "cfg6_step": {"ms": cfg6_ms, "timing_chains": len(g6.chains),
                           "grid": [g6.rows, g6.cols],
                           "kernel_ms": {k: sum(v) / len(v) for k, v in kt6.items()},
                           "workload": "cfg6: cfg4 + Standalone and SpecDecode (A100) columns, "
