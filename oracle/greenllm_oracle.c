@@ -23,14 +23,23 @@
  *            (Table 2; per-request mean TPOT, R25)
  *   carbon   Eqs. 1-3 with the fixed expression of R34
  *   Alg. 1   feasible set, argmin, fallback
- * Every rule R1-R40 it follows is listed in DESIGN.md §2.
+ * and the SURVEY §8(f) NEXT rows:
+ *   co-located Standalone / SpecDecode serving (R41-R44)
+ *   link bandwidth demand, 1 s sliding-window peak (R45-R47; Fig. 4)
+ *   §5 savings analysis per (Case 2, Standalone) pair (R48-R49; Eqs. 4-6)
+ *   collaborative filtering by ALS (R50-R53; Alg. 1 line 1)
+ * Every rule R1-R53 it follows is listed in DESIGN.md §2.
  *
  * Pins (tests/test_oracle_pins.py): Philox known-answer vectors; the E[acc]
  * closed form (1-alpha^(g+1))/(1-alpha); hand-worked queueing examples
  * (SURVEY Appendix A.1-A.5); an independent 1-us tick brute force on <=10
  * requests and exhaustive tiny enumerations; the max-plus longest-path form of
  * stages 1-2; the cap=1 Lindley recursion; the isolated-request and D/D/1
- * closed forms; carbon closed forms S:55-74; Alg. 1 against brute force.
+ * closed forms; carbon closed forms S:55-74; Alg. 1 against brute force;
+ * link demand against closed forms, S:372 accounting and the tick brute force
+ * scanning every window start (tests/test_oracle_link.py); the savings analysis
+ * against S:500 / S:499 and Eq. 5's three lines (tests/test_oracle_savings.py);
+ * ALS against numpy's ridge solves and exact rank-1 recovery (tests/test_oracle_cf.py).
  *
  * Build: gcc -O2 -std=c11 -ffp-contract=off -shared -fPIC (no threads, no SIMD
  * intrinsics).
