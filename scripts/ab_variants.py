@@ -488,3 +488,29 @@ def _pksel():
 
 
 VARIANTS["pksel"] = _pksel()
+
+# the time / counter advance k = min(kJ, kL) happens before the join/leave branch
+VARIANTS["kfirst"] = [
+    ("k_decode.cuh", '''                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;
+                        I += kJ;
+                        c_b += (lane == b) ? kJ : 0u;
+                        if (((nxt + 2) & 127) <= 1) break;  // ring refill due: joins at the top''',
+     '''                    const bool jn = kJ < kL;
+                    const uint32_t k = jn ? kJ : kL;
+                    T += (int64_t)k * st;
+                    I += k;
+                    c_b += (lane == b) ? k : 0u;
+                    if (jn) {  // the head joins at T + kJ * step[b]
+                        if (((nxt + 2) & 127) <= 1) break;  // ring refill due: joins at the top'''),
+    ("k_decode.cuh", '''                    } else {  // leave at iteration fmin (R16)
+                        T += (int64_t)kL * st;
+                        I = fmin;
+                        c_b += (lane == b) ? kL : 0u;
+                        const bool lv = Fm == I;''', '''                    } else {  // leave at iteration fmin (R16)
+                        const bool lv = Fm == I;'''),
+]
+# branch layout hint: the leave is the more frequent event
+VARIANTS["expect"] = [("k_decode.cuh", '''                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;''', '''                    if (__builtin_expect(kJ < kL, 0)) {  // the head joins at T + kJ * step[b]
+                        T += (int64_t)kJ * st;''')]
