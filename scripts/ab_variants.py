@@ -514,3 +514,25 @@ VARIANTS["kfirst"] = [
 VARIANTS["expect"] = [("k_decode.cuh", '''                    if (kJ < kL) {  // the head joins at T + kJ * step[b]
                         T += (int64_t)kJ * st;''', '''                    if (__builtin_expect(kJ < kL, 0)) {  // the head joins at T + kJ * step[b]
                         T += (int64_t)kJ * st;''')]
+
+# 32-bit relative time inside the light-load loop (DPD/DSD)
+_T32 = open(__import__("os").path.join(__import__("os").path.dirname(__file__), "ab_blocks",
+                                       "t32_light.txt")).read()
+VARIANTS["t32"] = [
+    ("k_decode.cuh", '''                bool slow = false;
+                for (;;) {
+                    const int64_t st = st_c;
+                    const uint32_t kL = fmin - I;
+                    const int64_t gap = h_r - T;''', _T32 + '''                for (;;) {
+                    const int64_t st = st_c;
+                    const uint32_t kL = fmin - I;
+                    const int64_t gap = h_r - T;'''),
+    ("k_decode.cuh", '''                        if (b == 0 || h_r <= T) break;
+                    }
+                }
+                if (!slow) continue;''', '''                        if (b == 0 || h_r <= T) break;
+                    }
+                }
+              }
+                if (!slow) continue;'''),
+]
