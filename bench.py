@@ -162,6 +162,50 @@ def cpu_baseline(grid, budget_s, chain_order=None):
                 chain_request_sims_per_s=len(done) * reqs / t_all)
 
 
+def _oracle_chain_worker(args):
+    """One whole chain through the oracle in a worker process (all-cores baseline)."""
+    cfg, n, ci = args
+    from oracle import oracle as O
+    from paper_2412_20322_b200.inputs import build_config
+    g = _worker_grid(cfg, n)
+    ch = g.chains[ci]
+    t0 = time.perf_counter()
+    O.simulate_chain(g.traces[ch.trace_idx], ch, per_request=False)
+    return time.perf_counter() - t0
+
+
+_WORKER_GRID = {}
+
+
+def _worker_grid(cfg, n):
+    from paper_2412_20322_b200.inputs import build_config
+    if (cfg, n) not in _WORKER_GRID:
+        _WORKER_GRID[(cfg, n)] = build_config(cfg, n=n)
+    return _WORKER_GRID[(cfg, n)]
+
+
+def cpu_baseline_all_cores(grid, n):
+    """The same single-threaded oracle, one chain per process across every host core
+    (per-core rate, aggregate, nproc).  Timing chains only (the
+    carbon/Alg. 1 epilogue is < 1% of the oracle's time); wall clock of the pool."""
+    import multiprocessing as mp
+    cores = os.cpu_count() or 1
+    jobs = [(4, n, ci) for ci in range(len(grid.chains))]
+    ctx = mp.get_context("fork")
+    with ctx.Pool(min(cores, len(jobs)), initializer=_worker_grid, initargs=(4, n)) as pool:
+        pool.map(_oracle_chain_worker, jobs[:min(cores, len(jobs))])  # warm the workers
+        t0 = time.perf_counter()
+        per = pool.map(_oracle_chain_worker, jobs)
+        wall = time.perf_counter() - t0
+    reqs = grid.traces[0].n
+    cells = int((grid.cell_chain >= 0).sum())
+    return {"value": cells * reqs / wall, "unit": UNIT, "cores": min(cores, len(jobs)),
+            "kind": "oracle", "sample": f"all {len(jobs)} timing chains x {reqs} requests, one "
+            f"process per chain on {min(cores, len(jobs))} of {cores} host cores, {wall:.1f} s wall",
+            "chain_request_sims_per_s": len(jobs) * reqs / wall,
+            "per_core_chain_request_sims_per_s": reqs / (sum(per) / len(per))}
+
+
 def _subset(grid, chain_ids):
     from paper_2412_20322_b200.inputs import subset_chains
     return subset_chains(grid, chain_ids)
@@ -348,6 +392,10 @@ def run_ours(args):
                          f"(all {cb['cells']} of their grid cells), single-threaded, "
                          f"{cb['seconds']:.1f} s",
                "chain_request_sims_per_s": cb["chain_request_sims_per_s"]}
+        try:
+            cpu["all_cores"] = cpu_baseline_all_cores(grid, args.n)
+        except Exception as exc:  # a host without fork / enough memory: report why
+            cpu["all_cores"] = {"unavailable": repr(exc)[:200]}
     clocks = sampler.summary(t_wall0, t_wall1)
     # cycles per decode event on the critical path.  Every
     # decode request is one join and one leave event; the launch lasts as long as
