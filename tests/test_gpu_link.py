@@ -126,3 +126,18 @@ def test_config3_bandwidth_axis():
     ids = list(range(0, 128, 9))
     lk = link_parity(subset_chains(g, ids), 1_000_000, check_eval=False)
     assert (lk["total_bytes"] > 0).all()
+
+
+@pytest.mark.parametrize("n_chains,n", [(4, 30000), (60, 3000)])
+def test_logged_speculation_stress(n_chains, n):
+    # quiet and busy phases: many idle points, long helper runs, aborted runs; the
+    # helpers' logs are copied by the leader only for accepted runs
+    from tests.test_gpu_parity import _phased_case
+    rng = np.random.default_rng(4242 + n_chains)
+    pairs, params = [], []
+    for i in range(n_chains):
+        mode = (MODE_DPD, MODE_DSD)[i % 2]
+        pairs.append(_phased_case(rng, n, mode, int(rng.choice([4, 16, 31, 48])),
+                                  monotone=(i % 4 < 2)))
+        params.append((int(rng.integers(1, 60)), int(rng.integers(1, 90))))
+    link_parity(grid_of(pairs), int(rng.choice([1000, 50_000, 1_000_000])), params)
