@@ -660,4 +660,53 @@ int32_t oracle_als_complete(const double *x, const uint8_t *obs, int32_t rows, i
     return status;
 }
 
+/*
+ * Alg. 1 lines 2-9 on explicit matrices C and SLO_att -- e.g. the ones
+ * collaborative filtering completed (line 1) -- with fractional attainments (R54):
+ * feasible iff present and SLO_att >= target; argmin C, ties -> higher SLO_att ->
+ * lower column; nothing feasible -> via_fallback = 1 and priority SLO -> argmax
+ * SLO_att (ties -> lower C -> lower column), priority DEFAULT -> default_col; a row
+ * without a present cell -> -1 (SLO) .  present may be NULL (all present).
+ */
+void oracle_alg1_matrices(int32_t rows, int32_t cols, const double *carbon, const double *att,
+                          const uint8_t *present, double target, int32_t priority,
+                          int32_t default_col, int32_t *choice, uint8_t *via_fallback)
+{
+    for (int32_t row = 0; row < rows; ++row) {
+        int32_t best = -1;
+        for (int32_t col = 0; col < cols; ++col) {
+            int64_t k = (int64_t)row * cols + col;
+            if (present && !present[k]) continue;
+            if (!(att[k] >= target)) continue;
+            if (best < 0) {
+                best = col;
+                continue;
+            }
+            int64_t kb = (int64_t)row * cols + best;
+            if (carbon[k] < carbon[kb] || (carbon[k] == carbon[kb] && att[k] > att[kb])) best = col;
+        }
+        if (best >= 0) {
+            choice[row] = best;
+            via_fallback[row] = 0;
+            continue;
+        }
+        via_fallback[row] = 1;
+        if (priority != 0) {
+            choice[row] = default_col;
+            continue;
+        }
+        for (int32_t col = 0; col < cols; ++col) {
+            int64_t k = (int64_t)row * cols + col;
+            if (present && !present[k]) continue;
+            if (best < 0) {
+                best = col;
+                continue;
+            }
+            int64_t kb = (int64_t)row * cols + best;
+            if (att[k] > att[kb] || (att[k] == att[kb] && carbon[k] < carbon[kb])) best = col;
+        }
+        choice[row] = best;
+    }
+}
+
 int32_t oracle_version(void) { return 1; }

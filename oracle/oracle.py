@@ -84,6 +84,10 @@ def lib():
                                               C.c_int32, C.c_double, C.c_int32, C.c_void_p,
                                               C.c_double, C.c_double, C.c_void_p, C.c_void_p,
                                               C.c_void_p]
+            L.oracle_alg1_matrices.restype = None
+            L.oracle_alg1_matrices.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p,
+                                               C.c_void_p, C.c_double, C.c_int32, C.c_int32,
+                                               C.c_void_p, C.c_void_p]
             L.oracle_alg1.restype = None
             L.oracle_alg1.argtypes = [C.c_int32, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p,
                                       C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_int32,
@@ -247,6 +251,21 @@ def als_complete(x, observed, rank, lam, iters, v0, lo=-np.inf, hi=np.inf):
     st = lib().oracle_als_complete(_ptr(x), _ptr(m), rows, cols, rank, float(lam), int(iters),
                                    _ptr(v), float(lo), float(hi), _ptr(out), _ptr(U), _ptr(V))
     return out, U, V, int(st)
+
+
+def alg1_matrices(carbon, att, present=None, target=0.9, priority=0, default_col=-1):
+    """Alg. 1 on explicit [rows, cols] matrices with fractional attainment
+    (oracle_alg1_matrices) -> (choice int32[rows], via_fallback uint8[rows])."""
+    carbon = _c(carbon, np.float64)
+    att = _c(att, np.float64)
+    rows, cols = carbon.shape
+    pr = None if present is None else _c(present, np.uint8)
+    choice = np.zeros(rows, np.int32)
+    fb = np.zeros(rows, np.uint8)
+    lib().oracle_alg1_matrices(rows, cols, _ptr(carbon), _ptr(att),
+                               None if pr is None else _ptr(pr), float(target), priority,
+                               default_col, _ptr(choice), _ptr(fb))
+    return choice, fb
 
 
 def alg1(total, ok, n, present, cap_ok, slo_num=9, slo_den=10, priority=0, default_col=-1):

@@ -110,3 +110,59 @@ def test_empty_row_and_column_status():
     m = np.ones((6, 4), np.uint8)
     m[:, 3] = 0
     assert O.als_complete(x, m, 1, 0.1, 3, als_init(4, 1))[3] == 2
+
+
+# ---- Alg. 1 on explicit (completed) matrices, R54
+def test_alg1_matrices_spec_examples_S431_441():
+    # 2x2 example: attainment [0.95, 0.92], carbon [5, 4], target 0.9 -> the second column
+    ch, fb = O.alg1_matrices(np.array([[5.0, 4.0]]), np.array([[0.95, 0.92]]), target=0.9)
+    assert ch[0] == 1 and fb[0] == 0
+    # fallback, priority SLO: attainment [0.5, 0.7, 0.6] -> argmax = second column
+    ch, fb = O.alg1_matrices(np.array([[1.0, 2.0, 3.0]]), np.array([[0.5, 0.7, 0.6]]), target=0.9)
+    assert ch[0] == 1 and fb[0] == 1
+    # priority DEFAULT -> the default column regardless of the values
+    ch, fb = O.alg1_matrices(np.array([[1.0, 2.0, 3.0]]), np.array([[0.5, 0.7, 0.6]]), target=0.9,
+                             priority=1, default_col=2)
+    assert ch[0] == 2 and fb[0] == 1
+    # all attainments equal in the fallback -> lowest carbon (tie rule)
+    ch, fb = O.alg1_matrices(np.array([[3.0, 1.0, 2.0]]), np.array([[0.5, 0.5, 0.5]]), target=0.9)
+    assert ch[0] == 1
+
+
+def test_alg1_matrices_vs_brute_force():
+    rng = np.random.default_rng(8)
+    for _ in range(1000):
+        rows, cols = 6, 8
+        carbon = rng.choice([1.0, 2.0, 3.0, 4.0], (rows, cols))  # ties on purpose
+        att = rng.choice([0.5, 0.85, 0.9, 0.95, 1.0], (rows, cols))
+        present = (rng.random((rows, cols)) < 0.85).astype(np.uint8)
+        target = float(rng.choice([0.9, 0.95]))
+        ch, fb = O.alg1_matrices(carbon, att, present, target)
+        for r in range(rows):
+            cols_p = [c for c in range(cols) if present[r, c]]
+            feas = [c for c in cols_p if att[r, c] >= target]
+            if feas:
+                want = min(feas, key=lambda c: (carbon[r, c], -att[r, c], c))
+                assert (ch[r], fb[r]) == (want, 0)
+            elif cols_p:
+                want = min(cols_p, key=lambda c: (-att[r, c], carbon[r, c], c))
+                assert (ch[r], fb[r]) == (want, 1)
+            else:
+                assert (ch[r], fb[r]) == (-1, 1)
+
+
+def test_alg1_matrices_agrees_with_integer_alg1():
+    # attainments ok/n: fp64 ok/n >= 0.9 decides exactly as 10 ok >= 9 n (the gap
+    # |ok/n - 0.9| >= 1/(10 n) is far above one ulp), so both forms must choose alike
+    rng = np.random.default_rng(9)
+    for _ in range(300):
+        rows, cols = 5, 7
+        n = rng.integers(1, 200, (rows, cols))
+        ok = (n * rng.choice([0.5, 0.89, 0.9, 0.91, 1.0], (rows, cols))).astype(np.int64)
+        total = rng.choice([1.0, 2.0, 2.5], (rows, cols))
+        present = (rng.random((rows, cols)) < 0.9).astype(np.uint8)
+        cap = np.ones((rows, cols), np.uint8)
+        for prio in (0, 1):
+            a = O.alg1(total, ok, n, present, cap, 9, 10, prio, 3)
+            b = O.alg1_matrices(total, ok / n, present, 0.9, prio, 3)
+            assert np.array_equal(a[0], b[0]) and np.array_equal(a[1], b[1])
