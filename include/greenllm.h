@@ -314,6 +314,23 @@ gl_status gl_complete_matrices(const double *x, const uint8_t *observed, int32_t
                                double *out, double *u_out, double *v_out, int32_t *status_out,
                                void *stream);
 
+/*
+ * Alg. 1 lines 2-9 on explicit matrices -- C and SLO_att as the paper
+ * states them, e.g. after gl_complete_matrices filled the unmeasured cells
+ * (line 1).  Attainments are fractions (R54): a cell is feasible iff present and
+ * att >= slo_target; per row argmin carbon, ties -> higher att -> lower column;
+ * nothing feasible -> via_fallback = 1 and priority SLO -> argmax att (ties ->
+ * lower carbon -> lower column; -1 if no present cell), DEFAULT -> default_col.
+ *   carbon, att   DEVICE double [rows*cols] row-major; present DEVICE uint8 or NULL
+ *   choice_out    DEVICE int32 [rows];  via_fallback_out DEVICE uint8 [rows]
+ * Errors: GL_E_INVALID (NULL, rows/cols <= 0, bad priority), GL_E_DOMAIN (target
+ * not in [0, 1] or non-finite), GL_E_LOOKUP (default_col out of range).
+ */
+gl_status gl_argmin_matrices(const double *carbon, const double *att, const uint8_t *present,
+                             int32_t rows, int32_t cols, double slo_target, int32_t priority,
+                             int32_t default_col, int32_t *choice_out, uint8_t *via_fallback_out,
+                             void *stream);
+
 /* Number of CUDA kernels the last successful call on this thread enqueued. */
 int32_t gl_last_launch_count(void);
 

@@ -188,6 +188,22 @@ def complete_matrices(x: torch.Tensor, observed: torch.Tensor, rank: int = 2,
     return out, U, V, status
 
 
+def argmin_matrices(carbon: torch.Tensor, att: torch.Tensor, present: torch.Tensor | None = None,
+                    target: float = 0.9, priority: int = 0, default_col: int = -1, stream=None):
+    """Alg. 1 on explicit [rows, cols] matrices (gl_argmin_matrices), e.g. the ones
+    complete_matrices filled -> (choice int32 [rows], via_fallback uint8 [rows])."""
+    carbon = carbon.contiguous().to(torch.float64)
+    att = att.contiguous().to(torch.float64)
+    rows, cols = carbon.shape
+    pr = None if present is None else present.contiguous().to(torch.uint8)
+    choice = torch.empty(rows, dtype=torch.int32, device=carbon.device)
+    fb = torch.empty(rows, dtype=torch.uint8, device=carbon.device)
+    N.argmin_matrices(carbon.data_ptr(), att.data_ptr(), None if pr is None else pr.data_ptr(),
+                      rows, cols, target, priority, default_col, choice.data_ptr(), fb.data_ptr(),
+                      _stream_ptr(stream))
+    return choice, fb
+
+
 def link_numpy(link: torch.Tensor) -> np.ndarray:
     """Device link tensor -> numpy structured array (gl_link_stats fields)."""
     return link.detach().cpu().numpy().view(N.LINK_DTYPE).reshape(-1)

@@ -775,6 +775,33 @@ gl_status gl_complete_matrices(const double *x, const uint8_t *observed, int32_t
     return GL_OK;
 }
 
+gl_status gl_argmin_matrices(const double *carbon, const double *att, const uint8_t *present,
+                             int32_t rows, int32_t cols, double slo_target, int32_t priority,
+                             int32_t default_col, int32_t *choice_out, uint8_t *via_fallback_out,
+                             void *stream_)
+{
+    g_last_launches = 0;
+    cudaStream_t stream = static_cast<cudaStream_t>(stream_);
+    if (!carbon || !att || !choice_out || !via_fallback_out || rows <= 0 || cols <= 0)
+        return GL_E_INVALID;
+    if (priority != GL_PRIORITY_SLO && priority != GL_PRIORITY_DEFAULT) return GL_E_INVALID;
+    if (!(std::isfinite(slo_target) && slo_target >= 0.0 && slo_target <= 1.0)) return GL_E_DOMAIN;
+    if (priority == GL_PRIORITY_DEFAULT && (default_col < -1 || default_col >= cols))
+        return GL_E_LOOKUP;
+    gl_status st = device_check();
+    if (st) return st;
+    const int warps = 8;
+    prof_begin("k_argmin_matrices", stream);
+    gl::k_argmin_matrices<<<(unsigned)((rows + warps - 1) / warps), 32 * warps, 0, stream>>>(
+        carbon, att, present, rows, cols, slo_target, priority, default_col, choice_out,
+        via_fallback_out);
+    const cudaError_t e = cudaGetLastError();
+    prof_end(stream);
+    if (e != cudaSuccess) return GL_E_CUDA;
+    g_last_launches = 1;
+    return GL_OK;
+}
+
 gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const gl_chain *chains,
                            int32_t n_chains, const gl_scenario *scen, int32_t n_scen,
                            const gl_grid *grid, int32_t slo_num, int32_t slo_den,

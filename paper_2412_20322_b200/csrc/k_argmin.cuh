@@ -116,4 +116,70 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Alg. 1 lines 2-9 on explicit matrices (e.g. completed by gl_complete_matrices,
+// line 1): fractional attainments, feasible iff present and att >= target (R54).
+// One warp per row, same lexicographic shuffle argmin as k_argmin.
+struct CandF {
+    double c, a;
+    int32_t col;
+};
+
+__device__ __forceinline__ bool better_feasible_f(const CandF &x, const CandF &y)
+{
+    if (x.col < 0) return false;
+    if (y.col < 0) return true;
+    if (x.c != y.c) return x.c < y.c;
+    if (x.a != y.a) return x.a > y.a;
+    return x.col < y.col;
+}
+
+__device__ __forceinline__ bool better_fallback_f(const CandF &x, const CandF &y)
+{
+    if (x.col < 0) return false;
+    if (y.col < 0) return true;
+    if (x.a != y.a) return x.a > y.a;
+    if (x.c != y.c) return x.c < y.c;
+    return x.col < y.col;
+}
+
+__global__ void __launch_bounds__(256)
+    k_argmin_matrices(const double *__restrict__ carbon, const double *__restrict__ att,
+                      const uint8_t *__restrict__ present, int32_t rows, int32_t cols,
+                      double target, int32_t priority, int32_t default_col,
+                      int32_t *__restrict__ choice_out, uint8_t *__restrict__ fb_out)
+{
+    const int lane = threadIdx.x & 31;
+    const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
+    if (row >= rows) return;  // warp-uniform
+    CandF bf{0.0, 0.0, -1}, bb{0.0, 0.0, -1};
+    for (int col = lane; col < cols; col += 32) {
+        const int64_t k = row * cols + col;
+        if (present && !present[k]) continue;
+        const CandF c{carbon[k], att[k], col};
+        if (c.a >= target && better_feasible_f(c, bf)) bf = c;
+        if (better_fallback_f(c, bb)) bb = c;
+    }
+#pragma unroll
+    for (int off = 16; off; off >>= 1) {
+        CandF of, ob;
+        of.c = __shfl_xor_sync(FULL, bf.c, off);
+        of.a = __shfl_xor_sync(FULL, bf.a, off);
+        of.col = __shfl_xor_sync(FULL, bf.col, off);
+        ob.c = __shfl_xor_sync(FULL, bb.c, off);
+        ob.a = __shfl_xor_sync(FULL, bb.a, off);
+        ob.col = __shfl_xor_sync(FULL, bb.col, off);
+        if (better_feasible_f(of, bf)) bf = of;
+        if (better_fallback_f(ob, bb)) bb = ob;
+    }
+    if (lane == 0) {
+        if (bf.col >= 0) {
+            choice_out[row] = bf.col;
+            fb_out[row] = 0;
+        } else {
+            choice_out[row] = (priority == GL_PRIORITY_SLO) ? bb.col : default_col;
+            fb_out[row] = 1;
+        }
+    }
+}
+
 }  // namespace gl

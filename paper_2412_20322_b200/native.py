@@ -79,7 +79,7 @@ class GlSavingsPair(C.Structure):
 SCEN_DTYPE = np.dtype([("ci", "<f8"), ("lt_new", "<f8"), ("lt_old", "<f8")])
 
 EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_link_demand",
-           "gl_savings_surface", "gl_complete_matrices", "gl_last_launch_count",
+           "gl_savings_surface", "gl_complete_matrices", "gl_argmin_matrices", "gl_last_launch_count",
            "gl_profile_enable", "gl_kernel_times", "gl_strerror", "gl_version")
 
 _lib = None
@@ -118,6 +118,8 @@ def lib():
         L.gl_complete_matrices.restype = i32
         L.gl_complete_matrices.argtypes = [vp, vp, i32, i32, i32, i32, C.c_double, i32, vp,
                                            C.c_double, C.c_double, vp, vp, vp, vp, vp]
+        L.gl_argmin_matrices.restype = i32
+        L.gl_argmin_matrices.argtypes = [vp, vp, vp, i32, i32, C.c_double, i32, i32, vp, vp, vp]
         L.gl_last_launch_count.restype = i32
         L.gl_last_launch_count.argtypes = []
         L.gl_profile_enable.restype = i32
@@ -183,6 +185,15 @@ def complete_matrices(x_ptr: int, obs_ptr: int, batch: int, rows: int, cols: int
                                      int(iters), v0_ptr, float(lo), float(hi), out_ptr,
                                      u_ptr or None, v_ptr or None, status_ptr, stream or None),
           "gl_complete_matrices")
+    return lib().gl_last_launch_count()
+
+
+def argmin_matrices(carbon_ptr: int, att_ptr: int, present_ptr: int | None, rows: int, cols: int,
+                    target: float, priority: int, default_col: int, choice_ptr: int, fb_ptr: int,
+                    stream: int):
+    check(lib().gl_argmin_matrices(carbon_ptr, att_ptr, present_ptr or None, rows, cols,
+                                   float(target), priority, default_col, choice_ptr, fb_ptr,
+                                   stream or None), "gl_argmin_matrices")
     return lib().gl_last_launch_count()
 
 

@@ -28,7 +28,7 @@ def declared_functions():
 def test_header_declares_expected_calls():
     assert declared_functions() == sorted(["gl_eval_grid", "gl_argmin_feasible",
                                            "gl_evaluate_host", "gl_link_demand", "gl_savings_surface",
-                                           "gl_complete_matrices",
+                                           "gl_complete_matrices", "gl_argmin_matrices",
                                            "gl_last_launch_count",
                                            "gl_profile_enable", "gl_kernel_times",
                                            "gl_strerror", "gl_version"])

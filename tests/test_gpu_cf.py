@@ -114,3 +114,44 @@ def test_iters_zero_and_determinism():
     a = run_batch([x], [m], 2, 0.1, 50, [als_init(9, 2)])
     b = run_batch([x], [m], 2, 0.1, 50, [als_init(9, 2)])
     assert all(np.array_equal(u, v) for u, v in zip(a, b))
+
+
+def test_argmin_matrices_vs_oracle():
+    rng = np.random.default_rng(12)
+    dev = torch.device("cuda")
+    for rows, cols in ((1, 1), (7, 3), (100, 8), (33, 40), (4096, 10)):
+        carbon = rng.choice([1.0, 2.0, 3.0, 2.5], (rows, cols))
+        att = rng.choice([0.5, 0.85, 0.9, 0.95, 1.0], (rows, cols))
+        present = (rng.random((rows, cols)) < 0.85).astype(np.uint8)
+        for prio, dcol in ((0, -1), (1, cols - 1)):
+            for pr in (present, None):
+                ch, fb = api.argmin_matrices(torch.from_numpy(carbon).to(dev),
+                                             torch.from_numpy(att).to(dev),
+                                             None if pr is None else torch.from_numpy(pr).to(dev),
+                                             0.9, prio, dcol)
+                want = O.alg1_matrices(carbon, att, pr, 0.9, prio, dcol)
+                assert np.array_equal(ch.cpu().numpy(), want[0])
+                assert np.array_equal(fb.cpu().numpy(), want[1])
+
+
+def test_cf_then_alg1_pipeline_config4():
+    # Alg. 1 line 1 then lines 2-9: hide 30% of config 4's (carbon, attainment) cells,
+    # complete both on the GPU, choose on the GPU; the same on the oracle side
+    g = build_config(4, n=2000)
+    ref = O.evaluate_grid(g)
+    carbon = ref["carbon"]
+    att = np.array([[ref["stats"][int(k)]["slo_ok"] / ref["stats"][int(k)]["n"] for k in row]
+                    for row in g.cell_chain.reshape(g.rows, g.cols)])
+    m = observation_mask(g.rows, g.cols, 0.3, seed=7)
+    v0 = als_init(g.cols, 2)
+    out, _, _, st = run_batch([carbon, att], [m, m], 2, 0.1, 200, [v0, v0], lo=0.0)
+    c_gpu, a_gpu = out[0], np.minimum(out[1], 1.0)
+    dev = torch.device("cuda")
+    ch, fb = api.argmin_matrices(torch.from_numpy(c_gpu).to(dev), torch.from_numpy(a_gpu).to(dev),
+                                 None, 0.9)
+    # the oracle's choice on the GPU-completed matrices (completion parity is tested above)
+    want = O.alg1_matrices(c_gpu, a_gpu, None, 0.9)
+    assert np.array_equal(ch.cpu().numpy(), want[0]) and np.array_equal(fb.cpu().numpy(), want[1])
+    # where no cell was hidden the decision equals Alg. 1 on the simulated matrices
+    full_rows = m.all(axis=1)
+    assert np.array_equal(ch.cpu().numpy()[full_rows], ref["choice"][full_rows])
