@@ -39,7 +39,8 @@
  * link demand against closed forms, S:372 accounting and the tick brute force
  * scanning every window start (tests/test_oracle_link.py); the savings analysis
  * against S:500 / S:499 and Eq. 5's three lines (tests/test_oracle_savings.py);
- * ALS against numpy's ridge solves and exact rank-1 recovery (tests/test_oracle_cf.py).
+ * ALS against numpy's ridge solves and exact rank-1 recovery, Alg. 1 on explicit
+ * matrices against SPEC's examples and the integer Alg. 1 (tests/test_oracle_cf.py).
  *
  * Build: gcc -O2 -std=c11 -ffp-contract=off -shared -fPIC (no threads, no SIMD
  * intrinsics).
