@@ -31,10 +31,12 @@ def build(name, edits):
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
            "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
            "-o", os.path.join(OUT, f"{name}.so"), os.path.join(tmp, "greenllm.cu")]
+    cmd[1:1] = os.environ.get("AB_FLAGS", "").split()  # e.g. AB_FLAGS="-Xptxas -O2"
     subprocess.check_call(cmd)
     print("built", name)
 
 
 names = sys.argv[1:] or list(VARIANTS)
 for n in names:
-    build(n, VARIANTS[n])
+    base_name = n.split("@")[0]  # "<variant>@<tag>": the same edits under AB_FLAGS
+    build(n, VARIANTS[base_name])

@@ -1,4 +1,4 @@
-"""Multi-rank host logic of the sharded evaluation on CPU (gloo, world 2 and 3).
+"""Multi-rank host logic of the sharded evaluation on CPU (gloo, world 2, 3 and 4).
 
 The shard computation is substituted by oracle statistics (no GPU here); what
 is tested is the product's sharding, the single all_gather of 80-byte records
@@ -88,7 +88,7 @@ def _worker(rank, world, port, n_chains_take, result_dir):
     dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world,n_chains", [(2, 40), (2, 5), (3, 40), (3, 7)])
+@pytest.mark.parametrize("world,n_chains", [(2, 40), (2, 5), (3, 40), (3, 7), (4, 40), (4, 3)])
 def test_sharded_gather_matches_single_process(tmp_path, world, n_chains):
     port = _free_port()
     mp.spawn(_worker, args=(world, port, n_chains, str(tmp_path)), nprocs=world, join=True)
