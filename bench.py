@@ -489,9 +489,20 @@ def link_demand_bench(dg, grid, flush, reps=3):
         kind = {0: "dpd", 1: "dsd"}.get(ch.mode)
         if kind:
             gbps.setdefault(kind, []).append(float(lk[ci]["peak_bytes"]) * 8 / 1e9)
+    # Fig. 4's view: DPD / DSD peak-demand ratio per GPU pair and rate.
+    # config 4's chain order is rate x pair x (DPD, DSD): chains 2k and 2k + 1 pair up.
+    fig4 = {}
+    for ci in range(0, len(grid.chains) - 1, 2):
+        a, b = grid.chains[ci], grid.chains[ci + 1]
+        if a.mode == 0 and b.mode == 1 and a.trace_idx == b.trace_idx:
+            pair = a.label.split(" ")[2]
+            rate = a.label.split(" ")[-1]
+            dpd, dsd = float(lk[ci]["peak_bytes"]), float(lk[ci + 1]["peak_bytes"])
+            fig4.setdefault(pair, {})[rate] = round(dpd / dsd, 1) if dsd > 0 else None
     return {"ms": sum(ms) / len(ms), "window_us": 1_000_000,
             "kernel_ms": {k: sum(v) / len(v) for k, v in kt.items()},
             "peak_gbps_range": {k: [min(v), max(v)] for k, v in gbps.items()},
+            "dpd_over_dsd_peak_ratio": fig4,
             "note": "peak link demand of every chain (R45-R47); logging decode + "
                     "k_link_scan/window/reduce; outside the timed step"}
 
