@@ -558,6 +558,20 @@ def analysis_bench(dg, grid, reps=3):
     for name, t in N.kernel_times():
         kt6.setdefault(name, []).append(t)
     N.profile_enable(False)
+    # the paper's headline view: Alg. 1's choice per workload row vs the
+    # Standalone column, over config 6's 8,192 rows (rate x CI x lifetimes)
+    c6, ch6, fb6 = api.argmin_feasible(dg6, stats6)
+    c6, ch6, fb6 = c6.cpu().numpy(), ch6.cpu().numpy(), fb6.cpu().numpy()
+    sa_col = g6.col_labels.index("Standalone A100")
+    picked = c6[np.arange(g6.rows), ch6]
+    red = 1.0 - picked / c6[:, sa_col]
+    feas = fb6 == 0
+    chosen = {g6.col_labels[c]: int(np.sum(ch6 == c)) for c in np.unique(ch6)}
+    alg1_summary = {"rows": int(g6.rows), "rows_feasible": int(feas.sum()),
+                    "carbon_reduction_vs_standalone_pct": {
+                        "median": round(100 * float(np.median(red[feas])), 1) if feas.any() else None,
+                        "max": round(100 * float(np.max(red[feas])), 1) if feas.any() else None},
+                    "chosen_columns": chosen}
     stats, _ = api.eval_grid(dg)
     carbon, _, _ = api.argmin_feasible(dg, stats)
     st = api.stats_numpy(stats)
@@ -588,7 +602,8 @@ def analysis_bench(dg, grid, reps=3):
                           "grid": [g6.rows, g6.cols],
                           "kernel_ms": {k: sum(v) / len(v) for k, v in kt6.items()},
                           "workload": "cfg6: cfg4 + Standalone and SpecDecode (A100) columns, "
-                                      "8,192 x 10 cells, 80 timing chains"},
+                                      "8,192 x 10 cells, 80 timing chains",
+                          "alg1_vs_standalone": alg1_summary},
             "savings_surface": {"ms": sav_ms, "cells": len(api_pairs(g6)) * len(g6.scenarios),
                                 "workload": "cfg6: 72 (Case 2, Standalone) pairs x 1,024 (CI, T_A, T_B)",
                                 "savings_vs_standalone": savings_summary},
