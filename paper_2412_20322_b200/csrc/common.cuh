@@ -40,7 +40,20 @@ struct DChainX {
     int32_t leader_pos;  // candidate the leader is at (helpers skip and abort below)
     int32_t next_seg;    // helper work counter
     int32_t n_ev;        // LOG launches: batch-size log entries written
-    int32_t pad[3];
+    int32_t stage_done;  // k_stages CTAs of this chain that have finished
+    int32_t pad[2];
+};
+
+// one k_stages CTA's share of a chain (k_stages splits a chain over S CTAs): its
+// aggregates are published with release flags for the CTAs after it, its partial
+// statistics are combined by the chain's last CTA (stream-ordered scratch, zeroed)
+struct DStagePart {
+    int64_t agg1_A, agg1_B;  // stage-1 max-plus map of the CTA's requests
+    int64_t agg2_A, agg2_B;  // stage-2 map
+    int64_t sums[6];         // busy_new, busy_old, e_new, e_old, tokens, max finish (o = 1)
+    int32_t dcount;          // decode requests of the CTA
+    uint32_t status;
+    int32_t flag1, flag2;    // release flags of the two aggregates
 };
 
 // one timing chain as the kernels see it (built by the host from gl_chain + gl_trace)
@@ -64,6 +77,7 @@ struct DChain {
     int32_t *seg_start; // [nseg + 1] candidate starts (q), seg_start[nseg] = M
     DSegOut *seg_out;   // [nseg]
     DChainX *x;
+    DStagePart *stp;    // [stage_split] k_stages partials of this chain
     longlong2 *ev;      // LOG launches: batch-size log [2 n + 16] of (T, b) (k_link.cuh);
                         // a run from decode request q0 writes from position 2 q0, unused
                         // positions keep the sentinel b = -1 (removed by k_link_scan)

@@ -14,8 +14,9 @@
  *
  * Kernels, in launch order:
  *   k_dsd_demand  (k_dsd_demand.cuh) one thread per (DSD demand group, request)
- *   k_stages      (k_stages.cuh)     one warp per chain: TMA-staged tables, 128-bit
- *                                    loads, max-plus warp scans -> decode stream
+ *   k_stages      (k_stages.cuh)     S 16-warp blocks per chain: TMA-staged tables,
+ *                                    128-bit loads, max-plus scans with decoupled
+ *                                    look-back between blocks -> decode stream
  *   k_segments    (k_stages.cuh)     idle-point candidates for the decode speculation
  *   k_decode      (k_decode.cuh)     leader + helper warps per chain: exact
  *                                    speculative decode event loops
@@ -294,6 +295,20 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     total += align256(sizeof(gl::DSegOut) * (size_t)seg_total);
     const size_t off_x = total;
     total += align256(sizeof(gl::DChainX) * (size_t)n_chains);
+    // k_stages: S co-resident blocks per chain (decoupled look-back between them)
+    int stage_split = 1;
+    {
+        int per_sm = 0;
+        if (cudaFuncSetAttribute(gl::k_stages, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 (int)smem_st) == cudaSuccess &&
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl::k_stages, 32 * gl::ST_WARPS,
+                                                          smem_st) == cudaSuccess)
+            stage_split = (int)std::max<int64_t>(
+                1, std::min<int64_t>(gl::ST_MAX_SPLIT, (int64_t)per_sm * n_sm / std::max(1, (int)n_chains)));
+        cudaGetLastError();
+    }
+    const size_t off_stp = total;
+    total += align256(sizeof(gl::DStagePart) * (size_t)n_chains * stage_split);
     const size_t zero_bytes = total - off_zero;
     unsigned char *scratch = nullptr;
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
@@ -333,6 +348,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         d.seg_start = reinterpret_cast<int32_t *>(scratch + off_segs) + seg_off[i];
         d.seg_out = reinterpret_cast<gl::DSegOut *>(scratch + off_segout) + seg_off[i];
         d.x = reinterpret_cast<gl::DChainX *>(scratch + off_x) + i;
+        d.stp = reinterpret_cast<gl::DStagePart *>(scratch + off_stp) + (size_t)stage_split * i;
         d.ev = lk ? reinterpret_cast<longlong2 *>(scratch + off_ev) + ev_off[i] : nullptr;
         d.ev_spec = lk ? reinterpret_cast<longlong2 *>(scratch + off_evs) + evs_off[i] : nullptr;
         d.ev_stride = 2 * tr.n + 16;
@@ -385,7 +401,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                                  (int)smem_st);
         if (e == cudaSuccess) {
             prof_begin("k_stages", stream);
-            gl::k_stages<<<n_chains, 32 * gl::ST_WARPS, smem_st, stream>>>(dc, stats_out, rows);
+            gl::k_stages<<<n_chains * stage_split, 32 * gl::ST_WARPS, smem_st, stream>>>(
+                dc, stats_out, rows, stage_split);
             e = cudaGetLastError();
             prof_end(stream);
             ++launches;

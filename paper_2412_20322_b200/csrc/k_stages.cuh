@@ -8,8 +8,10 @@
 //
 // Both stages are max-plus recurrences: element i is the map x -> max(x + A_i, B_i)
 // (A = s_i, B = a_i + s_i, resp. c_i + s_i) and a prefix is the composition
-// (A, B) o (A', B') = (A + A', max(B + A', B')).  One block of ST_WARPS warps per
-// chain; warp w owns a contiguous run of 128-request chunks:
+// (A, B) o (A', B') = (A + A', max(B + A', B')).  S blocks of ST_WARPS warps per
+// chain (S from the host: as many as fit co-resident, S = 1 for many chains); warp w
+// of block s owns the contiguous run s * ST_WARPS + w of 128-request chunks, and a
+// block waits (acquire) for the aggregates its predecessors publish (release):
 //   pass 1  aggregate of stage 1 over the run, decode count, stage sums, status
 //   pass 2  carry-in = composition of the previous runs' aggregates -> c_i, and
 //           the stage-2 aggregate of the run
@@ -26,6 +28,7 @@
 namespace gl {
 
 constexpr int ST_WARPS = 16;
+constexpr int ST_MAX_SPLIT = 4;  // blocks per chain
 
 struct MP {  // max-plus map x -> max(x + A, B)
     int64_t A, B;
@@ -157,17 +160,40 @@ __device__ __forceinline__ MP chunk_aggregate(const int64_t (&s)[4], const int64
     return MP{shfl_i64(inc.A, 31), shfl_i64(inc.B, 31)};
 }
 
+// the composition of the predecessors' aggregates, as the B-value applied to -inf,
+// and the sum of their decode counts (thread 0 of a block; spins on release flags)
+__device__ __forceinline__ void stage_lookback(const DChain &ch, int s, bool second,
+                                              int64_t &carry, int32_t &dbase)
+{
+    carry = NEG_INF;
+    dbase = 0;
+    for (int p = 0; p < s; ++p) {
+        DStagePart &q = ch.stp[p];
+        int32_t *flag = second ? &q.flag2 : &q.flag1;
+        while (ld_acquire_gpu(flag) == 0) {
+        }
+        const int64_t A = __ldcg(second ? &q.agg2_A : &q.agg1_A);
+        const int64_t B = __ldcg(second ? &q.agg2_B : &q.agg1_B);
+        carry = max(carry + A, B);
+        dbase += __ldcg(&q.dcount);
+    }
+}
+
 __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     k_stages(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
-             int64_t *__restrict__ perreq)
+             int64_t *__restrict__ perreq, int32_t S)
 {
+    __shared__ int64_t s_carry;
+    __shared__ int32_t s_dbase;
+    __shared__ int32_t s_last;
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int64_t agg_A[ST_WARPS], agg_B[ST_WARPS];
     __shared__ int32_t dcount[ST_WARPS];
     __shared__ int64_t red[6][ST_WARPS];
     __shared__ uint32_t red_status[ST_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const DChain ch = chains[blockIdx.x];
+    const int32_t chain = (int32_t)(blockIdx.x / S), sblk = (int32_t)(blockIdx.x % S);
+    const DChain ch = chains[chain];
     const int P = ch.max_prompt, cap = ch.cap;
     const int p1pad = round_up4(P + 1);
     int32_t *t1s = reinterpret_cast<int32_t *>(smem);
@@ -199,8 +225,9 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     const bool colo = ch.mode == GL_MODE_STANDALONE || ch.mode == GL_MODE_SPEC_COLO;
     const bool dsd = ch.mode == GL_MODE_DSD || ch.mode == GL_MODE_SPEC_COLO;  // demand K_j
     const int32_t nchunks = (n + CHUNK - 1) / CHUNK;
-    const int32_t per = (nchunks + ST_WARPS - 1) / ST_WARPS;
-    const int32_t c_lo = min(warp * per, nchunks), c_hi = min(c_lo + per, nchunks);
+    const int32_t runs = ST_WARPS * S, run = sblk * ST_WARPS + warp;
+    const int32_t per = (nchunks + runs - 1) / runs;
+    const int32_t c_lo = min(run * per, nchunks), c_hi = min(c_lo + per, nchunks);
 
     // ---- pass 1: stage-1 aggregate, decode count, stage sums, status -----------
     int64_t acc_busy_new = 0, acc_busy_old = 0, acc_e_new = 0, acc_e_old = 0, acc_tokens = 0;
@@ -272,14 +299,34 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
         dcount[warp] = ndec;
     }
     __syncthreads();
-    int64_t carry_c = NEG_INF;  // = B of the composition of the previous runs
-    int32_t dbase = 0;
+    if (threadIdx.x == 0) {  // publish this block's aggregate, then look back
+        DStagePart &me = ch.stp[sblk];
+        MP a{0, NEG_INF};
+        int32_t dc = 0;
+        for (int w = 0; w < ST_WARPS; ++w) {
+            a = mp_then(a, MP{agg_A[w], agg_B[w]});
+            dc += dcount[w];
+        }
+        me.agg1_A = a.A;
+        me.agg1_B = a.B;
+        me.dcount = dc;
+        __threadfence();
+        st_release_gpu(&me.flag1, 1);
+        int64_t cin;
+        int32_t db;
+        stage_lookback(ch, sblk, false, cin, db);
+        s_carry = cin;
+        s_dbase = db;
+    }
+    __syncthreads();
+    int64_t carry_c = s_carry;  // = B of the composition of the previous runs
+    int32_t dbase = s_dbase;
     for (int w = 0; w < warp; ++w) {
         carry_c = max(carry_c + agg_A[w], agg_B[w]);
         dbase += dcount[w];
     }
     int32_t M = 0;
-    for (int w = 0; w < ST_WARPS; ++w) M += dcount[w];
+    for (int w = 0; w < ST_WARPS; ++w) M += dcount[w];  // this block's share
     __syncthreads();
 
     // ---- pass 2: c with the true carry, stage-2 aggregate ---------------------
@@ -300,7 +347,21 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
         agg_B[warp] = agg2.B;
     }
     __syncthreads();
-    int64_t carry_r = NEG_INF;
+    if (threadIdx.x == 0) {
+        DStagePart &me = ch.stp[sblk];
+        MP a{0, NEG_INF};
+        for (int w = 0; w < ST_WARPS; ++w) a = mp_then(a, MP{agg_A[w], agg_B[w]});
+        me.agg2_A = a.A;
+        me.agg2_B = a.B;
+        __threadfence();
+        st_release_gpu(&me.flag2, 1);
+        int64_t cin;
+        int32_t db;
+        stage_lookback(ch, sblk, true, cin, db);
+        s_carry = cin;
+    }
+    __syncthreads();
+    int64_t carry_r = s_carry;
     for (int w = 0; w < warp; ++w) carry_r = max(carry_r + agg_A[w], agg_B[w]);
 
     // ---- pass 3: c, r -> rows and the compacted decode stream -----------------
@@ -354,6 +415,25 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
         red_status[warp] = status;
     }
     __syncthreads();
+    if (threadIdx.x == 0) {  // this block's partials; the chain's last block combines
+        DStagePart &me = ch.stp[sblk];
+        int64_t s[6] = {0, 0, 0, 0, 0, 0};
+        uint32_t st = 0;
+        for (int w = 0; w < ST_WARPS; ++w) {
+            for (int i = 0; i < 5; ++i) s[i] += red[i][w];
+            s[5] = max(s[5], red[5][w]);
+            st |= red_status[w];
+        }
+        for (int i = 0; i < 6; ++i) me.sums[i] = s[i];
+        me.status = st;
+        __threadfence();
+        s_last = atomicAdd(&ch.x->stage_done, 1) == S - 1;
+    }
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    M = 0;
+    for (int p = 0; p < S; ++p) M += __ldcg(&ch.stp[p].dcount);
     if (threadIdx.x < 2) {  // two sentinels after the last decode request
         ch.dec_r[(int64_t)M + threadIdx.x] = INT64_MAX;
         ch.dec_dj[(int64_t)M + threadIdx.x] = make_uint2(0u, 0u);
@@ -361,10 +441,11 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     if (threadIdx.x == 0) {
         int64_t s[6] = {0, 0, 0, 0, 0, 0};
         uint32_t st = 0;
-        for (int w = 0; w < ST_WARPS; ++w) {
-            for (int i = 0; i < 5; ++i) s[i] += red[i][w];
-            s[5] = max(s[5], red[5][w]);
-            st |= red_status[w];
+        for (int p = 0; p < S; ++p) {
+            const DStagePart &q = ch.stp[p];
+            for (int i = 0; i < 5; ++i) s[i] += __ldcg(&q.sums[i]);
+            s[5] = max(s[5], __ldcg(&q.sums[5]));
+            st |= __ldcg(&q.status);
         }
         gl_chain_stats o;
         o.n = ch.n;
@@ -378,7 +459,7 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
         o.req_hash = 0;
         o.status = st;
         o.capacity_ok = (uint32_t)ch.capacity_ok;
-        stats[blockIdx.x] = o;
+        stats[chain] = o;
         ch.x->M = skip ? 0 : M;
     }
 }
