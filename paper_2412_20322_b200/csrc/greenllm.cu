@@ -309,6 +309,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     }
     const size_t off_stp = total;
     total += align256(sizeof(gl::DStagePart) * (size_t)n_chains * stage_split);
+    const size_t off_ticket = total;
+    total += 256;
     const size_t zero_bytes = total - off_zero;
     unsigned char *scratch = nullptr;
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
@@ -402,7 +404,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         if (e == cudaSuccess) {
             prof_begin("k_stages", stream);
             gl::k_stages<<<n_chains * stage_split, 32 * gl::ST_WARPS, smem_st, stream>>>(
-                dc, stats_out, rows, stage_split);
+                dc, stats_out, rows, stage_split, reinterpret_cast<int32_t *>(scratch + off_ticket));
             e = cudaGetLastError();
             prof_end(stream);
             ++launches;

@@ -181,8 +181,9 @@ __device__ __forceinline__ void stage_lookback(const DChain &ch, int s, bool sec
 
 __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     k_stages(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
-             int64_t *__restrict__ perreq, int32_t S)
+             int64_t *__restrict__ perreq, int32_t S, int32_t *__restrict__ ticket)
 {
+    __shared__ int32_t s_vid;
     __shared__ int64_t s_carry;
     __shared__ int32_t s_dbase;
     __shared__ int32_t s_last;
@@ -192,7 +193,11 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     __shared__ int64_t red[6][ST_WARPS];
     __shared__ uint32_t red_status[ST_WARPS];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int32_t chain = (int32_t)(blockIdx.x / S), sblk = (int32_t)(blockIdx.x % S);
+    // virtual block ids in the order blocks start: a block only ever waits on blocks
+    // with smaller ids, which are already running (no assumption on dispatch order)
+    if (threadIdx.x == 0) s_vid = S > 1 ? atomicAdd(ticket, 1) : (int32_t)blockIdx.x;
+    __syncthreads();
+    const int32_t chain = s_vid / S, sblk = s_vid % S;
     const DChain ch = chains[chain];
     const int P = ch.max_prompt, cap = ch.cap;
     const int p1pad = round_up4(P + 1);

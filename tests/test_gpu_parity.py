@@ -186,6 +186,22 @@ def test_decode_speculation_stress(n_chains, n):
     assert_parity(grid_of(pairs))
 
 
+@pytest.mark.parametrize("n_chains", [1, 37, 49, 74, 149])
+def test_stage_split_block_boundaries(n_chains):
+    # k_stages splits a chain over S = min(4, 148 // chains) blocks (4, 4, 3, 2, 2, 1):
+    # lengths around the 128-request chunk and 2048-request block-run boundaries, so
+    # the decoupled look-back carries stage maps and decode counts across ragged runs
+    rng = np.random.default_rng(9000 + n_chains)
+    lens = [1, 127, 128, 129, 2047, 2048, 2049, 4097, 6143, 8191, 8193]
+    pairs = []
+    for i in range(n_chains):
+        n = lens[i % len(lens)] if n_chains > 1 else 12289
+        tr, ch = random_case(rng, n=n, mode=ALL_MODES[i % 4], cap=int(rng.choice([1, 3, 8, 40])))
+        tr = dataclasses.replace(tr, arrival_us=np.sort(rng.integers(0, 40 * n + 1, n)))
+        pairs.append((tr, ch))
+    assert_parity(grid_of(pairs))
+
+
 def test_iteration_rebase_and_far_gaps():
     """> 2^31 decode iterations (the 32-bit iteration counter rebases) and joins
     more than 2^31 us after the current boundary (the exact 64-bit path), in
