@@ -295,16 +295,27 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     total += align256(sizeof(gl::DSegOut) * (size_t)seg_total);
     const size_t off_x = total;
     total += align256(sizeof(gl::DChainX) * (size_t)n_chains);
-    // k_stages: S co-resident blocks per chain (decoupled look-back between them)
+    // k_stages: S blocks per chain (decoupled look-back between them), S <= 4 chosen
+    // to minimise the waves per chain's work, ceil(chains S / resident) / S (ties to
+    // the smaller S): 2 on config 4's 64 chains, 3 on config 6's 80, 4 on config 5's 320
     int stage_split = 1;
     {
         int per_sm = 0;
         if (cudaFuncSetAttribute(gl::k_stages, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_st) == cudaSuccess &&
             cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl::k_stages, 32 * gl::ST_WARPS,
-                                                          smem_st) == cudaSuccess)
-            stage_split = (int)std::max<int64_t>(
-                1, std::min<int64_t>(gl::ST_MAX_SPLIT, (int64_t)per_sm * n_sm / std::max(1, (int)n_chains)));
+                                                          smem_st) == cudaSuccess &&
+            per_sm > 0) {
+            const int64_t slots = (int64_t)per_sm * n_sm;
+            int64_t best_w = (n_chains + slots - 1) / slots;
+            for (int S = 2; S <= gl::ST_MAX_SPLIT; ++S) {
+                const int64_t w = ((int64_t)n_chains * S + slots - 1) / slots;
+                if (w * stage_split < best_w * S) {
+                    best_w = w;
+                    stage_split = S;
+                }
+            }
+        }
         cudaGetLastError();
     }
     const size_t off_stp = total;

@@ -188,7 +188,8 @@ def test_decode_speculation_stress(n_chains, n):
 
 @pytest.mark.parametrize("n_chains", [1, 37, 49, 74, 149])
 def test_stage_split_block_boundaries(n_chains):
-    # k_stages splits a chain over S = min(4, 148 // chains) blocks (4, 4, 3, 2, 2, 1):
+    # k_stages splits a chain over S blocks (S = 4, 4, 3, 2, 4 here; 149 chains
+    # x 4 = 596 blocks is more than one wave, so later blocks start as earlier finish):
     # lengths around the 128-request chunk and 2048-request block-run boundaries, so
     # the decoupled look-back carries stage maps and decode counts across ragged runs
     rng = np.random.default_rng(9000 + n_chains)
