@@ -399,9 +399,13 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         e = cudaMemsetAsync(scratch + off_ev, 0xFF, sizeof(longlong2) * (size_t)ev_total, stream);
     int launches = 0;
     if (e == cudaSuccess && !groups.empty()) {
+        // persistent quads: about 16 resident blocks of 256 threads per SM in total,
+        // spread over the groups, never more than one quad per request
         int64_t gmax = 0;
         for (auto &g : groups) gmax = std::max(gmax, g.n);
-        dim3 grid((unsigned)((gmax * gl::DSD_QL + 255) / 256), (unsigned)groups.size());
+        const int64_t want = std::max<int64_t>(1, (16 * (int64_t)n_sm) / (int64_t)groups.size());
+        const int64_t need_b = (gmax * gl::DSD_QL + 255) / 256;
+        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, need_b)), (unsigned)groups.size());
         prof_begin("k_dsd_demand", stream);
         gl::k_dsd_demand<<<grid, 256, 0, stream>>>(
             reinterpret_cast<const DGroup *>(scratch + off_groups));

@@ -11,8 +11,9 @@
 //
 // Work split: QL = 4 lanes per request.  In round t lane l evaluates Philox call
 // 4t + l (steps 16t + 4l .. +3); the four calls' token counts are prefix-summed with
-// two shuffles and the crossing step is found without a serial walk, so a warp
-// waits on the longest of 8 requests (not 32) and each request finishes 4x sooner.
+// two shuffles and the crossing step is found without a serial walk.  The quads are
+// persistent (a grid of a few waves per group): a finished quad starts its next
+// request in the same loop trip, so lanes idle only at the end of the group.
 // The gamma thresholds sit in registers (the kernel is instantiated per gamma;
 // the block's group picks the instance), compared as 64-bit (thr = 2^32 at alpha = 1).
 #pragma once
@@ -39,17 +40,24 @@ __device__ __forceinline__ void dsd_demand_body(const DGroup *g)
 #pragma unroll
     for (int c = 0; c < G; ++c) thr[c] = g->thr[c];
     const int lane = threadIdx.x & 31, sub = lane & (DSD_QL - 1);
-    const unsigned gmask = 0xFu << (lane & ~(DSD_QL - 1));  // this request's 4 lanes
-    const int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / DSD_QL;
-    const bool valid = j < g->n;
-    uint32_t o = valid ? __ldg(g->o + j) : 1u;
-    if (o >= O_LIMIT) o = O_LIMIT - 1;
-    const int64_t need = (int64_t)o - 1;
+    const int qbase = lane & ~(DSD_QL - 1);
+    // persistent quads: quad q of the group's blocks takes requests q, q + Q, ...; a
+    // quad whose request is done takes its next one at the top of the same loop, so
+    // the warp's lanes stay busy until the group's requests run out (not until the
+    // longest of the warp's 8 current requests finishes)
+    const int64_t Q = (int64_t)gridDim.x * (blockDim.x / DSD_QL);
+    int64_t j = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) / DSD_QL;
+    const int64_t n = g->n;
     const uint32_t k0 = (uint32_t)g->seed, k1 = (uint32_t)(g->seed >> 32);
+    auto need_of = [&](int64_t jj) -> int64_t {
+        uint32_t o = jj < n ? __ldg(g->o + jj) : 1u;
+        if (o >= O_LIMIT) o = O_LIMIT - 1;
+        return (int64_t)o - 1;
+    };
+    int64_t need = need_of(j);
     int64_t tok = 0;  // tokens accepted before this round
-    uint32_t K = 0;
-    bool done = need <= 0;
-    for (uint32_t t = 0; !__all_sync(gmask, done); ++t) {
+    uint32_t t = 0;
+    while (__any_sync(FULL, j < n)) {
         // this lane's call: steps s0 .. s0+3 of request j
         const uint32_t call = DSD_QL * t + sub;
         const uint4 w = philox4x32_10(make_uint4(call, (uint32_t)j, ACCEPT_STREAM, 0u), k0, k1);
@@ -58,34 +66,37 @@ __device__ __forceinline__ void dsd_demand_body(const DGroup *g)
         const uint32_t mine = a0 + a1 + a2 + a3;
         // inclusive prefix over the 4 lanes of this request
         uint32_t inc = mine;
-        uint32_t y = __shfl_up_sync(gmask, inc, 1, DSD_QL);
+        uint32_t y = __shfl_up_sync(FULL, inc, 1, DSD_QL);
         if (sub >= 1) inc += y;
-        y = __shfl_up_sync(gmask, inc, 2, DSD_QL);
+        y = __shfl_up_sync(FULL, inc, 2, DSD_QL);
         if (sub >= 2) inc += y;
-        const uint32_t round_tot = __shfl_sync(gmask, inc, DSD_QL - 1, DSD_QL);
-        if (!done) {
-            const int64_t before = tok + (inc - mine);  // tokens before this lane's call
-            // the crossing lies in this lane's call iff before < need <= before + mine
-            int64_t cum = before;
-            uint32_t ks = 0;
-            if (before < need && need <= before + mine) {
-                cum += a0;
-                ks = 1;
-                if (cum < need) { cum += a1; ks = 2; }
-                if (cum < need) { cum += a2; ks = 3; }
-                if (cum < need) { ks = 4; }
-            }
-            const unsigned hit = __ballot_sync(gmask, ks != 0) & gmask;
-            if (hit) {
-                const int src = __ffs(hit) - 1;
-                const uint32_t kk = __shfl_sync(gmask, ks, src & (32 - 1));
-                K = 4 * (DSD_QL * t + (uint32_t)(src & (DSD_QL - 1))) + kk;
-                done = true;
-            }
+        const uint32_t round_tot = __shfl_sync(FULL, inc, DSD_QL - 1, DSD_QL);
+        const int64_t before = tok + (inc - mine);  // tokens before this lane's call
+        // the crossing lies in this lane's call iff before < need <= before + mine
+        int64_t cum = before;
+        uint32_t ks = 0;
+        if (before < need && need <= before + mine) {
+            cum += a0;
+            ks = 1;
+            if (cum < need) { cum += a1; ks = 2; }
+            if (cum < need) { cum += a2; ks = 3; }
+            if (cum < need) { ks = 4; }
+        }
+        const unsigned hit = (__ballot_sync(FULL, ks != 0) >> qbase) & 0xFu;
+        const int src = __ffs(hit | 0x10u) - 1;  // 4: no crossing this round
+        const uint32_t kk = __shfl_sync(FULL, ks, (qbase + (src & 3)) & 31);
+        if (hit != 0u || need <= 0) {  // request j done: K_j, then its next request
+            const uint32_t K = need <= 0 ? 0u : 4 * (DSD_QL * t + (uint32_t)src) + kk;
+            if (j < n && sub == 0) g->K[j] = K;
+            j += Q;
+            need = need_of(j);
+            tok = 0;
+            t = 0;
+        } else {
             tok += round_tot;
+            ++t;
         }
     }
-    if (valid && sub == 0) g->K[j] = K;
 }
 
 __global__ void __launch_bounds__(256) k_dsd_demand(const DGroup *__restrict__ groups)
