@@ -536,3 +536,20 @@ VARIANTS["t32"] = [
               }
                 if (!slow) continue;'''),
 ]
+
+# branch layout hints on the light loop's exits (the common one-leave / one-join
+# path falls through to the back edge)
+_EXP_NL = ("k_decode.cuh", '''                        if (nl != 1) {  // several members left at once: leave the loop''',
+           '''                        if (__builtin_expect(nl != 1, 0)) {  // several members left at once''')
+_EXP_LV = ("k_decode.cuh", '''                        if (b == 0 || h_r <= T) break;
+                    }''', '''                        if (__builtin_expect(b == 0 || h_r <= T, 0)) break;
+                    }''')
+_EXP_JN = ("k_decode.cuh", '''                        if (((nxt + 2) & 127) <= 1) break;  // ring refill due: joins at the top''',
+           '''                        if (__builtin_expect(((nxt + 2) & 127) <= 1, 0)) break;  // refill due''')
+_EXP_JN2 = ("k_decode.cuh", '''                        if (b == cap || h_r <= T) break;
+                    } else {''', '''                        if (__builtin_expect(b == cap || h_r <= T, 0)) break;
+                    } else {''')
+VARIANTS["expnl"] = [_EXP_NL]
+VARIANTS["explv"] = [_EXP_NL, _EXP_LV]
+VARIANTS["expjn"] = [_EXP_JN, _EXP_JN2]
+VARIANTS["expall"] = [_EXP_NL, _EXP_LV, _EXP_JN, _EXP_JN2]
