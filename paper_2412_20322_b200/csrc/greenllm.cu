@@ -453,14 +453,16 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         cudaStream_t side = nullptr;
         cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
         if (has_disg && has_colo && !lk) {
-            if (cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess &&
+            const bool forked =
+                cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess &&
                 cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
                 cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) == cudaSuccess &&
                 cudaEventRecord(ev_fork, stream) == cudaSuccess &&
-                cudaStreamWaitEvent(side, ev_fork, 0) == cudaSuccess) {
-            } else {
-                e = cudaGetLastError();
-                if (e == cudaSuccess) e = cudaErrorUnknown;
+                cudaStreamWaitEvent(side, ev_fork, 0) == cudaSuccess;
+            if (!forked) {  // no fork: both launches stay on `stream` (serialised)
+                cudaGetLastError();
+                if (side) cudaStreamDestroy(side);
+                side = nullptr;
             }
         }
         // disaggregated chains, then co-located ones (each launch skips the others)
