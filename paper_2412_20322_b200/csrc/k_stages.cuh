@@ -29,6 +29,7 @@ namespace gl {
 
 constexpr int ST_WARPS = 16;
 constexpr int ST_MAX_SPLIT = 4;  // blocks per chain
+constexpr int DEC_TAIL = 416;    // decode-stream entries written past M (< the 512 allocated)
 
 struct MP {  // max-plus map x -> max(x + A, B)
     int64_t A, B;
@@ -439,9 +440,13 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     __threadfence();
     M = 0;
     for (int p = 0; p < S; ++p) M += __ldcg(&ch.stp[p].dcount);
-    if (threadIdx.x < 2) {  // two sentinels after the last decode request
-        ch.dec_r[(int64_t)M + threadIdx.x] = INT64_MAX;
-        ch.dec_dj[(int64_t)M + threadIdx.x] = make_uint2(0u, 0u);
+    // two sentinels after the last decode request, and the rest of the tail the
+    // decode ring prefetches (up to 2 x 128 + 2 entries past M; the host allocates
+    // n + 512) set to "no request", so no copy reads uninitialised memory
+    for (int t = threadIdx.x; t < DEC_TAIL; t += blockDim.x) {
+        ch.dec_r[(int64_t)M + t] = INT64_MAX;
+        ch.dec_dj[(int64_t)M + t] = make_uint2(0u, 0u);
+        ch.dec_pf[(int64_t)M + t] = 0;
     }
     if (threadIdx.x == 0) {
         int64_t s[6] = {0, 0, 0, 0, 0, 0};

@@ -1,0 +1,53 @@
+"""Every C-ABI entry point once at small sizes, for compute-sanitizer
+(memcheck / racecheck / synccheck / initcheck).  Product path only: no oracle.
+
+usage: compute-sanitizer --tool memcheck python scripts/sanitize_run.py
+Exercises: gl_eval_grid (DPD, DSD, Standalone, co-located SpecDecode chains; caps
+<= 31 and > 31; k_stages split widths 1-4; side-stream fork), gl_argmin_feasible,
+gl_link_demand, gl_savings_surface, gl_complete_matrices (cooperative and
+one-CTA paths), gl_argmin_matrices, gl_evaluate_host.
+"""
+import sys
+
+import numpy as np
+import torch
+
+sys.path.insert(0, ".")
+from paper_2412_20322_b200 import api  # noqa: E402
+from paper_2412_20322_b200.inputs import build_config, subset_chains  # noqa: E402
+from paper_2412_20322_b200.inputs.cf import low_rank_matrix, observation_mask  # noqa: E402
+
+
+def main():
+    torch.cuda.set_device(0)
+    grids = [build_config(1), build_config(2, n=800), build_config(6, n=1500),
+             subset_chains(build_config(3, n=1200), list(range(0, 128, 16))),
+             build_config(1, cap=40), build_config(1, cap=200)]
+    for g in grids:
+        dg = api.DeviceGrid(g)
+        stats, rows = api.eval_grid(dg, per_request=True)
+        api.argmin_feasible(dg, stats)
+        _, link = api.link_demand(dg, 50_000)
+        torch.cuda.synchronize()
+        api.check_status(api.stats_numpy(stats))
+        print(g.name, "chains", len(g.chains), "ok", flush=True)
+    g6 = build_config(6, n=1500)
+    dg6 = api.DeviceGrid(g6)
+    st6, _ = api.eval_grid(dg6)
+    sav = api.savings_surface(dg6, st6)
+    host = api.evaluate_host(dg6, dg6.pinned_traces(), want_carbon=True)
+    torch.cuda.synchronize()
+    print("savings", tuple(sav.shape), "evaluate_host choice[0]", int(host.choice[0]), flush=True)
+    for (B, R, C, k) in ((2, 300, 8, 2), (1, 33, 64, 3), (5, 40, 6, 1)):
+        x = np.stack([low_rank_matrix(R, C, k, seed=7 + b) for b in range(B)])
+        m = np.stack([observation_mask(R, C, 0.3, seed=11 + b) for b in range(B)])
+        out, U, V, status = api.complete_matrices(torch.from_numpy(x).cuda(),
+                                                  torch.from_numpy(m).cuda(), rank=k, iters=20)
+        choice, fb = api.argmin_matrices(out[0], out[0].clamp(0, 1))
+        torch.cuda.synchronize()
+        print("als", (B, R, C, k), "status", status.cpu().tolist()[:3], flush=True)
+    print("sanitize_run done")
+
+
+if __name__ == "__main__":
+    main()
