@@ -489,7 +489,7 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
 //   scan    exclusive prefix max over windows (carry across rounds)
 //   pass 2  warp per window: in-window prefix max (8 warp scans), best slack
 //   compact candidate flags -> seg_start[]
-constexpr int SEG_ROUND = 1024;
+constexpr int SEG_ROUND = 128;  // windows per round: a round (512 KB per chain) stays in L2 for pass 2
 
 __global__ void __launch_bounds__(1024)
     k_segments(const DChain *__restrict__ chains)
@@ -519,9 +519,13 @@ __global__ void __launch_bounds__(1024)
         for (int32_t w = warp; w < nwr; w += nw) {  // pass 1
             const int32_t lo = (w0 + w) * SEG_LEN, hi = min(lo + SEG_LEN, M);
             int64_t m = NEG_INF;
-            for (int32_t q = lo + lane; q < hi; q += 32)
-                m = max(m, __ldg(ch.dec_r + q) + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
-                               (colo ? __ldg(ch.dec_pf + q) : 0));
+#pragma unroll
+            for (int u = 0; u < SEG_LEN / 32; ++u) {  // all loads of the window in flight
+                const int32_t q = lo + 32 * u + lane;
+                if (q < hi)
+                    m = max(m, __ldg(ch.dec_r + q) + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
+                                   (colo ? __ldg(ch.dec_pf + q) : 0));
+            }
             m = warp_max_i64(m);
             if (lane == 0) wpre[w] = m;
         }
@@ -550,18 +554,26 @@ __global__ void __launch_bounds__(1024)
             int64_t pre = wpre[w];
             int64_t best = -1;
             int32_t best_q = INT32_MAX;
-            for (int32_t q0 = lo; q0 < hi; q0 += 32) {
-                const int32_t q = q0 + lane;
+            int64_t rqs[SEG_LEN / 32], lbs[SEG_LEN / 32];
+#pragma unroll
+            for (int u = 0; u < SEG_LEN / 32; ++u) {  // all loads of the window in flight
+                const int32_t q = lo + 32 * u + lane;
                 const bool v = q < hi;
-                const int64_t rq = v ? __ldg(ch.dec_r + q) : 0;
-                int64_t lb = v ? rq + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
-                                     (colo ? __ldg(ch.dec_pf + q) : 0)
-                               : NEG_INF;
-                int64_t inc = lb;
+                rqs[u] = v ? __ldg(ch.dec_r + q) : 0;
+                lbs[u] = v ? rqs[u] + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
+                                 (colo ? __ldg(ch.dec_pf + q) : 0)
+                           : NEG_INF;
+            }
+#pragma unroll
+            for (int u = 0; u < SEG_LEN / 32; ++u) {
+                const int32_t q = lo + 32 * u + lane;
+                const bool v = q < hi;
+                const int64_t rq = rqs[u];
+                int64_t inc = lbs[u];
 #pragma unroll
                 for (int off = 1; off < 32; off <<= 1) {
-                    const int64_t u = shfl_up_i64(inc, off);
-                    if (lane >= off) inc = max(inc, u);
+                    const int64_t t = shfl_up_i64(inc, off);
+                    if (lane >= off) inc = max(inc, t);
                 }
                 int64_t ex = shfl_up_i64(inc, 1);
                 ex = lane == 0 ? pre : max(pre, ex);
