@@ -229,6 +229,9 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
     int32_t nxt = q0;
     int64_t h_r = rr[nxt & RING_MASK], n_r = rr[(nxt + 1) & RING_MASK];
     uint2 h_dj = rdj[nxt & RING_MASK], n_dj = rdj[(nxt + 1) & RING_MASK];
+    // co-located: the head's prefill time, kept in a register like h_r (off the
+    // event chain's shared-memory latency)
+    int32_t h_pf = COLO ? rpf[nxt & RING_MASK] : 0, n_pf = COLO ? rpf[(nxt + 1) & RING_MASK] : 0;
     // next candidate after k0, for stop checks and leader_pos
     const int32_t nseg_r = cx.nseg;
     int32_t kb = k0 + 1;
@@ -257,6 +260,10 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
         const int e1 = (nxt + 1) & RING_MASK;
         n_r = rr[e1];
         n_dj = rdj[e1];
+        if constexpr (COLO) {
+            h_pf = n_pf;
+            n_pf = rpf[e1];
+        }
     };
     // advance() when no ring maintenance is due ((nxt + 2) & 127 > 1): no
     // convergent operations, so no reconvergence region in the loops using it
@@ -267,6 +274,10 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
         const int e1 = (nxt + 1) & RING_MASK;
         n_r = rr[e1];
         n_dj = rdj[e1];
+        if constexpr (COLO) {
+            h_pf = n_pf;
+            n_pf = rpf[e1];
+        }
     };
     auto fin_addr = [&](uint32_t j, int32_t q) -> int64_t * {
         return to_rows ? fin_rows + 2 * (int64_t)j : fin_spec + q;
@@ -295,7 +306,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
         // fast paths hand such heads to the admission loop.
         auto prefill = [&]() {
             if constexpr (COLO) {
-                T += (int64_t)rpf[nxt & RING_MASK];
+                T += (int64_t)h_pf;
                 if (lane == 0) {
                     if (to_rows) fin_rows[2 * (int64_t)h_dj.y - 1] = T - h_r;
                     else ttft_spec[nxt] = T - h_r;
@@ -549,7 +560,7 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                     I = 0;
                 }
                 if constexpr (COLO) {  // the prefill runs alone on the GPU (R42)
-                    T += (int64_t)rpf[nxt & RING_MASK];
+                    T += (int64_t)h_pf;
                     const uint32_t j = h_dj.y;
                     if (lane == 0) {
                         if (to_rows) fin_rows[2 * (int64_t)j - 1] = T - h_r;
