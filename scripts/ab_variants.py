@@ -553,3 +553,24 @@ VARIANTS["expnl"] = [_EXP_NL]
 VARIANTS["explv"] = [_EXP_NL, _EXP_LV]
 VARIANTS["expjn"] = [_EXP_JN, _EXP_JN2]
 VARIANTS["expall"] = [_EXP_NL, _EXP_LV, _EXP_JN, _EXP_JN2]
+
+# the run's makespan from T where the batch empties (idle branch) instead of a
+# 64-bit move at every leave of the SPL = 1 fast loops
+VARIANTS["nomk"] = [
+    ("k_decode.cuh", '''                    if (lv) *fa = T;
+                    mk = T;
+                    const bool one = (lm & (lm - 1u)) == 0u;''', '''                    if (lv) *fa = T;
+                    const bool one = (lm & (lm - 1u)) == 0u;'''),
+    ("k_decode.cuh", '''                        b -= nl;
+                        log_b();
+                        mk = T;
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        shift_down();''', '''                        b -= nl;
+                        log_b();
+                        fmin = __reduce_min_sync(FULL, Fm);
+                        shift_down();'''),
+    ("k_decode.cuh", '''            if (b == 0) {  // idle until the next decode request is ready (R17)
+                if (h_r == INT64_MAX) {''', '''            if (b == 0) {  // idle until the next decode request is ready (R17)
+                mk = T;  // the batch emptied at its last finish
+                if (h_r == INT64_MAX) {'''),
+]
