@@ -14,7 +14,7 @@ from oracle import oracle as O
 from paper_2412_20322_b200 import api
 from paper_2412_20322_b200 import native as N
 from paper_2412_20322_b200.inputs import (MODE_DPD, MODE_DSD, MODE_SPEC_COLO, MODE_STANDALONE,
-                                          GridSpec, build_config, custom_trace)
+                                          GridSpec, build_config, custom_trace, subset_chains)
 
 ALL_MODES = (MODE_DPD, MODE_DSD, MODE_STANDALONE, MODE_SPEC_COLO)
 from tests.helpers import make_chain, make_tables, random_case
@@ -297,6 +297,24 @@ def test_determinism_and_chain_order_invariance():
         api.eval_grid(dg, lo, hi, stats=full[lo:hi])
     torch.cuda.synchronize()
     assert api.stats_numpy(full).tobytes() == a.tobytes()
+
+
+def test_concurrent_calls_on_two_streams():
+    # two gl_eval_grid calls in flight at once on different streams, each splitting
+    # its chains over several k_stages blocks (decoupled look-back, ticket order) and
+    # running speculative decode helpers: no deadlock, results equal to one at a time
+    gs = [build_config(4, n=6000), subset_chains(build_config(2, n=4000), list(range(8)))]
+    dgs = [api.DeviceGrid(g) for g in gs]
+    want = [api.stats_numpy(api.eval_grid(dg)[0]) for dg in dgs]
+    outs = [torch.empty((dg.n_chains, 80), dtype=torch.uint8, device="cuda") for dg in dgs]
+    streams = [torch.cuda.Stream(), torch.cuda.Stream()]
+    torch.cuda.synchronize()
+    for rep in range(3):
+        for dg, out, st in zip(dgs, outs, streams):
+            api.eval_grid(dg, stats=out, stream=st)
+        torch.cuda.synchronize()
+        for w, out in zip(want, outs):
+            assert api.stats_numpy(out).tobytes() == w.tobytes()
 
 
 # ------------------------------------------------------------------- Alg. 1
