@@ -204,6 +204,36 @@ def test_break_even_ci_A5():
         assert choice[0] == want and fb[0] == 0
 
 
+def test_ci_limits_and_lower_envelope():
+    """CI limits (Eq. 4): at CI = 0 Alg. 1 picks the
+    least embodied chain, as CI grows it ends on the least-energy chain, and in
+    between the choice is piecewise constant, walking down the lower envelope of
+    the lines total(CI) = emb + CI kWh -- each switch goes to a chain with strictly
+    less energy and more embodied carbon.  Embodied carbon is monotone in busy time
+    (Eq. 1) and kWh in integer energy (Eq. 2), so the extremes are fixed by integers."""
+    rng = np.random.default_rng(77)
+    lt = 7 * YEAR
+    for trial in range(20):
+        k = int(rng.integers(2, 9))
+        e = rng.choice(np.arange(1, 10_000), size=k, replace=False) * 10**9  # distinct uJ
+        busy = rng.choice(np.arange(1, 10_000), size=k, replace=False) * 10**6  # distinct us
+        st = [_stats(e_new=e[i], busy_new=busy[i]) for i in range(k)]
+
+        def choose(ci):
+            tot = np.array([[O.carbon(x, 26340.0, 10300.0, ci, lt, lt)[2] for x in st]])
+            c, fb = O.alg1(tot, np.ones((1, k)), np.ones((1, k)), np.ones((1, k)), np.ones((1, k)))
+            assert fb[0] == 0
+            return int(c[0])
+        assert choose(0.0) == int(np.argmin(busy))        # least embodied
+        assert choose(1e12) == int(np.argmin(e))          # least energy
+        path = [choose(ci) for ci in np.geomspace(1e-6, 1e12, 200)]
+        switches = [(a, b) for a, b in zip(path, path[1:]) if a != b]
+        assert len(switches) <= k - 1
+        for a_, b_ in switches:                            # down the lower envelope
+            assert e[b_] < e[a_] and busy[b_] > busy[a_]
+        assert len(set(path)) == len(switches) + 1         # no chain chosen twice
+
+
 def test_eq5_savings_ratio_from_totals():
     """Eq. 5: ratio of Case-2 to Case-1 totals equals
     ((N_A'+N_B) a + E_A'+E_B) / (N_A a + E_A); SPEC S:500 example 183.5/261.5."""
