@@ -574,3 +574,34 @@ VARIANTS["nomk"] = [
                 mk = T;  // the batch emptied at its last finish
                 if (h_r == INT64_MAX) {'''),
 ]
+
+# co-located light loop: heads already ready after a join's prefill join at once
+# inside the loop (each after its own prefill) instead of via the admission loop
+VARIANTS["colojoin"] = [("k_decode.cuh", '''                        ++b;
+                        log_b();
+                        shift_up();
+                        advance_fast();
+                        if (b == cap || h_r <= T) break;
+                    } else {  // leave at iteration fmin (R16)''', '''                        ++b;
+                        log_b();
+                        shift_up();
+                        advance_fast();
+                        if constexpr (COLO) {
+                            while (b < cap && h_r <= T && h_dj.x != 0 && ((nxt + 2) & 127) > 1) {
+                                prefill();
+                                const unsigned bit2 = fr & (0u - fr);
+                                fr ^= bit2;
+                                const uint32_t fnew2 = I + h_dj.x;
+                                if (lane_bit == bit2) {
+                                    Fm = fnew2;
+                                    fa = fin_addr(h_dj.y, nxt);
+                                }
+                                fmin = min(fmin, fnew2);
+                                ++b;
+                                log_b();
+                                shift_up();
+                                advance_fast();
+                            }
+                        }
+                        if (b == cap || h_r <= T) break;
+                    } else {  // leave at iteration fmin (R16)''')]
