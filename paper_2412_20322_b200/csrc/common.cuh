@@ -41,7 +41,8 @@ struct DChainX {
     int32_t next_seg;    // helper work counter
     int32_t n_ev;        // LOG launches: batch-size log entries written
     int32_t stage_done;  // k_stages CTAs of this chain that have finished
-    int32_t pad[2];
+    int32_t seg_done;    // k_segments CTAs of this chain that have finished
+    int32_t pad;
 };
 
 // one k_stages CTA's share of a chain (k_stages splits a chain over S CTAs): its

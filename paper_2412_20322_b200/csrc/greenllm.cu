@@ -258,6 +258,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     total += align256(sizeof(int64_t) * (size_t)dec_total * 2 * (size_t)std::max(extra, 1));
     const size_t off_segs = total;
     total += align256(sizeof(int32_t) * (size_t)seg_total);
+    const size_t off_segwc = total;
+    total += align256(sizeof(int32_t) * (size_t)seg_total);
     // gl_link_demand: batch-size logs [2 n + 8], prefix sums, per-block partials, stats
     std::vector<int64_t> ev_off(n_chains, 0), rq_off(n_chains, 0), evs_off(n_chains, 0);
     int64_t ev_total = 0, rq_total = 0, evs_total = 0;
@@ -427,7 +429,10 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     }
     if (e == cudaSuccess) {
         prof_begin("k_segments", stream);
-        gl::k_segments<<<n_chains, 1024, 0, stream>>>(dc);
+        // k_segments: 1024-thread blocks, one per SM; S per chain while they fit in a wave
+        const int seg_split = std::max(1, std::min(4, n_sm / std::max(1, (int)n_chains)));
+        gl::k_segments<<<n_chains * seg_split, 1024, 0, stream>>>(
+            dc, seg_split, (int64_t)((off_segwc - off_segs) / sizeof(int32_t)));
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;

@@ -484,21 +484,27 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
 // requests, the request with the largest slack if it is >= 0 (ties: the first).
 // Any choice is exact -- k_decode verifies every candidate it uses -- this one
 // makes almost all candidates true idle points (SEG_LEN bounds how many there are).
-// One 1024-thread block per chain; windows are processed in rounds of SEG_ROUND:
+// S 1024-thread blocks per chain, each over a contiguous range of windows (its
+// carry-in: a plain max over the earlier windows); windows in rounds of SEG_ROUND:
 //   pass 1  warp per window: max of the lower bounds          -> smem
 //   scan    exclusive prefix max over windows (carry across rounds)
 //   pass 2  warp per window: in-window prefix max (8 warp scans), best slack
-//   compact candidate flags -> seg_start[]
+//   per-window candidates -> seg_wc[]; the chain's last block compacts them into
+//   seg_start[] (in window order)
 constexpr int SEG_ROUND = 128;  // windows per round: a round (512 KB per chain) stays in L2 for pass 2
 
 __global__ void __launch_bounds__(1024)
-    k_segments(const DChain *__restrict__ chains)
+    k_segments(const DChain *__restrict__ chains, int32_t S, int64_t wc_delta)
 {
     __shared__ int64_t wpre[SEG_ROUND];
-    __shared__ int32_t wcand[SEG_ROUND];
     __shared__ int32_t s_min_step;
+    __shared__ int32_t s_last;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nw = blockDim.x >> 5;
-    const DChain &ch = chains[blockIdx.x];
+    const int32_t chain = (int32_t)(blockIdx.x / S), sb = (int32_t)(blockIdx.x % S);
+    const DChain &ch = chains[chain];
+    // each window's candidate (q) or -1: a scratch array laid out like seg_start,
+    // wc_delta entries after it (kept out of DChain, whose layout k_decode sees)
+    int32_t *const seg_wc = ch.seg_start + wc_delta;
     const int32_t M = ch.x->M;
     const bool colo = ch.mode == GL_MODE_STANDALONE || ch.mode == GL_MODE_SPEC_COLO;
     if (threadIdx.x == 0) s_min_step = INT32_MAX;
@@ -511,20 +517,35 @@ __global__ void __launch_bounds__(1024)
     }
     __syncthreads();
     const int64_t smin = s_min_step;
+    auto lb_of = [&](int32_t q) -> int64_t {  // finish-time lower bound of request q
+        return __ldg(ch.dec_r + q) + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
+               (colo ? __ldg(ch.dec_pf + q) : 0);
+    };
     const int32_t nwin = (M + SEG_LEN - 1) / SEG_LEN;
-    int64_t carry = NEG_INF;  // max lower bound over all earlier rounds
-    int32_t ncand = 0;
-    for (int32_t w0 = 0; w0 < nwin; w0 += SEG_ROUND) {
-        const int32_t nwr = min(SEG_ROUND, nwin - w0);
+    // block sb of the chain's S blocks takes a contiguous range of windows; its
+    // carry-in is the max lower bound over all earlier windows (a plain reduction)
+    const int32_t per = (nwin + S - 1) / S;
+    const int32_t wlo = min(sb * per, nwin), whi = min(wlo + per, nwin);
+    int64_t carry = NEG_INF;  // max lower bound over all earlier windows (warp 0)
+    if (wlo > 0) {
+        int64_t m = NEG_INF;
+        const int32_t qe = wlo * SEG_LEN;
+        for (int32_t q = threadIdx.x; q < qe; q += blockDim.x) m = max(m, lb_of(q));
+        m = warp_max_i64(m);
+        if (lane == 0) wpre[warp] = m;
+        __syncthreads();
+        if (warp == 0) carry = warp_max_i64(lane < nw ? wpre[lane] : NEG_INF);
+        __syncthreads();
+    }
+    for (int32_t w0 = wlo; w0 < whi; w0 += SEG_ROUND) {
+        const int32_t nwr = min(SEG_ROUND, whi - w0);
         for (int32_t w = warp; w < nwr; w += nw) {  // pass 1
             const int32_t lo = (w0 + w) * SEG_LEN, hi = min(lo + SEG_LEN, M);
             int64_t m = NEG_INF;
 #pragma unroll
             for (int u = 0; u < SEG_LEN / 32; ++u) {  // all loads of the window in flight
                 const int32_t q = lo + 32 * u + lane;
-                if (q < hi)
-                    m = max(m, __ldg(ch.dec_r + q) + (int64_t)__ldg(&ch.dec_dj[q].x) * smin +
-                                   (colo ? __ldg(ch.dec_pf + q) : 0));
+                if (q < hi) m = max(m, lb_of(q));
             }
             m = warp_max_i64(m);
             if (lane == 0) wpre[w] = m;
@@ -545,8 +566,7 @@ __global__ void __launch_bounds__(1024)
                 if (w < nwr) wpre[w] = ex;
                 run = max(run, shfl_i64(v, 31));
             }
-            if (lane == 0) wcand[0] = 0;  // placeholder, rewritten in pass 2
-            carry = run;                   // lane-uniform
+            carry = run;  // lane-uniform
         }
         __syncthreads();
         for (int32_t w = warp; w < nwr; w += nw) {  // pass 2
@@ -593,25 +613,32 @@ __global__ void __launch_bounds__(1024)
                     best_q = oq;
                 }
             }
-            if (lane == 0) wcand[w] = (w0 + w == 0) ? 0 : (best >= 0 ? best_q : -1);
-        }
-        __syncthreads();
-        if (warp == 0) {  // compact the round's candidates
-            for (int32_t base = 0; base < nwr; base += 32) {
-                const int32_t w = base + lane;
-                const int32_t cq = w < nwr ? wcand[w] : -1;
-                const unsigned bal = __ballot_sync(FULL, cq >= 0);
-                if (cq >= 0) ch.seg_start[ncand + __popc(bal & ((1u << lane) - 1u))] = cq;
-                ncand += __popc(bal);
-            }
+            if (lane == 0) seg_wc[w0 + w] = (w0 + w == 0) ? 0 : (best >= 0 ? best_q : -1);
         }
         __syncthreads();
     }
-    if (threadIdx.x == 0) {
-        ch.seg_start[ncand] = M;
-        ch.x->nseg = ncand;
-        ch.x->leader_pos = 0;
-        ch.x->next_seg = 1;
+    // the chain's last block compacts every window's candidate into seg_start[]
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(&ch.x->seg_done, 1) == S - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    int32_t ncand = 0;
+    if (warp == 0) {
+        for (int32_t base = 0; base < nwin; base += 32) {
+            const int32_t w = base + lane;
+            const int32_t cq = w < nwin ? __ldcg(seg_wc + w) : -1;
+            const unsigned bal = __ballot_sync(FULL, cq >= 0);
+            if (cq >= 0) ch.seg_start[ncand + __popc(bal & ((1u << lane) - 1u))] = cq;
+            ncand += __popc(bal);
+        }
+        if (lane == 0) {
+            ch.seg_start[ncand] = M;
+            ch.x->nseg = ncand;
+            ch.x->leader_pos = 0;
+            ch.x->next_seg = 1;
+        }
     }
 }
 
