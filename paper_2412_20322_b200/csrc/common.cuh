@@ -89,6 +89,9 @@ struct DChain {
     int64_t out_off;  // first row of this chain in the per-request (ttft, finish) array
     int32_t mode, cap, max_prompt, capacity_ok;
 };
+// A size that is a multiple of 16 B keeps every chains[i] 16-B aligned, which k_decode's
+// schedule depends on: an 8-B pad field made k_decode 2.6% slower.
+static_assert(sizeof(DChain) % 16 == 0, "DChain: keep the size a multiple of 16 bytes");
 
 // ceil(gap / st) for 0 < gap < 2^31, 1 <= st < 2^31 without a division:
 // Lemire, Kaser & Kurz (2019): with M = floor((2^64 - 1) / d) + 1, floor(x / d) =

@@ -605,3 +605,31 @@ VARIANTS["colojoin"] = [("k_decode.cuh", '''                        ++b;
                         }
                         if (b == cap || h_r <= T) break;
                     } else {  // leave at iteration fmin (R16)''')]
+
+# DChain layout variants (ptxas schedules k_decode differently per layout; adding a
+# pointer field after seg_start cost 2.6%)
+_DC_END = '''    int32_t mode, cap, max_prompt, capacity_ok;
+};'''
+VARIANTS["lay_pad8"] = [("common.cuh", _DC_END, '''    int32_t mode, cap, max_prompt, capacity_ok;
+    int64_t pad0;
+};''')]
+VARIANTS["lay_pad16"] = [("common.cuh", _DC_END, '''    int32_t mode, cap, max_prompt, capacity_ok;
+    int64_t pad0, pad1;
+};''')]
+VARIANTS["lay_stp_end"] = [
+    ("common.cuh", '''    DStagePart *stp;    // [stage_split] k_stages partials of this chain
+''', ''),
+    ("common.cuh", _DC_END, '''    int32_t mode, cap, max_prompt, capacity_ok;
+    DStagePart *stp;
+};''')]
+VARIANTS["lay_pad_front"] = [("common.cuh", '''    int64_t *dec_r;
+    uint2 *dec_dj;''', '''    void *pad_front;
+    int64_t *dec_r;
+    uint2 *dec_dj;''')]
+VARIANTS["lay_x_first"] = [
+    ("common.cuh", '''    DChainX *x;
+    DStagePart *stp;''', '''    DStagePart *stp;'''),
+    ("common.cuh", '''struct DChain {
+    const int64_t *a;''', '''struct DChain {
+    DChainX *x;
+    const int64_t *a;''')]
