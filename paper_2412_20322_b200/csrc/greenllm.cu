@@ -35,6 +35,7 @@
 #include <cstdlib>
 #include <cstring>
 #include <map>
+#include <set>
 #include <tuple>
 #include <vector>
 
@@ -155,6 +156,46 @@ gl_status validate_chain(const gl_chain &c, int32_t n_traces)
 
 gl_status cuda_status(cudaError_t e) { return e == cudaSuccess ? GL_OK : GL_E_CUDA; }
 
+// A side stream forked from `from` (its work starts after everything enqueued on
+// `from` so far), with an event for joining it back.  One per (host thread, device,
+// slot), created on first use and kept: creating a stream per call costs more than
+// the overlap it buys.  Returns false (and nothing to join) if CUDA refuses.
+struct SideStream {
+    cudaStream_t s = nullptr;
+    cudaEvent_t fork = nullptr, join = nullptr;
+};
+bool side_fork(int slot, cudaStream_t from, cudaStream_t &side, cudaEvent_t &join)
+{
+    thread_local SideStream tl[16][2];  // [device][slot]
+    int dev = 0;
+    if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) {
+        cudaGetLastError();
+        return false;
+    }
+    SideStream &ss = tl[dev][slot];
+    if (!ss.s) {
+        SideStream n;
+        if (cudaStreamCreateWithFlags(&n.s, cudaStreamNonBlocking) == cudaSuccess &&
+            cudaEventCreateWithFlags(&n.fork, cudaEventDisableTiming) == cudaSuccess &&
+            cudaEventCreateWithFlags(&n.join, cudaEventDisableTiming) == cudaSuccess) {
+            ss = n;
+        } else {
+            cudaGetLastError();
+            if (n.s) cudaStreamDestroy(n.s);
+            if (n.fork) cudaEventDestroy(n.fork);
+            return false;
+        }
+    }
+    if (cudaEventRecord(ss.fork, from) != cudaSuccess ||
+        cudaStreamWaitEvent(ss.s, ss.fork, 0) != cudaSuccess) {
+        cudaGetLastError();
+        return false;
+    }
+    side = ss.s;
+    join = ss.join;
+    return true;
+}
+
 // the extra work of gl_link_demand
 struct LinkReq {
     const gl_link_params *params;  // host [n_chains]
@@ -164,7 +205,8 @@ struct LinkReq {
 
 gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
                     int32_t n_chains, gl_chain_stats *stats_out, int64_t *per_request_out,
-                    cudaStream_t stream, const LinkReq *lk)
+                    cudaStream_t stream, const LinkReq *lk,
+                    cudaEvent_t stages_wait = nullptr)  // k_stages waits for it (host path)
 {
     gl_status st = validate_traces(traces, n_traces);
     if (st) return st;
@@ -415,6 +457,9 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         prof_end(stream);
         ++launches;
     }
+    // gl_evaluate_host: the arrival arrays may still be in flight on a copy stream
+    // (k_dsd_demand above needs only the output lengths)
+    if (e == cudaSuccess && stages_wait) e = cudaStreamWaitEvent(stream, stages_wait, 0);
     if (e == cudaSuccess) {
         e = cudaFuncSetAttribute(gl::k_stages, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_st);
@@ -456,19 +501,9 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         // side stream forked from `stream` and joined back, so the two launches
         // (disjoint chains) overlap; the call stays stream-ordered on `stream`.
         cudaStream_t side = nullptr;
-        cudaEvent_t ev_fork = nullptr, ev_join = nullptr;
-        if (has_disg && has_colo && !lk) {
-            const bool forked =
-                cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking) == cudaSuccess &&
-                cudaEventCreateWithFlags(&ev_fork, cudaEventDisableTiming) == cudaSuccess &&
-                cudaEventCreateWithFlags(&ev_join, cudaEventDisableTiming) == cudaSuccess &&
-                cudaEventRecord(ev_fork, stream) == cudaSuccess &&
-                cudaStreamWaitEvent(side, ev_fork, 0) == cudaSuccess;
-            if (!forked) {  // no fork: both launches stay on `stream` (serialised)
-                cudaGetLastError();
-                if (side) cudaStreamDestroy(side);
-                side = nullptr;
-            }
+        cudaEvent_t ev_join = nullptr;
+        if (has_disg && has_colo && !lk && !side_fork(0, stream, side, ev_join)) {
+            side = nullptr;  // no fork: both launches stay on `stream` (serialised)
         }
         // disaggregated chains, then co-located ones (each launch skips the others)
         if (has_disg && lk) {  // runs that also log the batch size
@@ -507,9 +542,6 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             if (r == cudaSuccess) r = cudaStreamWaitEvent(stream, ev_join, 0);
             if (e == cudaSuccess) e = r;
         }
-        if (ev_fork) cudaEventDestroy(ev_fork);
-        if (ev_join) cudaEventDestroy(ev_join);
-        if (side) cudaStreamDestroy(side);  // released once its work completes
     }
     if (e == cudaSuccess) {
         const int per_thread = 8;
@@ -890,9 +922,22 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&dev), total, stream)))) return st;
     std::vector<gl_trace> dtr(n_traces);
     cudaError_t e = cudaSuccess;
-    for (size_t k = 0; k < arr_list.size() && e == cudaSuccess; ++k)
-        e = cudaMemcpyAsync(dev + arr_off[arr_list[k]], arr_list[k].first, arr_list[k].second,
-                            cudaMemcpyHostToDevice, stream);
+    // Arrival arrays go on a side stream forked from `stream`, so their copy overlaps
+    // k_dsd_demand (which needs only the output lengths, copied first on `stream`);
+    // k_stages waits for the side stream's event.  No fork: everything on `stream`.
+    std::set<const void *> arrivals;
+    for (int32_t t = 0; t < n_traces; ++t) arrivals.insert(host_traces[t].arrival_us);
+    cudaStream_t side = nullptr;
+    cudaEvent_t ev_arr = nullptr;
+    if (!side_fork(1, stream, side, ev_arr)) side = nullptr;
+    for (int pass = 0; pass < 2; ++pass)  // lengths first, then arrivals
+        for (size_t k = 0; k < arr_list.size() && e == cudaSuccess; ++k) {
+            const bool arr = arrivals.count(arr_list[k].first) != 0;
+            if (arr != (pass == 1)) continue;
+            e = cudaMemcpyAsync(dev + arr_off[arr_list[k]], arr_list[k].first, arr_list[k].second,
+                                cudaMemcpyHostToDevice, (arr && side) ? side : stream);
+        }
+    if (e == cudaSuccess && side) e = cudaEventRecord(ev_arr, side);
     for (int32_t t = 0; t < n_traces; ++t) {
         const gl_trace &h = host_traces[t];
         const size_t n = (size_t)h.n;
@@ -904,7 +949,9 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
     int launches = 0;
     if (e == cudaSuccess) {
         gl_chain_stats *dstats = reinterpret_cast<gl_chain_stats *>(dev + o_stats);
-        st = gl_eval_grid(dtr.data(), n_traces, chains, n_chains, dstats, nullptr, stream_);
+        g_last_launches = 0;
+        st = eval_impl(dtr.data(), n_traces, chains, n_chains, dstats, nullptr, stream, nullptr,
+                       side ? ev_arr : nullptr);
         launches += g_last_launches;
         if (st == GL_OK) {
             st = gl_argmin_feasible(dstats, n_chains, chains, scen, n_scen, grid, slo_num, slo_den,
@@ -927,6 +974,10 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
                 e = cudaMemcpyAsync(via_fallback_host, dev + o_fb, rows, cudaMemcpyDeviceToHost,
                                     stream);
         }
+    }
+    if (side) {  // join the side stream (a no-op when k_stages already waited on it)
+        cudaError_t r = cudaStreamWaitEvent(stream, ev_arr, 0);
+        if (e == cudaSuccess) e = r;
     }
     cudaError_t ef = cudaFreeAsync(dev, stream);
     cudaError_t es = cudaStreamSynchronize(stream);
