@@ -19,12 +19,14 @@
  *    implements the same rules independently.
  *  - "device" = CUDA device memory of the current device; "host" = CPU memory.
  *  - The caller owns every buffer.  The library keeps no global state besides
- *    a cached device-capability check, allocates only stream-ordered scratch
- *    (cudaMallocAsync / cudaFreeAsync on `stream`) and never synchronises
- *    except in gl_evaluate_host.  When one gl_eval_grid call holds both
- *    disaggregated and co-located chains, it forks a temporary side stream from
- *    `stream` (event record / wait) for the co-located decode launch and joins it
- *    back before returning, so the call remains ordered on `stream`.
+ *    a cached device-capability check and, per host thread and device, two side
+ *    streams with their events (created on first use, kept for the process);
+ *    it allocates only stream-ordered scratch (cudaMallocAsync / cudaFreeAsync
+ *    on `stream`) and never synchronises except in gl_evaluate_host.  When one
+ *    gl_eval_grid call holds both disaggregated and co-located chains, it forks
+ *    a side stream from `stream` (event record / wait) for the co-located decode
+ *    launch and joins it back before returning, so the call remains ordered on
+ *    `stream`; if the fork fails the two launches run one after the other.
  *  - Calls are asynchronous and stream-ordered (except gl_evaluate_host):
  *    device buffers must stay valid until `stream` has passed the call; host
  *    descriptor arrays are consumed before the call returns.
@@ -200,9 +202,11 @@ gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains,
 
 /*
  * End to end from host buffers: copies the traces host->device (each distinct
- * host array once -- traces sharing an array share its device copy), runs
- * gl_eval_grid and gl_argmin_feasible, copies the results device->host and
- * synchronises `stream` before returning.
+ * host array once -- traces sharing an array share its device copy; the arrival
+ * arrays on a side stream forked from `stream`, overlapping the DSD demand
+ * kernel), runs gl_eval_grid and gl_argmin_feasible, copies the results
+ * device->host and synchronises `stream` before returning.  Host arrays should
+ * be pinned for the copies to be asynchronous.
  *   host_traces      HOST descriptors with HOST data pointers
  *   chains           as for gl_eval_grid (tables stay in DEVICE memory)
  *   stats_host       HOST [n_chains];  carbon_host HOST [rows*cols] or NULL
