@@ -383,6 +383,31 @@ def test_evaluate_host_matches_device_path():
     assert res.launches == 6 and res.h2d_bytes > 0
 
 
+def test_evaluate_host_pageable_inputs_other_stream_both_families():
+    # pageable host arrays (synchronous staging), a non-default stream, and a grid
+    # with disaggregated and co-located chains (both side streams in use)
+    g = build_config(6, n=2500)
+    dg = api.DeviceGrid(g)
+    stats, _ = api.eval_grid(dg)
+    _, choice, fb = api.argmin_feasible(dg, stats)
+    torch.cuda.synchronize()
+    cache = {}
+    host = []
+    for tr in g.traces:
+        arrs = []
+        for x in (tr.arrival_us, tr.prompt_len, tr.output_len):
+            if id(x) not in cache:
+                cache[id(x)] = torch.from_numpy(np.ascontiguousarray(x).copy())
+            arrs.append(cache[id(x)])
+        host.append(tuple(arrs))
+    st = torch.cuda.Stream()
+    for _ in range(2):
+        res = api.evaluate_host(dg, host, stream=st)
+        assert res.stats.tobytes() == api.stats_numpy(stats).tobytes()
+        assert np.array_equal(res.choice, choice.cpu().numpy())
+        assert np.array_equal(res.via_fallback, fb.cpu().numpy())
+
+
 def test_abi_errors():
     g = build_config(1)
     dg = api.DeviceGrid(g)
