@@ -527,7 +527,7 @@ __global__ void __launch_bounds__(1024)
     const int32_t per = (nwin + S - 1) / S;
     const int32_t wlo = min(sb * per, nwin), whi = min(wlo + per, nwin);
     int64_t carry = NEG_INF;  // max lower bound over all earlier windows (warp 0)
-    if (wlo > 0) {
+    if (wlo > 0 && wlo < whi) {  // (earlier windows are full: wlo * SEG_LEN <= M)
         int64_t m = NEG_INF;
         const int32_t qe = wlo * SEG_LEN;
         for (int32_t q = threadIdx.x; q < qe; q += blockDim.x) m = max(m, lb_of(q));
