@@ -633,3 +633,8 @@ VARIANTS["lay_x_first"] = [
     const int64_t *a;''', '''struct DChain {
     DChainX *x;
     const int64_t *a;''')]
+
+# k_stages: 8-warp blocks (two per SM by registers), split width up to 8
+VARIANTS["st8"] = [("k_stages.cuh", '''constexpr int ST_WARPS = 16;
+constexpr int ST_MAX_SPLIT = 4;  // blocks per chain''', '''constexpr int ST_WARPS = 8;
+constexpr int ST_MAX_SPLIT = 8;  // blocks per chain''')]
