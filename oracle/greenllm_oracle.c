@@ -241,6 +241,7 @@ static uint32_t or_simulate(const int64_t *a, const uint32_t *p, const uint32_t 
                 ++nxt;
             }
             if (size == 0) { /* idle until the next arrival */
+                if (nxt >= n) break; /* the last admissions were o = 1 requests */
                 T = or_max(T, a[nxt]);
                 continue;
             }

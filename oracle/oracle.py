@@ -20,6 +20,12 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "greenllm_oracle.c")
 LIB = os.path.join(HERE, "liboracle.so")
 CFLAGS = ["-O2", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-shared", "-fPIC"]
+# the same source under AddressSanitizer + UndefinedBehaviorSanitizer
+# (any report aborts); tests/test_oracle_sanitizers.py runs the pin suite against it
+SAN_LIB = os.path.join(HERE, "liboracle_san.so")
+SAN_CFLAGS = ["-O1", "-g", "-std=gnu11", "-ffp-contract=off", "-fno-fast-math", "-shared",
+              "-fPIC", "-fsanitize=address,undefined", "-fno-sanitize-recover=all",
+              "-fno-omit-frame-pointer"]
 
 ST_UNSORTED, ST_PROMPT_RANGE, ST_OUTPUT_ZERO, ST_OVERFLOW, ST_NEG_ARRIVAL = 1, 2, 4, 8, 16
 STAT_FIELDS = ("n", "slo_ok", "tokens", "busy_new_us", "busy_old_us", "e_new_uj", "e_old_uj",
@@ -56,12 +62,25 @@ def build(force: bool = False) -> str:
     return LIB
 
 
+def build_sanitized(force: bool = False) -> str:
+    """Compile liboracle_san.so (ASan + UBSan; load it under LD_PRELOAD=libasan)."""
+    if force or not os.path.exists(SAN_LIB) or os.path.getmtime(SAN_LIB) < os.path.getmtime(SRC):
+        tmp = SAN_LIB + f".tmp{os.getpid()}"
+        subprocess.check_call(["gcc", *SAN_CFLAGS, "-o", tmp, SRC, "-lm"])
+        os.replace(tmp, SAN_LIB)
+    return SAN_LIB
+
+
 def lib():
     global _lib
     with _lock:
         if _lib is None:
-            build()
-            L = C.CDLL(LIB)
+            # GREENLLM_ORACLE_SANITIZED=1: the ASan/UBSan build (test_oracle_sanitizers)
+            if os.environ.get("GREENLLM_ORACLE_SANITIZED") == "1":
+                L = C.CDLL(build_sanitized())
+            else:
+                build()
+                L = C.CDLL(LIB)
             L.oracle_simulate_chain.restype = C.c_uint32
             L.oracle_simulate_chain.argtypes = [C.c_void_p, C.c_void_p, C.c_void_p, C.c_int64,
                                                 C.POINTER(OrChain), C.POINTER(OrStats),
@@ -336,7 +355,9 @@ def evaluate_grid(grid, chain_ids=None, per_request=False):
             total[r, c] = carbon(st, ch.ce_new_g, ch.ce_old_g, sc[0], sc[1], sc[2])[2]
             ok[r, c], n[r, c] = st["slo_ok"], st["n"]
             present[r, c] = 1
-            cap[r, c] = ch.capacity_ok
+            # R55: a chain with invalid input (status bits) is never feasible; like a
+            # capacity-infeasible one it counts as ok = 0, total = +inf in the fallback
+            cap[r, c] = 1 if (ch.capacity_ok and st["status"] == 0) else 0
     choice, fb = alg1(total, ok, n, present, cap, grid.slo_num, grid.slo_den, grid.priority,
                       grid.default_col)
     return dict(stats=stats, per_request=per, carbon=total, choice=choice, via_fallback=fb,

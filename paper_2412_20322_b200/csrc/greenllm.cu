@@ -30,6 +30,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <atomic>
 #include <cmath>
 #include <cstdint>
 #include <cstdlib>
@@ -87,24 +88,44 @@ void prof_end(cudaStream_t s)
     ++g_prof.used;
 }
 
+// Per device (ordinal < 64): the compute-capability verdict, cached in an atomic
+// once known (a failed query is retried next call); the pool setup it does is
+// idempotent, so two threads racing on the first call are harmless.  Devices
+// beyond 64 are checked every call.
+constexpr int MAX_DEV = 64;
+std::atomic<int> g_dev_ok[MAX_DEV];  // 0 = unknown, 1 = sm_100, 2 = unsupported
+
+int query_device(int dev)
+{
+    int major = 0, minor = 0;
+    if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
+        cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess) {
+        cudaGetLastError();
+        return 3;
+    }
+    if (major != 10 || minor != 0) return 2;
+    cudaMemPool_t pool;
+    if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
+        uint64_t thr = UINT64_MAX;  // keep stream-ordered scratch cached in the pool
+        cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
+    }
+    cudaGetLastError();
+    return 1;
+}
+
 gl_status device_check()
 {
-    static int cached = -1;  // 1 = ok, 0 = unsupported
     int dev = 0;
-    if (cudaGetDevice(&dev) != cudaSuccess) return GL_E_CUDA;
-    if (cached < 0) {
-        int major = 0, minor = 0;
-        if (cudaDeviceGetAttribute(&major, cudaDevAttrComputeCapabilityMajor, dev) != cudaSuccess ||
-            cudaDeviceGetAttribute(&minor, cudaDevAttrComputeCapabilityMinor, dev) != cudaSuccess)
-            return GL_E_CUDA;
-        cached = (major == 10 && minor == 0) ? 1 : 0;
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, dev) == cudaSuccess) {
-            uint64_t thr = UINT64_MAX;  // keep stream-ordered scratch cached in the pool
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &thr);
-        }
+    if (cudaGetDevice(&dev) != cudaSuccess) {
+        cudaGetLastError();
+        return GL_E_CUDA;
     }
-    return cached ? GL_OK : GL_E_UNSUPPORTED;
+    int v = (dev >= 0 && dev < MAX_DEV) ? g_dev_ok[dev].load() : 0;
+    if (v == 0) {
+        v = query_device(dev);  // 3 = the query failed: not cached
+        if (v != 3 && dev >= 0 && dev < MAX_DEV) g_dev_ok[dev].store(v);
+    }
+    return v == 1 ? GL_OK : (v == 2 ? GL_E_UNSUPPORTED : GL_E_CUDA);
 }
 
 bool aligned16(const void *p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; }
@@ -292,12 +313,14 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     // SM in total; each helper keeps its finish times in a buffer of its own
     // (capped at 8 GiB of scratch)
     int extra = std::max(0, std::min(15, (4 * n_sm) / std::max(1, (int)n_chains) - 1));
-    // (gl_link_demand: helpers also keep batch-size logs, 2 entries x 16 B per request)
-    const size_t per_helper_req = 2 * sizeof(int64_t) + (lk ? 2 * sizeof(longlong2) : 0);
+    // helpers' buffers per decode-stream entry: finish times (co-located chains keep
+    // two columns, finish and TTFT) and, for gl_link_demand, batch-size logs (2
+    // entries x 16 B per request); none at all when there are no helpers
+    const int spec_mult = has_colo ? 2 : 1;
+    const size_t per_helper_req = spec_mult * sizeof(int64_t) + (lk ? 2 * sizeof(longlong2) : 0);
     while (extra > 0 && (size_t)dec_total * per_helper_req * extra > ((size_t)8 << 30)) --extra;
     const size_t off_spec = total;
-    // (co-located chains keep two columns per helper: finish and TTFT)
-    total += align256(sizeof(int64_t) * (size_t)dec_total * 2 * (size_t)std::max(extra, 1));
+    total += align256(sizeof(int64_t) * (size_t)dec_total * spec_mult * (size_t)extra);
     const size_t off_segs = total;
     total += align256(sizeof(int32_t) * (size_t)seg_total);
     const size_t off_segwc = total;
@@ -315,7 +338,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             rq_off[i] = rq_total;
             rq_total += n + 8;
             evs_off[i] = evs_total;
-            evs_total += (2 * n + 16) * std::max(extra, 1);
+            evs_total += (2 * n + 16) * extra;
         }
         off_ev = total;
         total += align256(sizeof(longlong2) * (size_t)ev_total);
@@ -399,7 +422,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         d.dec_r = reinterpret_cast<int64_t *>(scratch + off_dec_r) + dec_off[i];
         d.dec_dj = reinterpret_cast<uint2 *>(scratch + off_dec_dj) + dec_off[i];
         d.dec_pf = reinterpret_cast<int32_t *>(scratch + off_dec_pf) + dec_off[i];
-        d.spec_fin = reinterpret_cast<int64_t *>(scratch + off_spec) + dec_off[i] * 2 * std::max(extra, 1);
+        d.spec_fin = reinterpret_cast<int64_t *>(scratch + off_spec) + dec_off[i] * spec_mult * extra;
         d.spec_stride = ((tr.n + 512 + 31) & ~(int64_t)31) *
                         ((c.mode == GL_MODE_STANDALONE || c.mode == GL_MODE_SPEC_COLO) ? 2 : 1);
         d.seg_start = reinterpret_cast<int32_t *>(scratch + off_segs) + seg_off[i];
@@ -937,7 +960,11 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
             e = cudaMemcpyAsync(dev + arr_off[arr_list[k]], arr_list[k].first, arr_list[k].second,
                                 cudaMemcpyHostToDevice, (arr && side) ? side : stream);
         }
-    if (e == cudaSuccess && side) e = cudaEventRecord(ev_arr, side);
+    if (side) {  // recorded whatever happened above, so the joins below never wait
+                 // on a stale record while copies queued on `side` are in flight
+        const cudaError_t r = cudaEventRecord(ev_arr, side);
+        if (e == cudaSuccess) e = r;
+    }
     for (int32_t t = 0; t < n_traces; ++t) {
         const gl_trace &h = host_traces[t];
         const size_t n = (size_t)h.n;
@@ -977,6 +1004,9 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
     }
     if (side) {  // join the side stream (a no-op when k_stages already waited on it)
         cudaError_t r = cudaStreamWaitEvent(stream, ev_arr, 0);
+        // on any error the join may not cover the copies queued on `side`: wait for
+        // them before the scratch they write is freed
+        if (r != cudaSuccess || e != cudaSuccess || st != GL_OK) cudaStreamSynchronize(side);
         if (e == cudaSuccess) e = r;
     }
     cudaError_t ef = cudaFreeAsync(dev, stream);

@@ -92,7 +92,9 @@ __global__ void __launch_bounds__(256)
         const DCarbon cp = cpar[k];
         const double total = carbon_total(s, cp, sc);
         if (carbon_out) carbon_out[row * cols + col] = total;
-        const bool cap_ok = cp.cap_ok != 0;
+        // capacity-infeasible (R38) or invalid input (status bits, R55): never
+        // feasible, and ok = 0 / total = +inf in the fallback (R37)
+        const bool cap_ok = cp.cap_ok != 0 && s.status == 0;
         const bool feas = cap_ok && (int64_t)slo_den * s.slo_ok >= (int64_t)slo_num * s.n;
         const Cand cf{total, s.slo_ok, s.n, col};
         if (feas && better_feasible(cf, bf)) bf = cf;

@@ -869,6 +869,7 @@ __global__ void __launch_bounds__(256)
 {
     __shared__ unsigned long long s_ok[8], s_hash[8];
     const DChain &ch = chains[blockIdx.y];
+    if (stats[blockIdx.y].status != 0) return;  // invalid input: only n and status (R55)
     const int64_t n = ch.n;
     const int64_t *rows = perreq + 2 * ch.out_off;
     const int64_t ttft_slo = ch.ttft_slo, tpot_slo = ch.tpot_slo;

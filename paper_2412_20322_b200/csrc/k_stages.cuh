@@ -457,20 +457,24 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
             s[5] = max(s[5], __ldcg(&q.sums[5]));
             st |= __ldcg(&q.status);
         }
+        // a chain with invalid input (any status bit) keeps only n and its status;
+        // its decode stage is empty (M = 0) and k_finalize skips it, so every other
+        // field is 0, as in the oracle, and Alg. 1 treats it as infeasible (R55)
+        const bool valid = st == 0;
         gl_chain_stats o;
         o.n = ch.n;
         o.slo_ok = 0;
-        o.tokens = s[4];
-        o.busy_new_us = s[0];
-        o.busy_old_us = s[1];
-        o.e_new_uj = s[2];
-        o.e_old_uj = s[3];
-        o.makespan_us = s[5];
+        o.tokens = valid ? s[4] : 0;
+        o.busy_new_us = valid ? s[0] : 0;
+        o.busy_old_us = valid ? s[1] : 0;
+        o.e_new_uj = valid ? s[2] : 0;
+        o.e_old_uj = valid ? s[3] : 0;
+        o.makespan_us = valid ? s[5] : 0;
         o.req_hash = 0;
         o.status = st;
         o.capacity_ok = (uint32_t)ch.capacity_ok;
         stats[chain] = o;
-        ch.x->M = skip ? 0 : M;
+        ch.x->M = valid ? M : 0;
     }
 }
 

@@ -231,10 +231,51 @@ def test_status_bits_match_oracle():
     for i, (tr, ch) in enumerate(pairs):
         want, _, _ = O.simulate_chain(tr, ch, per_request=False)
         assert st[i]["status"] == want["status"] != 0
+        # R55: only n and the status survive; every other statistic is 0 on both sides
+        for f in INT_FIELDS:
+            assert int(st[i][f]) == int(want[f]), (i, f)
     # table errors are device-only (GL_ST_TABLE)
     bad = make_tables(4, 2, lambda p: 1, lambda p: 1, [0, 0, 3])
     st, *_ = run_gpu(grid_of([(custom_trace([0], [1], [3]), make_chain(bad))]), per_request=False)
     assert st[0]["status"] & N.ST_TABLE
+    assert all(int(st[0][f]) == 0 for f in INT_FIELDS if f not in ("n", "status", "capacity_ok"))
+
+
+def test_invalid_chains_never_feasible():
+    """R55: a chain with status bits -- a device-only table error or an
+    input violation -- is excluded from Alg. 1's feasible set like a capacity-
+    infeasible one, and its statistics are deterministic (0) whatever the scratch
+    memory held before."""
+    tr = custom_trace(np.arange(0, 4000, 40), [2] * 100, [5] * 100)
+    good = _edge_chain(cap=8)  # feasible: generous SLOs below
+    good = dataclasses.replace(good, ttft_slo_us=10**9, tpot_slo_us=10**9, ce_new_g=99999.0)
+    badtab = make_tables(8, 8, lambda p: 1, lambda p: 1, [0, 0] + [3] * 7)  # step[1] = 0
+    cheap = make_chain(badtab, MODE_DPD, 8, ttft_slo=10**9, tpot_slo=10**9, ce_new=1.0, ce_old=1.0)
+    unsorted = custom_trace(np.arange(100)[::-1].copy(), [2] * 100, [5] * 100)
+    traces = [tr, unsorted]
+    chains = [dataclasses.replace(good, trace_idx=0), dataclasses.replace(cheap, trace_idx=0),
+              dataclasses.replace(cheap, trace_idx=1, tables=_edge_chain(cap=8).tables)]
+    lt = 7 * 365 * 24 * 3600.0
+    # row 0: all three; row 1: only the two invalid chains; row 2: only the table error
+    cells = np.array([0, 1, 2, -1, 1, 2, -1, 1, -1], np.int32)
+    for prio, dcol in ((0, -1), (1, 2)):
+        g = GridSpec("invalid", traces, chains, np.array([[261.0, lt, lt]]), np.zeros(3, np.int32),
+                     cells, 3, 3, 9, 10, prio, dcol)
+        for rep in range(3):  # fill the pool with garbage between runs
+            junk = torch.full((1 << 24,), -7, dtype=torch.int64, device="cuda")
+            del junk
+            st, _, carbon, choice, fb = run_gpu(g, per_request=False)
+            assert st[1]["status"] & N.ST_TABLE and st[2]["status"] & 1
+            ref = O.evaluate_grid(g, chain_ids=[0, 2])  # (the oracle has no table check)
+            for ci in (0, 2):
+                for f in INT_FIELDS:
+                    assert int(st[ci][f]) == int(ref["stats"][ci][f]), (ci, f)
+            assert choice[0] == 0 and fb[0] == 0
+            assert fb[1] == 1 and fb[2] == 1
+            if prio == 1:
+                assert choice[1] == 2 and choice[2] == 2
+            else:  # SLO fallback: both count as ok = 0 / +inf -> the lower column
+                assert choice[1] == 1 and choice[2] == 1
 
 
 # ------------------------------------------------------------ BASELINE configs
