@@ -337,6 +337,15 @@ def evaluate_grid(grid, chain_ids=None, per_request=False):
         stats[ci] = st
         if per_request:
             per[ci] = (ttft, fin)
+    out = grid_epilogue(grid, stats)
+    out["per_request"] = per
+    return out
+
+
+def grid_epilogue(grid, stats):
+    """Carbon (Eqs. 1-3) per present cell and Alg. 1 per row from per-chain oracle
+    statistics ``stats`` = {chain: stats dict}; cells of chains not in ``stats``
+    are treated as absent."""
     rows, cols = grid.rows, grid.cols
     total = np.zeros((rows, cols))
     ok = np.zeros((rows, cols), np.int64)
@@ -360,5 +369,4 @@ def evaluate_grid(grid, chain_ids=None, per_request=False):
             cap[r, c] = 1 if (ch.capacity_ok and st["status"] == 0) else 0
     choice, fb = alg1(total, ok, n, present, cap, grid.slo_num, grid.slo_den, grid.priority,
                       grid.default_col)
-    return dict(stats=stats, per_request=per, carbon=total, choice=choice, via_fallback=fb,
-                present=present)
+    return dict(stats=stats, carbon=total, choice=choice, via_fallback=fb, present=present)
