@@ -1,6 +1,7 @@
 """Benchmark: the full config-4 grid (BASELINE.json configs[3]) per step.
 
     python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+                    [--config 4|5|7]
 
 One step = the whole hot path over the grid: gl_eval_grid on this rank's
 shard of timing chains (k_dsd_demand, k_stages, k_segments, k_decode, k_finalize), one NCCL all_gather of the
@@ -9,6 +10,10 @@ shard of timing chains (k_dsd_demand, k_stages, k_segments, k_decode, k_finalize
 write) between timed steps, outside the timed events.  Rank 0 prints one JSON
 line.  ``--impl reference`` times the CPU oracle (oracle/) on a bounded
 sample of the same workload instead (the reference arm of this tier).
+``--config 5`` times BASELINE configs[4] instead (320 chains x 1M LongBench
+requests, the configuration BASELINE states "at 1/2/4/8 GPUs"); ``--config 7``
+the HumanEval grid.  Chains are sharded over ranks in
+cost-balanced contiguous blocks.
 """
 from __future__ import annotations
 
@@ -28,8 +33,17 @@ sys.path.insert(0, ROOT)
 
 METRIC = "config×request evals/sec at 1/2/4/8 B200; % HBM roofline; speedup vs CPU oracle"
 UNIT = "config×request evals/s"
-WORKLOAD = ("cfg4: full grid, Llama-7B DPD + DSD(1B draft, gamma 4, alpha 0.8) x 4 GPU pairs "
-            "x 8 rates (0.5-8 req/s) x 64 CI x 16 lifetimes, 100k chat requests per trace")
+WORKLOADS = {
+    4: ("cfg4: full grid, Llama-7B DPD + DSD(1B draft, gamma 4, alpha 0.8) x 4 GPU pairs "
+        "x 8 rates (0.5-8 req/s) x 64 CI x 16 lifetimes, 100k chat requests per trace"),
+    5: ("cfg5: Llama-70B DSD with a 7B draft (A100 + T4), gamma 1..8 x alpha 0.5..0.9 x 8 "
+        "rates (0.5-8 req/s), 1M LongBench requests per trace"),
+    7: ("cfg7: HumanEval code requests, 7B DPD + DSD(1B, gamma 4, alpha 0.8) x 4 GPU pairs + "
+        "Standalone + SpecDecode (A100) x 8 rates (0.5-11 req/s) x 64 CI x 16 lifetimes, "
+        "100k requests per trace"),
+}
+WORKLOAD = WORKLOADS[4]
+DEFAULT_N = {4: 100_000, 5: 1_000_000, 7: 100_000}
 
 
 def parse():
@@ -38,7 +52,8 @@ def parse():
     ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
-    ap.add_argument("--n", type=int, default=100_000, help="requests per trace")
+    ap.add_argument("--config", type=int, default=4, choices=sorted(WORKLOADS))
+    ap.add_argument("--n", type=int, default=None, help="requests per trace (default: the config's)")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-analysis", action="store_true")
     ap.add_argument("--cpu-budget-s", type=float, default=15.0)
@@ -52,7 +67,12 @@ def dist_env():
     return rank, world, local
 
 
-DECODE_BYTES_PER_REQUEST = 24  # k_decode: reads r (i64) + (demand, j) (2 x u32), writes the finish (i64)
+# 16 B of input per (timing chain, request) -- arrival i64 + prompt u32
+# + output u32 -- is the path's algorithmic traffic
+BYTES_PER_CHAIN_REQUEST = 16
+# the build's own intermediate: k_decode reads the decode stream k_stages wrote (r i64 +
+# (demand, j) 2 x u32) and writes each finish time (i64) -- a secondary view
+DECODE_BYTES_PER_REQUEST = 24
 
 
 def decode_requests(grid, lo, hi):
@@ -68,17 +88,23 @@ def decode_requests(grid, lo, hi):
 
 
 def algorithmic_bytes(grid, lo, hi):
-    """Algorithmic bytes of one k_decode launch: 24 B per decode
-    request -- the decode stream k_stages wrote (r i64 + demand u32 + request index
-    u32) is read once and each finish time (i64) is written once.  The step-table
-    staging is O(cap) per chain and the speculation's scratch (helpers' finish times,
-    segment results) is not algorithmic."""
+    """SURVEY §8(d)'s algorithmic bytes of one launch over chains [lo, hi): 16 B per
+    (timing chain, request) -- the request's arrival (i64), prompt and output
+    lengths (2 x u32); tables amortise to < 1 B/request and CI x lifetime scenarios
+    add 0 B per request."""
+    return BYTES_PER_CHAIN_REQUEST * sum(grid.traces[c.trace_idx].n for c in grid.chains[lo:hi])
+
+
+def stream_bytes(grid, lo, hi):
+    """The build's decode-stream view: 24 B per decode request read
+    and written by k_decode."""
     return DECODE_BYTES_PER_REQUEST * sum(decode_requests(grid, lo, hi))
 
 
-def shard_bounds(n_chains, world):
-    from paper_2412_20322_b200.dist import shard_bounds as sb
-    return sb(n_chains, world)
+def shard_bounds(grid, world):
+    """Cost-balanced contiguous blocks of chains, N (1 + w_DSD) per chain."""
+    from paper_2412_20322_b200.dist import chain_costs, shard_bounds_cost
+    return shard_bounds_cost(chain_costs(grid), world)
 
 
 # --------------------------------------------------------------- clocks sampler
@@ -166,7 +192,6 @@ def _oracle_chain_worker(args):
     """One whole chain through the oracle in a worker process (all-cores baseline)."""
     cfg, n, ci = args
     from oracle import oracle as O
-    from paper_2412_20322_b200.inputs import build_config
     g = _worker_grid(cfg, n)
     ch = g.chains[ci]
     t0 = time.perf_counter()
@@ -184,24 +209,37 @@ def _worker_grid(cfg, n):
     return _WORKER_GRID[(cfg, n)]
 
 
-def cpu_baseline_all_cores(grid, n):
+def host_cores():
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline_all_cores(grid, cfg, n, max_rounds=2):
     """The same single-threaded oracle, one chain per process across every host core
     (per-core rate, aggregate, nproc).  Timing chains only (the
-    carbon/Alg. 1 epilogue is < 1% of the oracle's time); wall clock of the pool."""
+    carbon/Alg. 1 epilogue is < 1% of the oracle's time); wall clock of the pool.
+    A bounded sample (at most ``max_rounds`` chains per core, spread over the grid)
+    when the workload has more chains than that (config 5: ~5 s per chain)."""
     import multiprocessing as mp
-    cores = os.cpu_count() or 1
-    jobs = [(4, n, ci) for ci in range(len(grid.chains))]
+    cores = host_cores()
+    all_ids = list(range(len(grid.chains)))
+    k = min(len(all_ids), max_rounds * cores)
+    ids = all_ids[::max(1, len(all_ids) // k)][:k]
+    jobs = [(cfg, n, ci) for ci in ids]
+    procs = min(cores, len(jobs))
     ctx = mp.get_context("fork")
-    with ctx.Pool(min(cores, len(jobs)), initializer=_worker_grid, initargs=(4, n)) as pool:
-        pool.map(_oracle_chain_worker, jobs[:min(cores, len(jobs))])  # warm the workers
+    with ctx.Pool(procs, initializer=_worker_grid, initargs=(cfg, n)) as pool:
         t0 = time.perf_counter()
-        per = pool.map(_oracle_chain_worker, jobs)
+        per = pool.map(_oracle_chain_worker, jobs, chunksize=1)
         wall = time.perf_counter() - t0
     reqs = grid.traces[0].n
-    cells = int((grid.cell_chain >= 0).sum())
-    return {"value": cells * reqs / wall, "unit": UNIT, "cores": min(cores, len(jobs)),
-            "kind": "oracle", "sample": f"all {len(jobs)} timing chains x {reqs} requests, one "
-            f"process per chain on {min(cores, len(jobs))} of {cores} host cores, {wall:.1f} s wall",
+    cells = int(np.isin(grid.cell_chain, ids).sum())
+    return {"value": cells * reqs / wall, "unit": UNIT, "cores": procs,
+            "kind": "oracle", "sample": f"{len(jobs)} of {len(all_ids)} timing chains x {reqs} "
+            f"requests (all {cells} of their grid cells), one process per chain on {procs} of "
+            f"{cores} host cores, {wall:.1f} s wall",
             "chain_request_sims_per_s": len(jobs) * reqs / wall,
             "per_core_chain_request_sims_per_s": reqs / (sum(per) / len(per))}
 
@@ -218,8 +256,8 @@ def run_reference(args):
     from oracle import oracle as O
     from paper_2412_20322_b200.inputs import build_config
     O.lib()
-    grid = build_config(4, n=args.n)
-    per_step_chains = 2
+    grid = build_config(args.config, n=args.n)
+    per_step_chains = 1 if args.config == 5 else 2  # a config-5 chain is ~5 s of oracle
     times, evals = [], []
     for step in range(args.warmup + args.steps):
         ids = [(step * per_step_chains + k) % len(grid.chains) for k in range(per_step_chains)]
@@ -231,17 +269,32 @@ def run_reference(args):
             times.append(dt)
             evals.append(int(ref["present"].sum()) * grid.traces[0].n)
     value = sum(evals) / sum(times)
+    cells_per_chain = grid.grid_points // len(grid.chains)
     out = {"impl": "reference", "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world,
            "steps": args.steps, "warmup": args.warmup,
            "ms_per_step": 1e3 * sum(times) / len(times), "higher_is_better": True,
            "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-           "config": {"workload": WORKLOAD, "sample": f"{per_step_chains} timing chains "
-                      "(each 100k requests, all 1,024 of its grid cells) per step, rotating"},
+           "config": {"workload": WORKLOADS[args.config],
+                      "sample": f"{per_step_chains} timing chain(s) (each {grid.traces[0].n} "
+                      f"requests, all {cells_per_chain} of its grid cells) per step, rotating"},
            "cpu_baseline": {"value": value, "unit": UNIT, "cores": 1, "kind": "oracle",
-                            "sample": f"{per_step_chains} of 64 chains per step"},
+                            "sample": f"{per_step_chains} of {len(grid.chains)} chains per step"},
            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(out))
     return 0
+
+
+def load_profile_json(name, cfg):
+    """A committed ncu summary under profiles/: the entry for this config
+    ("cfg5": {...}) or, for config 4, the top-level fields."""
+    path = os.path.join(ROOT, "profiles", name)
+    try:
+        pj = json.load(open(path))
+    except (OSError, ValueError):
+        return {}
+    if f"cfg{cfg}" in pj:
+        return pj[f"cfg{cfg}"]
+    return pj if cfg == 4 else {}
 
 
 # --------------------------------------------------------------------- ours
@@ -261,9 +314,9 @@ def run_ours(args):
     else:
         torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    grid = build_config(4, n=args.n)
+    grid = build_config(args.config, n=args.n)
     dg = api.DeviceGrid(grid, dev)
-    bounds = shard_bounds(dg.n_chains, world)
+    bounds = shard_bounds(grid, world)
     lo, hi = bounds[rank]
     max_shard = max(h - l for l, h in bounds)
     local_stats = torch.zeros((max_shard, 80), dtype=torch.uint8, device=dev)
@@ -350,7 +403,7 @@ def run_ours(args):
         e2e = e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush, dev)
 
     analysis = None
-    if world == 1 and not args.no_analysis:
+    if world == 1 and not args.no_analysis and args.config == 4:
         analysis = {"link_demand": link_demand_bench(dg, grid, flush),
                     **analysis_bench(dg, grid)}
 
@@ -363,26 +416,24 @@ def run_ours(args):
     evals = grid.grid_points * reqs
     value = evals / (ms_per_step / 1e3)
     chain_req = dg.chain_n.sum() / (ms_per_step / 1e3)
-    kdec = kt.get("k_decode", [])
+    kname = "k_decode" if "k_decode" in kt else max(kt, key=lambda k: sum(kt[k]), default="k_decode")
+    kdec = kt.get(kname, [])
     kdec_ms = sum(kdec) / max(1, len(kdec))
     peaks = {}
     try:
         peaks = json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))
     except OSError:
         pass
-    hbm_peak = peaks.get("hbm_gbs", 6650.0)
+    hbm_peak = peaks.get("hbm_gbs")
+    peak_src = "MEASURED_PEAKS.json hbm_gbs (burst copy bandwidth)"
+    if hbm_peak is None:
+        hbm_peak, peak_src = 7700.0, "B200_PROFILING.md fallback (no MEASURED_PEAKS.json)"
     alg_bytes = algorithmic_bytes(grid, lo, hi)
     achieved = alg_bytes / (kdec_ms / 1e3) / 1e9 if kdec_ms > 0 else 0.0
-    traffic = None
-    winst = None
-    prof_path = os.path.join(ROOT, "profiles", "k_decode_dram_bytes.json")
-    if os.path.exists(prof_path):
-        try:
-            pj = json.load(open(prof_path))
-            traffic = pj.get("dram_bytes_per_launch")
-            winst = pj.get("warp_inst_per_launch")
-        except (OSError, ValueError):
-            traffic = None
+    sbytes = stream_bytes(grid, lo, hi)
+    prof = load_profile_json("k_decode_dram_bytes.json", args.config)
+    traffic = prof.get("dram_bytes_per_launch")
+    winst = prof.get("warp_inst_per_launch")
     step_total = {k: sum(v) / max(1, len(v)) for k, v in kt.items()}
     cpu = None
     if not args.no_cpu_baseline:
@@ -393,41 +444,46 @@ def run_ours(args):
                          f"{cb['seconds']:.1f} s",
                "chain_request_sims_per_s": cb["chain_request_sims_per_s"]}
         try:
-            cpu["all_cores"] = cpu_baseline_all_cores(grid, args.n)
+            cpu["all_cores"] = cpu_baseline_all_cores(grid, args.config, args.n)
         except Exception as exc:  # a host without fork / enough memory: report why
             cpu["all_cores"] = {"unavailable": repr(exc)[:200]}
     clocks = sampler.summary(t_wall0, t_wall1)
-    # cycles per decode event on the critical path.  Every
-    # decode request is one join and one leave event; the launch lasts as long as
-    # its slowest chain, so this is an upper bound for that chain.
-    m_max = max(decode_requests(grid, lo, hi) or [0])
     sm_mhz = (clocks or {}).get("sm_mhz") or 1965.0
-    latency = {"max_decode_requests_per_chain": m_max, "events_per_chain": 2 * m_max,
-               "cycles_per_event_bound": (kdec_ms * 1e-3 * sm_mhz * 1e6 / (2 * m_max)) if m_max
-               else None, "sm_mhz": sm_mhz}
+    latency = latency_view(grid, lo, hi, kdec_ms, sm_mhz, args.config)
     out = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
         "scaling": "strong", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
-        "config": {"workload": WORKLOAD, "grid_points": grid.grid_points,
+        "config": {"workload": WORKLOADS[args.config], "grid_points": grid.grid_points,
                    "timing_chains": len(grid.chains), "requests_per_trace": reqs,
                    "l2": "flushed between timed steps (512 MiB device write, outside the events)",
-                   "parallelism": f"chains sharded over {world} GPU(s), one NCCL all_gather of "
-                                  "80-B chain stats" if world > 1 else "1 GPU",
+                   "parallelism": f"chains sharded over {world} GPU(s) in cost-balanced "
+                                  "contiguous blocks, one NCCL all_gather of 80-B chain stats"
+                                  if world > 1 else "1 GPU",
                    "grid_point_factorisation": "each timing chain is simulated once and scores "
-                                               "its 1,024 CI x lifetime cells (SURVEY F2)"},
+                                               f"its {grid.grid_points // len(grid.chains)} grid "
+                                               "cells (CI x lifetime rows share it; SURVEY F2)"},
         "chain_request_sims_per_s": chain_req,
         "kernel_ms_per_step": step_total,
-        "roofline": {"bound": "hbm", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic,
-                     "kernel": "k_decode", "algorithmic_bytes_per_launch": alg_bytes,
-                     "bytes_per_unit": DECODE_BYTES_PER_REQUEST, "unit_name": "decode request",
+        "roofline": {"bound": "latency", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
+                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                     "kernel": kname, "algorithmic_bytes_per_launch": alg_bytes,
+                     "bytes_per_unit": BYTES_PER_CHAIN_REQUEST,
+                     "unit_name": "(timing chain, request): arrival i64 + prompt u32 + output u32 "
+                                  "(SURVEY §8(d))",
+                     "units_per_launch": alg_bytes // BYTES_PER_CHAIN_REQUEST,
                      "kernel_ms": kdec_ms,
+                     "stream_view": {"bytes_per_decode_request": DECODE_BYTES_PER_REQUEST,
+                                     "bytes_per_launch": sbytes,
+                                     "achieved_gbs": sbytes / (kdec_ms / 1e3) / 1e9 if kdec_ms else 0.0,
+                                     "note": "the decode stream k_stages writes and k_decode reads "
+                                             "(r, demand, index) plus the finish times written"},
                      "latency": latency,
                      "alu_view": alu_view(winst, kdec_ms, sm_mhz, grid, lo, hi),
-                     "note": "k_decode is bound by the dependent latency of the slowest chain's "
-                             "serial decode event loop (busy periods cannot be split exactly), "
-                             "not by HBM (DESIGN.md §5)"},
+                     "note": "bound = latency: k_decode runs one serial event loop per timing "
+                             "chain (a busy period cannot be split exactly), so the step lasts as "
+                             "long as the slowest chain's dependent chain of events; HBM and the "
+                             "issue rate are both far from saturated (DESIGN.md §4)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,
@@ -438,6 +494,29 @@ def run_ours(args):
     if world > 1:
         dist.destroy_process_group()
     return 0
+
+
+def latency_view(grid, lo, hi, kernel_ms, sm_mhz, cfg):
+    """The latency roofline of k_decode.  Every decode request
+    is one join and one leave event of its chain's serial loop; the launch lasts as
+    long as its slowest chain, so the achieved cycles per event of the critical
+    chain are at most kernel cycles / (2 x its decode requests).  The floor is the
+    loop's minimal dependent-instruction cycles per event from the committed
+    analysis (profiles/k_decode_latency.json: measured instruction latencies,
+    scripts/ubench/lat.cu, along the SASS of the loop body); frac = floor / achieved."""
+    m_max = max(decode_requests(grid, lo, hi) or [0])
+    achieved = (kernel_ms * 1e-3 * sm_mhz * 1e6 / (2 * m_max)) if m_max and kernel_ms else None
+    lat = load_profile_json("k_decode_latency.json", 4)
+    floor = lat.get("min_cycles_per_event")
+    out = {"max_decode_requests_per_chain": m_max, "events_per_chain": 2 * m_max,
+           "cycles_per_event": achieved, "sm_mhz": sm_mhz,
+           "min_cycles_per_event": floor,
+           "frac": (floor / achieved) if (floor and achieved) else None,
+           "floor_source": lat.get("source")}
+    crit = lat.get("critical_chain", {}).get(f"cfg{cfg}")
+    if crit:
+        out["critical_chain"] = crit
+    return out
 
 
 def alu_view(warp_inst, kernel_ms, sm_mhz, grid, lo, hi):
@@ -582,7 +661,7 @@ def analysis_bench(dg, grid, reps=3):
     cf_ms = timed(lambda: api.complete_matrices(x, mm, 2, 0.1, 200, lo=0.0))
     # the other BASELINE configurations, one device-timed step each (inputs resident)
     others = {}
-    for k in (1, 2, 3, 5):
+    for k in (1, 2, 3, 5, 7):
         gk = build_config(k)
         dk = api.DeviceGrid(gk, dg.device)
         sk, _ = api.eval_grid(dk)
@@ -617,8 +696,11 @@ def api_pairs(g):
 
 
 def e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush, dev):
-    """N > 1: each rank copies its shard's traces from pinned host memory, runs
-    its chains, all_gathers stats, runs Alg. 1 and reads the choices back."""
+    """N > 1, end to end per rank: pinned host -> device copies of its shard's traces
+    (each distinct host array once), gl_eval_grid ON THOSE COPIES, the NCCL
+    all_gather of the 80-B records, gl_argmin_feasible on every row, and the
+    device -> host read of the choices; CUDA events on the launching stream, max
+    over ranks."""
     import torch
     import torch.distributed as dist
 
@@ -626,25 +708,33 @@ def e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush
     from paper_2412_20322_b200.dist import all_gather_stats
     host = dg.pinned_traces()
     needed = sorted({grid.chains[c].trace_idx for c in range(lo, hi)})
-    dev_tr = {t: tuple(torch.empty_like(x, device=dev) for x in host[t]) for t in needed}
+    dev_of = {}  # one device buffer per distinct host array
+    for t in needed:
+        for x in host[t]:
+            if x.data_ptr() not in dev_of:
+                dev_of[x.data_ptr()] = (x, torch.empty_like(x, device=dev))
+    # the shard's traces point at the copies; traces outside the shard are never read
+    traces = [tuple(dev_of[x.data_ptr()][1] for x in host[t]) if t in needed
+              else dg.trace_tensors[t] for t in range(len(grid.traces))]
     stream = torch.cuda.current_stream()
-    times = []
-    h2d = sum(x.numel() * x.element_size() for t in needed for x in host[t])
-    d2h = 0
+    h2d = sum(h.numel() * h.element_size() for h, _ in dev_of.values())
+    times, d2h = [], 0
+    c_h = torch.empty(grid.rows, dtype=torch.int32, pin_memory=True)
+    f_h = torch.empty(grid.rows, dtype=torch.uint8, pin_memory=True)
     for i in range(args.warmup + max(3, args.steps // 2)):
         flush.fill_(i & 0xFF)
         dist.barrier()
         torch.cuda.synchronize()
         e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
         e0.record(stream)
-        for t in needed:
-            for d, h in zip(dev_tr[t], host[t]):
-                d.copy_(h, non_blocking=True)
+        for h, d in dev_of.values():
+            d.copy_(h, non_blocking=True)
         if hi > lo:
-            api.eval_grid(dg, lo, hi, stats=local_stats[: hi - lo])
+            api.eval_grid(dg, lo, hi, stats=local_stats[: hi - lo], traces=traces)
         full = all_gather_stats(local_stats, gathered, bounds, dg.n_chains)
         _, choice, fb = api.argmin_feasible(dg, full, want_carbon=False)
-        c_h, f_h = choice.cpu(), fb.cpu()
+        c_h.copy_(choice, non_blocking=True)
+        f_h.copy_(fb, non_blocking=True)
         e1.record(stream)
         torch.cuda.synchronize()
         d2h = c_h.numel() * 4 + f_h.numel()
@@ -655,14 +745,16 @@ def e2e_distributed(args, dg, grid, bounds, lo, hi, local_stats, gathered, flush
     ms = float(t.item())
     return {"value": grid.grid_points * grid.traces[0].n / (ms / 1e3), "unit": UNIT,
             "ms_per_step": ms, "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-            "path": "per rank: pinned H2D of its shard's traces, gl_eval_grid, NCCL all_gather, "
-                    "gl_argmin_feasible, D2H of choices"}
+            "path": "per rank: pinned H2D of its shard's traces, gl_eval_grid on the copies, "
+                    "NCCL all_gather, gl_argmin_feasible, D2H of choices (max over ranks)"}
 
 
 def main():
     args = parse()
     if args.warmup < 3:
         args.warmup = 3
+    if args.n is None:
+        args.n = DEFAULT_N[args.config]
     if args.impl == "reference":
         return run_reference(args)
     return run_ours(args)

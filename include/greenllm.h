@@ -36,7 +36,8 @@
  *  - Errors: invalid host-visible arguments return a gl_status synchronously
  *    and launch nothing.  Data-dependent violations found on the device are
  *    reported per chain in gl_chain_stats.status (GL_ST_* bits); the chain's
- *    other statistics are then unspecified.
+ *    other statistics are then 0 (n and status kept; R55) and Alg. 1 never
+ *    selects it as feasible.
  */
 #ifndef GREENLLM_H
 #define GREENLLM_H
@@ -47,7 +48,7 @@
 extern "C" {
 #endif
 
-#define GL_VERSION 1
+#define GL_VERSION 2  /* 2: carbon_per_token_out in gl_argmin_feasible */
 #define GL_MAX_CAP 256        /* batch cap: 8 active-set slots per lane x 32 lanes */
 #define GL_MAX_GAMMA 16       /* DSD draft length */
 #define GL_MAX_PROMPT 16384   /* prompt-indexed tables live in shared memory */
@@ -188,17 +189,25 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
  * is feasible via_fallback = 1 and: priority SLO -> argmax attainment (capacity-
  * infeasible cells count as 0 and +inf), ties -> lower total -> lower column,
  * -1 if the row has no present cell; priority DEFAULT -> default_col.
+ * A chain with status bits (invalid input) is never feasible and counts like a
+ * capacity-infeasible one (R55).
  *   stats            DEVICE [n_chains] (all chains, e.g. after an allgather)
  *   chains           HOST [n_chains] (ce_new_g, ce_old_g, capacity_ok are read)
  *   scen             HOST [n_scen];  grid: HOST arrays
  *   carbon_out       DEVICE double [rows*cols] (absent cells: NaN) or NULL
+ *   carbon_per_token_out  DEVICE double [rows*cols] or NULL: the paper's reported
+ *                    metric, gCO2 per token (R33) = total / (double)tokens
+ *                    (one IEEE division after the total; absent cells NaN).  A
+ *                    row's cells share one trace, hence one token count, so the
+ *                    argmin over totals is the argmin over per-token carbon.
  *   choice_out       DEVICE int32 [rows];  via_fallback_out DEVICE uint8 [rows]
  */
 gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains,
                              const gl_chain *chains, const gl_scenario *scen, int32_t n_scen,
                              const gl_grid *grid, int32_t slo_num, int32_t slo_den,
                              int32_t priority, int32_t default_col, double *carbon_out,
-                             int32_t *choice_out, uint8_t *via_fallback_out, void *stream);
+                             double *carbon_per_token_out, int32_t *choice_out,
+                             uint8_t *via_fallback_out, void *stream);
 
 /*
  * End to end from host buffers: copies the traces host->device (each distinct
@@ -210,6 +219,7 @@ gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains,
  *   host_traces      HOST descriptors with HOST data pointers
  *   chains           as for gl_eval_grid (tables stay in DEVICE memory)
  *   stats_host       HOST [n_chains];  carbon_host HOST [rows*cols] or NULL
+ *   carbon_per_token_host  HOST [rows*cols] or NULL (as gl_argmin_feasible's)
  *   choice_host      HOST [rows];      via_fallback_host HOST [rows]
  */
 gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces,
@@ -217,7 +227,8 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces,
                            int32_t n_scen, const gl_grid *grid, int32_t slo_num,
                            int32_t slo_den, int32_t priority, int32_t default_col,
                            gl_chain_stats *stats_host, double *carbon_host,
-                           int32_t *choice_host, uint8_t *via_fallback_host, void *stream);
+                           double *carbon_per_token_host, int32_t *choice_host,
+                           uint8_t *via_fallback_host, void *stream);
 
 /* ---- Link bandwidth demand (Fig. 4, "bandwidth
  * requirement"; "peak bandwidth demand over a 1 s sliding window").

@@ -379,6 +379,15 @@ void oracle_carbon(const or_stats *st, double ce_new_g, double ce_old_g, double 
     out[2] = op + emb;
 }
 
+/* Carbon per token (§6 "Carbon Per Token: gCO2 of carbon emission per
+ * token"; R33): the chain's Eq. 3 total over the tokens it generated, sum of o_j
+ * (every output token, prefill's first included, R7).  0 tokens (a chain whose
+ * statistics are void, R55) gives total/0 by IEEE rules. */
+double oracle_carbon_per_token(const or_stats *st, double total)
+{
+    return total / (double)st->tokens;
+}
+
 /*
  * §5 carbon-efficiency analysis for one
  * (Case 2 = disaggregated chain d, Case 1 = Standalone chain s) pair under one

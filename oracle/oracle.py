@@ -93,6 +93,8 @@ def lib():
             L.oracle_carbon.restype = None
             L.oracle_carbon.argtypes = [C.POINTER(OrStats), C.c_double, C.c_double, C.c_double,
                                         C.c_double, C.c_double, C.POINTER(C.c_double)]
+            L.oracle_carbon_per_token.restype = C.c_double
+            L.oracle_carbon_per_token.argtypes = [C.POINTER(OrStats), C.c_double]
             L.oracle_savings.restype = None
             L.oracle_savings.argtypes = [C.POINTER(OrStats), C.c_double, C.c_double,
                                          C.POINTER(OrStats), C.c_double, C.c_double,
@@ -218,6 +220,11 @@ def carbon(stats: dict, ce_new_g: float, ce_old_g: float, ci: float, lt_new_s: f
     lib().oracle_carbon(C.byref(_stats_struct(stats)), ce_new_g, ce_old_g, ci, lt_new_s,
                         lt_old_s, out)
     return out[0], out[1], out[2]
+
+
+def carbon_per_token(stats: dict, total: float) -> float:
+    """gCO2 per generated token (R33): total / tokens."""
+    return lib().oracle_carbon_per_token(C.byref(_stats_struct(stats)), float(total))
 
 
 def savings(stats_d: dict, ce_d, stats_s: dict, ce_s, ci: float, lt_new_s: float,
@@ -348,6 +355,7 @@ def grid_epilogue(grid, stats):
     are treated as absent."""
     rows, cols = grid.rows, grid.cols
     total = np.zeros((rows, cols))
+    per_token = np.zeros((rows, cols))
     ok = np.zeros((rows, cols), np.int64)
     n = np.ones((rows, cols), np.int64)
     present = np.zeros((rows, cols), np.uint8)
@@ -362,6 +370,7 @@ def grid_epilogue(grid, stats):
             ch = grid.chains[k]
             st = stats[k]
             total[r, c] = carbon(st, ch.ce_new_g, ch.ce_old_g, sc[0], sc[1], sc[2])[2]
+            per_token[r, c] = carbon_per_token(st, total[r, c])
             ok[r, c], n[r, c] = st["slo_ok"], st["n"]
             present[r, c] = 1
             # R55: a chain with invalid input (status bits) is never feasible; like a
@@ -369,4 +378,5 @@ def grid_epilogue(grid, stats):
             cap[r, c] = 1 if (ch.capacity_ok and st["status"] == 0) else 0
     choice, fb = alg1(total, ok, n, present, cap, grid.slo_num, grid.slo_den, grid.priority,
                       grid.default_col)
-    return dict(stats=stats, carbon=total, choice=choice, via_fallback=fb, present=present)
+    return dict(stats=stats, carbon=total, carbon_per_token=per_token, choice=choice,
+                via_fallback=fb, present=present)

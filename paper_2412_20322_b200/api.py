@@ -103,9 +103,11 @@ def _stream_ptr(stream) -> int:
 
 
 def eval_grid(dg: DeviceGrid, chain_lo: int = 0, chain_hi: int | None = None, stats=None,
-              per_request: bool = False, stream=None):
+              per_request: bool = False, stream=None, traces=None):
     """Simulate chains [chain_lo, chain_hi) -> (stats uint8 tensor [k, 80], per-request
-    int64 tensor [sum n, 2] or None).  ``stats`` may be a preallocated view."""
+    int64 tensor [sum n, 2] or None).  ``stats`` may be a preallocated view.
+    ``traces`` = [(arrival, prompt, output) device tensors] per trace replaces the
+    grid's resident copies (e.g. buffers just copied from the host)."""
     hi = dg.n_chains if chain_hi is None else chain_hi
     chains = dg.chain_arr(chain_lo, hi)
     k = len(chains)
@@ -115,7 +117,16 @@ def eval_grid(dg: DeviceGrid, chain_lo: int = 0, chain_hi: int | None = None, st
     if per_request:
         tot = int(dg.chain_n[chain_lo:hi].sum())
         pr = torch.empty((tot, 2), dtype=torch.int64, device=dg.device)
-    dg.last_launches = N.eval_grid(dg.trace_arr(), chains, stats.data_ptr(),
+    if traces is None:
+        tr = dg.trace_arr()
+    else:
+        assert len(traces) == len(dg.gl_traces)
+        for (a, p, o), g in zip(traces, dg.gl_traces):
+            assert a.numel() == g.n and p.numel() == g.n and o.numel() == g.n
+            assert a.is_cuda and p.is_cuda and o.is_cuda
+        tr = [N.GlTrace(a.data_ptr(), p.data_ptr(), o.data_ptr(), a.numel())
+              for (a, p, o) in traces]
+    dg.last_launches = N.eval_grid(tr, chains, stats.data_ptr(),
                                    pr.data_ptr() if pr is not None else None, _stream_ptr(stream))
     return stats, pr
 
@@ -209,19 +220,25 @@ def link_numpy(link: torch.Tensor) -> np.ndarray:
     return link.detach().cpu().numpy().view(N.LINK_DTYPE).reshape(-1)
 
 
-def argmin_feasible(dg: DeviceGrid, stats: torch.Tensor, want_carbon: bool = True, stream=None):
+def argmin_feasible(dg: DeviceGrid, stats: torch.Tensor, want_carbon: bool = True, stream=None,
+                    per_token_out: torch.Tensor | None = None):
     """Alg. 1 over the grid -> (carbon f64 [rows, cols] or None, choice int32 [rows],
-    via_fallback uint8 [rows]) as device tensors."""
+    via_fallback uint8 [rows]) as device tensors.  ``per_token_out`` (f64 [rows,
+    cols], device), when given, receives the carbon per token."""
     g = dg.grid
     carbon = torch.empty((g.rows, g.cols), dtype=torch.float64, device=dg.device) \
         if want_carbon else None
     choice = torch.empty(g.rows, dtype=torch.int32, device=dg.device)
     fb = torch.empty(g.rows, dtype=torch.uint8, device=dg.device)
+    if per_token_out is not None:
+        assert per_token_out.dtype == torch.float64 and per_token_out.is_contiguous()
+        assert per_token_out.numel() == g.rows * g.cols
     dg.last_launches = N.argmin_feasible(
         stats.data_ptr(), dg.chain_arr(), g.scenarios, g.rows, g.cols, g.row_scenario,
         g.cell_chain, g.slo_num, g.slo_den, g.priority, g.default_col,
         carbon.data_ptr() if carbon is not None else None, choice.data_ptr(), fb.data_ptr(),
-        _stream_ptr(stream))
+        _stream_ptr(stream),
+        per_token_ptr=per_token_out.data_ptr() if per_token_out is not None else None)
     return carbon, choice, fb
 
 
@@ -234,10 +251,11 @@ class HostResult:
     launches: int
     h2d_bytes: int
     d2h_bytes: int
+    carbon_per_token: np.ndarray | None = None
 
 
 def evaluate_host(dg: DeviceGrid, host_traces, want_carbon: bool = False, stream=None,
-                  out: HostResult | None = None) -> HostResult:
+                  out: HostResult | None = None, want_per_token: bool = False) -> HostResult:
     """End to end through gl_evaluate_host: pinned host traces in, host results out."""
     g = dg.grid
     gl_tr = [N.GlTrace(a.data_ptr(), p.data_ptr(), o.data_ptr(), a.shape[0])
@@ -248,11 +266,14 @@ def evaluate_host(dg: DeviceGrid, host_traces, want_carbon: bool = False, stream
         out = HostResult(pinned(dg.n_chains * N.STATS_DTYPE.itemsize).view(N.STATS_DTYPE),
                          pinned(g.rows * g.cols * 8).view(np.float64).reshape(g.rows, g.cols)
                          if want_carbon else None,
-                         pinned(g.rows * 4).view(np.int32), pinned(g.rows), 0, 0, 0)
+                         pinned(g.rows * 4).view(np.int32), pinned(g.rows), 0, 0, 0,
+                         pinned(g.rows * g.cols * 8).view(np.float64).reshape(g.rows, g.cols)
+                         if want_per_token else None)
     out.launches = N.evaluate_host(gl_tr, dg.chain_arr(), g.scenarios, g.rows, g.cols,
                                    g.row_scenario, g.cell_chain, g.slo_num, g.slo_den, g.priority,
                                    g.default_col, out.stats, out.carbon, out.choice,
-                                   out.via_fallback, _stream_ptr(stream))
+                                   out.via_fallback, _stream_ptr(stream),
+                                   per_token_out=out.carbon_per_token)
     seen = set()
     h2d = 0
     for arrs in host_traces:
@@ -263,6 +284,7 @@ def evaluate_host(dg: DeviceGrid, host_traces, want_carbon: bool = False, stream
                 h2d += key[1]
     out.h2d_bytes = h2d
     out.d2h_bytes = out.stats.nbytes + (out.carbon.nbytes if out.carbon is not None else 0) + \
+        (out.carbon_per_token.nbytes if out.carbon_per_token is not None else 0) + \
         out.choice.nbytes + out.via_fallback.nbytes
     return out
 

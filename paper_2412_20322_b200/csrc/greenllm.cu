@@ -633,8 +633,8 @@ gl_status gl_link_demand(const gl_trace *traces, int32_t n_traces, const gl_chai
 gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains, const gl_chain *chains,
                              const gl_scenario *scen, int32_t n_scen, const gl_grid *grid,
                              int32_t slo_num, int32_t slo_den, int32_t priority,
-                             int32_t default_col, double *carbon_out, int32_t *choice_out,
-                             uint8_t *via_fallback_out, void *stream_)
+                             int32_t default_col, double *carbon_out, double *per_token_out,
+                             int32_t *choice_out, uint8_t *via_fallback_out, void *stream_)
 {
     g_last_launches = 0;
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
@@ -694,7 +694,8 @@ gl_status gl_argmin_feasible(const gl_chain_stats *stats, int32_t n_chains, cons
             reinterpret_cast<const gl_scenario *>(scratch + o_scen),
             reinterpret_cast<const int32_t *>(scratch + o_rows),
             reinterpret_cast<const int32_t *>(scratch + o_cells), (int32_t)rows, (int32_t)cols,
-            slo_num, slo_den, priority, default_col, carbon_out, choice_out, via_fallback_out);
+            slo_num, slo_den, priority, default_col, carbon_out, per_token_out, choice_out,
+            via_fallback_out);
         e = cudaGetLastError();
         prof_end(stream);
     }
@@ -902,8 +903,8 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
                            int32_t n_chains, const gl_scenario *scen, int32_t n_scen,
                            const gl_grid *grid, int32_t slo_num, int32_t slo_den,
                            int32_t priority, int32_t default_col, gl_chain_stats *stats_host,
-                           double *carbon_host, int32_t *choice_host, uint8_t *via_fallback_host,
-                           void *stream_)
+                           double *carbon_host, double *per_token_host, int32_t *choice_host,
+                           uint8_t *via_fallback_host, void *stream_)
 {
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     gl_status st = validate_traces(host_traces, n_traces);
@@ -937,6 +938,8 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
     total += align256(sizeof(gl_chain_stats) * n_chains);
     const size_t o_carbon = total;
     total += carbon_host ? align256(sizeof(double) * rows * cols) : 0;
+    const size_t o_ptok = total;
+    total += per_token_host ? align256(sizeof(double) * rows * cols) : 0;
     const size_t o_choice = total;
     total += align256(sizeof(int32_t) * rows);
     const size_t o_fb = total;
@@ -984,6 +987,7 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
             st = gl_argmin_feasible(dstats, n_chains, chains, scen, n_scen, grid, slo_num, slo_den,
                                     priority, default_col,
                                     carbon_host ? reinterpret_cast<double *>(dev + o_carbon) : nullptr,
+                                    per_token_host ? reinterpret_cast<double *>(dev + o_ptok) : nullptr,
                                     reinterpret_cast<int32_t *>(dev + o_choice),
                                     reinterpret_cast<uint8_t *>(dev + o_fb), stream_);
             launches += g_last_launches;
@@ -993,6 +997,9 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
                                 cudaMemcpyDeviceToHost, stream);
             if (e == cudaSuccess && carbon_host)
                 e = cudaMemcpyAsync(carbon_host, dev + o_carbon, sizeof(double) * rows * cols,
+                                    cudaMemcpyDeviceToHost, stream);
+            if (e == cudaSuccess && per_token_host)
+                e = cudaMemcpyAsync(per_token_host, dev + o_ptok, sizeof(double) * rows * cols,
                                     cudaMemcpyDeviceToHost, stream);
             if (e == cudaSuccess)
                 e = cudaMemcpyAsync(choice_host, dev + o_choice, sizeof(int32_t) * rows,

@@ -74,7 +74,8 @@ __global__ void __launch_bounds__(256)
              const gl_scenario *__restrict__ scen, const int32_t *__restrict__ row_scen,
              const int32_t *__restrict__ cells, int32_t rows, int32_t cols, int32_t slo_num,
              int32_t slo_den, int32_t priority, int32_t default_col, double *__restrict__ carbon_out,
-             int32_t *__restrict__ choice_out, uint8_t *__restrict__ fb_out)
+             double *__restrict__ per_token_out, int32_t *__restrict__ choice_out,
+             uint8_t *__restrict__ fb_out)
 {
     const int lane = threadIdx.x & 31;
     const int64_t row = (int64_t)blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32;
@@ -85,13 +86,17 @@ __global__ void __launch_bounds__(256)
     for (int col = lane; col < cols; col += 32) {
         const int32_t k = cells[row * cols + col];
         if (k < 0) {
-            if (carbon_out) carbon_out[row * cols + col] = __longlong_as_double(0x7ff8000000000000ll);
+            const double nan = __longlong_as_double(0x7ff8000000000000ll);
+            if (carbon_out) carbon_out[row * cols + col] = nan;
+            if (per_token_out) per_token_out[row * cols + col] = nan;
             continue;
         }
         const gl_chain_stats s = stats[k];
         const DCarbon cp = cpar[k];
         const double total = carbon_total(s, cp, sc);
         if (carbon_out) carbon_out[row * cols + col] = total;
+        // carbon per token (R33): one IEEE division after the total
+        if (per_token_out) per_token_out[row * cols + col] = __ddiv_rn(total, (double)s.tokens);
         // capacity-infeasible (R38) or invalid input (status bits, R55): never
         // feasible, and ok = 0 / total = +inf in the fallback (R37)
         const bool cap_ok = cp.cap_ok != 0 && s.status == 0;

@@ -20,7 +20,7 @@ import numpy as np
 
 from .tables import (GPUS, ChainTables, capacity_ok, dpd_tables, dsd_tables, spec_colo_tables,
                      standalone_tables)
-from .workload import BASE_SEED, RATES8, WORKLOADS, Trace, lengths, make_trace
+from .workload import BASE_SEED, RATES8, RATES_CODE8, WORKLOADS, Trace, lengths, make_trace
 
 MODE_DPD = 0
 MODE_DSD = 1
@@ -167,10 +167,11 @@ def config3(n: int = 100_000, cap: int = 16, rates=RATES8, bws=BW8) -> GridSpec:
                     row_labels=rl, col_labels=["DPD", "DSD"], workload="chat")
 
 
-def config4(n: int = 100_000, cap: int = 16, rates=RATES8) -> GridSpec:
+def config4(n: int = 100_000, cap: int = 16, rates=RATES8, workload: str = "chat",
+            name: str = "cfg4") -> GridSpec:
     """Full grid: 4 GPU pairs x 2 modes x 64 CI x 16 lifetimes x 8 rates.
     64 timing chains (rate x pair x mode) score 8,192 rows x 8 columns."""
-    traces = _rate_traces("chat", n, rates)
+    traces = _rate_traces(workload, n, rates)
     chains = []
     chain_of = {}
     tabs = {}
@@ -181,7 +182,7 @@ def config4(n: int = 100_000, cap: int = 16, rates=RATES8) -> GridSpec:
         for pi, (new, old) in enumerate(PAIRS4):
             for mode in (MODE_DPD, MODE_DSD):
                 chain_of[(ri, pi, mode)] = len(chains)
-                chains.append(_chain(mode, ri, cap, tabs[(pi, mode)], "chat", new, old, "7B",
+                chains.append(_chain(mode, ri, cap, tabs[(pi, mode)], workload, new, old, "7B",
                                      "1B" if mode == MODE_DSD else None,
                                      4 if mode == MODE_DSD else 0,
                                      0.8 if mode == MODE_DSD else 0.0,
@@ -199,9 +200,9 @@ def config4(n: int = 100_000, cap: int = 16, rates=RATES8) -> GridSpec:
                 for mode in (MODE_DPD, MODE_DSD):
                     cells.append(chain_of[(ri, pi, mode)])
     cols = [f"{'DPD' if m == 0 else 'DSD'} {a}+{b}" for (a, b) in PAIRS4 for m in (0, 1)]
-    return GridSpec("cfg4", traces, chains, scen, np.array(row_scen, np.int32),
+    return GridSpec(name, traces, chains, scen, np.array(row_scen, np.int32),
                     np.array(cells, np.int32), len(row_scen), 8,
-                    row_labels=rl, col_labels=cols, workload="chat")
+                    row_labels=rl, col_labels=cols, workload=workload)
 
 
 def config5(n: int = 1_000_000, cap: int = 16, rates=RATES8) -> GridSpec:
@@ -224,23 +225,24 @@ def config5(n: int = 1_000_000, cap: int = 16, rates=RATES8) -> GridSpec:
                     workload="summ")
 
 
-def config6(n: int = 100_000, cap: int = 16, rates=RATES8) -> GridSpec:
+def config6(n: int = 100_000, cap: int = 16, rates=RATES8, workload: str = "chat",
+            name: str = "cfg6") -> GridSpec:
     """config 4 plus the paper's two single-GPU columns
      -- Standalone 7B on an A100 (the paper's baseline) and
     SpecDecode 7B/1B (gamma 4, alpha 0.8) co-located on an A100 -- so Alg. 1
     chooses among all four configuration families.  80 timing chains score
     8,192 rows x 10 columns."""
-    g4 = config4(n, cap, rates)
+    g4 = config4(n, cap, rates, workload, name)
     chains = list(g4.chains)
     st = standalone_tables("A100", "7B", cap)
     sc = spec_colo_tables("A100", "7B", "1B", 4, cap)
     extra = {}
     for ri, r in enumerate(rates):
         extra[(ri, 0)] = len(chains)
-        chains.append(_chain(MODE_STANDALONE, ri, cap, st, "chat", "A100", None, "7B", None,
+        chains.append(_chain(MODE_STANDALONE, ri, cap, st, workload, "A100", None, "7B", None,
                              label=f"{st.label} {r}rps"))
         extra[(ri, 1)] = len(chains)
-        chains.append(_chain(MODE_SPEC_COLO, ri, cap, sc, "chat", "A100", None, "7B", "1B", 4,
+        chains.append(_chain(MODE_SPEC_COLO, ri, cap, sc, workload, "A100", None, "7B", "1B", 4,
                              0.8, label=f"{sc.label} {r}rps"))
     cells4 = g4.cell_chain.reshape(g4.rows, g4.cols)
     n_scen = len(g4.scenarios)
@@ -248,10 +250,20 @@ def config6(n: int = 100_000, cap: int = 16, rates=RATES8) -> GridSpec:
     for row in range(g4.rows):
         ri = row // n_scen
         cells.extend(list(cells4[row]) + [extra[(ri, 0)], extra[(ri, 1)]])
-    return GridSpec("cfg6", g4.traces, chains, g4.scenarios, g4.row_scenario,
+    return GridSpec(name, g4.traces, chains, g4.scenarios, g4.row_scenario,
                     np.array(cells, np.int32), g4.rows, g4.cols + 2, row_labels=g4.row_labels,
                     col_labels=g4.col_labels + ["Standalone A100", "SpecDecode A100"],
-                    workload="chat")
+                    workload=workload)
+
+
+def config7(n: int = 100_000, cap: int = 16, rates=RATES_CODE8) -> GridSpec:
+    """The paper's third workload (§6): HumanEval code requests (Table 2,
+    P:428: TTFT 125 ms / TPOT 200 ms SLOs, sizes 108/136/182 in, 31/55/88 out) at
+    rates covering its QPS window [0.5, 11], on config 6's candidate set:
+    7B DPD and DSD (1B, gamma 4, alpha 0.8) on the four GPU pairs, plus Standalone
+    and SpecDecode on an A100.  80 timing chains score 8,192 (rate x CI64 x LT16)
+    rows x 10 columns."""
+    return config6(n, cap, rates, workload="code", name="cfg7")
 
 
 def savings_pairs(grid: GridSpec):
@@ -262,7 +274,8 @@ def savings_pairs(grid: GridSpec):
             if c.mode != MODE_STANDALONE and c.trace_idx in base]
 
 
-CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5, 6: config6}
+CONFIGS = {1: config1, 2: config2, 3: config3, 4: config4, 5: config5, 6: config6,
+           7: config7}
 
 
 def build_config(k: int, **kw) -> GridSpec:

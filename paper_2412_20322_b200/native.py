@@ -104,11 +104,12 @@ def lib():
         L.gl_eval_grid.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32, vp, vp, vp]
         L.gl_argmin_feasible.restype = i32
         L.gl_argmin_feasible.argtypes = [vp, i32, C.POINTER(GlChain), C.POINTER(GlScenario), i32,
-                                         C.POINTER(GlGrid), i32, i32, i32, i32, vp, vp, vp, vp]
+                                         C.POINTER(GlGrid), i32, i32, i32, i32, vp, vp, vp, vp,
+                                         vp]
         L.gl_evaluate_host.restype = i32
         L.gl_evaluate_host.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
                                        C.POINTER(GlScenario), i32, C.POINTER(GlGrid), i32, i32,
-                                       i32, i32, vp, vp, vp, vp, vp]
+                                       i32, i32, vp, vp, vp, vp, vp, vp]
         L.gl_link_demand.restype = i32
         L.gl_link_demand.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
                                      C.POINTER(GlLinkParams), C.c_int64, vp, vp, vp]
@@ -200,7 +201,7 @@ def argmin_matrices(carbon_ptr: int, att_ptr: int, present_ptr: int | None, rows
 def argmin_feasible(stats_ptr: int, chains, scen: np.ndarray, rows: int, cols: int,
                     row_scenario: np.ndarray, cell_chain: np.ndarray, slo_num: int, slo_den: int,
                     priority: int, default_col: int, carbon_ptr: int | None, choice_ptr: int,
-                    fb_ptr: int, stream: int):
+                    fb_ptr: int, stream: int, per_token_ptr: int | None = None):
     c_arr = _arr(GlChain, chains)
     s, s_arr = _scen_arr(scen)
     rs = np.ascontiguousarray(row_scenario, dtype=np.int32)
@@ -208,13 +209,15 @@ def argmin_feasible(stats_ptr: int, chains, scen: np.ndarray, rows: int, cols: i
     g = GlGrid(rows, cols, rs.ctypes.data, cc.ctypes.data)
     check(lib().gl_argmin_feasible(stats_ptr, len(chains), c_arr, s_arr, len(s), C.byref(g),
                                    slo_num, slo_den, priority, default_col, carbon_ptr or None,
-                                   choice_ptr, fb_ptr, stream or None), "gl_argmin_feasible")
+                                   per_token_ptr or None, choice_ptr, fb_ptr, stream or None),
+          "gl_argmin_feasible")
     return lib().gl_last_launch_count()
 
 
 def evaluate_host(host_traces, chains, scen, rows, cols, row_scenario, cell_chain, slo_num,
                   slo_den, priority, default_col, stats_out: np.ndarray, carbon_out,
-                  choice_out: np.ndarray, fb_out: np.ndarray, stream: int):
+                  choice_out: np.ndarray, fb_out: np.ndarray, stream: int,
+                  per_token_out: np.ndarray | None = None):
     t_arr = _arr(GlTrace, host_traces)
     c_arr = _arr(GlChain, chains)
     s, s_arr = _scen_arr(scen)
@@ -225,6 +228,7 @@ def evaluate_host(host_traces, chains, scen, rows, cols, row_scenario, cell_chai
                                  C.byref(g), slo_num, slo_den, priority, default_col,
                                  stats_out.ctypes.data,
                                  None if carbon_out is None else carbon_out.ctypes.data,
+                                 None if per_token_out is None else per_token_out.ctypes.data,
                                  choice_out.ctypes.data, fb_out.ctypes.data, stream or None),
           "gl_evaluate_host")
     return lib().gl_last_launch_count()

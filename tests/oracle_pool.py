@@ -12,6 +12,7 @@ from __future__ import annotations
 
 import multiprocessing as mp
 import os
+import warnings
 
 import numpy as np
 
@@ -71,7 +72,10 @@ def evaluate_grid(grid, chain_ids=None, gpu_per_request=None, per_request=False,
                 if bad:
                     mism[ci] = bad
         else:
-            with mp.get_context("fork").Pool(procs) as pool:
+            with warnings.catch_warnings():  # the workers never touch CUDA or threads
+                warnings.simplefilter("ignore", DeprecationWarning)
+                pool = mp.get_context("fork").Pool(procs)
+            with pool:
                 for ci, st, bad in pool.imap_unordered(_chain, order, chunksize=1):
                     stats[ci] = st
                     if bad:

@@ -47,7 +47,7 @@ def test_library_exports_every_declared_symbol(built):
 
 def test_version_and_strerror_without_gpu(built):
     lib = built.lib()
-    assert lib.gl_version() == 1
+    assert lib.gl_version() == 2
     assert lib.gl_strerror(0) == b"ok"
     assert b"invalid" in lib.gl_strerror(-1)
 

@@ -31,3 +31,28 @@ def test_reference_arm_nonzero_rank_is_silent():
                           "--warmup", "3", "--n", "500"], cwd=ROOT, capture_output=True,
                          text=True, timeout=300, env=env)
     assert out.returncode == 0 and out.stdout.strip() == ""
+
+
+def test_reference_arm_other_configs():
+    """--config 5 / 7 select BASELINE configs[4] and the HumanEval grid."""
+    for cfg in (5, 7):
+        out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--steps", "1",
+                              "--warmup", "3", "--n", "800", "--config", str(cfg)], cwd=ROOT,
+                             capture_output=True, text=True, timeout=600)
+        assert out.returncode == 0, out.stderr[-2000:]
+        d = json.loads(out.stdout.strip().splitlines()[-1])
+        assert d["config"]["workload"].startswith(f"cfg{cfg}:") and d["value"] > 0
+
+
+def test_bench_helpers_roofline_units():
+    """The roofline's algorithmic bytes are SURVEY §8(d)'s 16 B per (timing chain,
+    request); shards are cost-balanced and cover every chain."""
+    sys.path.insert(0, ROOT)
+    import bench
+    from paper_2412_20322_b200.inputs import build_config
+    g = build_config(4, n=1000)
+    assert bench.algorithmic_bytes(g, 0, 64) == 16 * 64 * 1000
+    assert bench.algorithmic_bytes(g, 3, 5) == 16 * 2 * 1000
+    for w in (1, 2, 4, 8):
+        b = bench.shard_bounds(g, w)
+        assert b[0][0] == 0 and b[-1][1] == 64 and len(b) == w

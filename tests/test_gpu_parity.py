@@ -45,11 +45,16 @@ def grid_of(pairs, name="cases"):
                     np.arange(k, dtype=np.int32), k, 1)
 
 
+_LAST_PER_TOKEN = {}
+
+
 def run_gpu(g, per_request=True):
     dg = api.DeviceGrid(g)
     stats, pr = api.eval_grid(dg, per_request=per_request)
-    carbon, choice, fb = api.argmin_feasible(dg, stats)
+    ptok = torch.empty((g.rows, g.cols), dtype=torch.float64, device="cuda")
+    carbon, choice, fb = api.argmin_feasible(dg, stats, per_token_out=ptok)
     torch.cuda.synchronize()
+    _LAST_PER_TOKEN["v"] = ptok.cpu().numpy()
     return (api.stats_numpy(stats), None if pr is None else pr.cpu().numpy(),
             carbon.cpu().numpy(), choice.cpu().numpy(), fb.cpu().numpy())
 
@@ -70,6 +75,10 @@ def assert_parity(g, chain_ids=None, per_request=True, check_grid=True):
         m = ref["present"].astype(bool)
         assert np.array_equal(carbon[m], ref["carbon"][m])  # bit-identical (R34)
         np.testing.assert_allclose(carbon[m], ref["carbon"][m], rtol=1e-9)
+        # carbon per token: one division after the total, bit-identical too
+        ptok = _LAST_PER_TOKEN["v"]
+        assert np.array_equal(ptok[m], ref["carbon_per_token"][m], equal_nan=True)
+        assert np.all(np.isnan(ptok[~m]))
         assert np.array_equal(choice, ref["choice"])
         assert np.array_equal(fb, ref["via_fallback"])
     return st
@@ -319,6 +328,14 @@ def test_config5_full_size_all_chains():
     assert np.all(st["status"] == 0)
 
 
+def test_config7_humaneval_full_size():
+    """The paper's third workload (HumanEval code lengths, Table 2) over its
+    QPS window 0.5-11 req/s: 80 chains (7B DPD / DSD on four GPU pairs,
+    Standalone, SpecDecode) x 100k requests, every request and every Alg. 1 cell
+    of 8,192 x 10, carbon and carbon per token bit for bit."""
+    assert_parity(build_config(7))
+
+
 def test_config6_colocated_columns_full_size():
     """NEXT #1 at the bench size: config 4 plus the Standalone / SpecDecode A100
     columns (80 chains x 100k requests), every request, every chain, every Alg. 1
@@ -423,11 +440,15 @@ def test_evaluate_host_matches_device_path():
     stats, _ = api.eval_grid(dg)
     carbon, choice, fb = api.argmin_feasible(dg, stats)
     torch.cuda.synchronize()
-    res = api.evaluate_host(dg, dg.pinned_traces(), want_carbon=True)
+    ptok = torch.empty((g.rows, g.cols), dtype=torch.float64, device="cuda")
+    api.argmin_feasible(dg, stats, per_token_out=ptok)
+    torch.cuda.synchronize()
+    res = api.evaluate_host(dg, dg.pinned_traces(), want_carbon=True, want_per_token=True)
     assert res.stats.tobytes() == api.stats_numpy(stats).tobytes()
     assert np.array_equal(res.choice, choice.cpu().numpy())
     assert np.array_equal(res.via_fallback, fb.cpu().numpy())
     assert np.array_equal(res.carbon, carbon.cpu().numpy())
+    assert np.array_equal(res.carbon_per_token, ptok.cpu().numpy())
     assert res.launches == 6 and res.h2d_bytes > 0
 
 
@@ -481,3 +502,20 @@ def test_abi_errors():
                           np.zeros(1), np.zeros(1), 9, 10, 0, -1, None,
                           stats.data_ptr(), stats.data_ptr(), 0)
     assert e.value.status == N.GL_E_DOMAIN
+
+
+def test_eval_grid_on_copied_traces():
+    """api.eval_grid(traces=...) computes on the given device buffers (the
+    distributed end-to-end path copies its shard's traces from the host and
+    evaluates on the copies); results equal the resident path, and a copy with a
+    changed arrival changes the result."""
+    g = build_config(4, n=3000)
+    dg = api.DeviceGrid(g)
+    want = api.stats_numpy(api.eval_grid(dg, 8, 24)[0])
+    host = dg.pinned_traces()
+    copies = [tuple(x.to("cuda") for x in t) for t in host]
+    got = api.stats_numpy(api.eval_grid(dg, 8, 24, traces=copies)[0])
+    assert got.tobytes() == want.tobytes()
+    copies[1][0][5:] += 1000  # shift trace 1 (chains 8..15) by 1 ms after request 5
+    moved = api.stats_numpy(api.eval_grid(dg, 8, 24, traces=copies)[0])
+    assert moved[:8].tobytes() != want[:8].tobytes() and moved[8:].tobytes() == want[8:].tobytes()

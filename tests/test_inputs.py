@@ -108,3 +108,20 @@ def test_grid_shapes():
     assert (len(g2.chains), g2.rows, g2.cols) == (40, 5, 8)
     # every rate of one workload shares one length sequence (R5)
     assert g4.traces[0].output_len is g4.traces[5].output_len
+
+
+def test_config7_humaneval_grid():
+    """Config 7: HumanEval lengths and SLOs (Table 2) at rates spanning the
+    paper's QPS window [0.5, 11], config 6's candidate set."""
+    g = build_config(7, n=2000)
+    assert (len(g.chains), g.rows, g.cols, g.grid_points) == (80, 8192, 10, 81920)
+    rates = sorted({t.rate for t in g.traces})
+    assert rates[0] == 0.5 and rates[-1] == 11.0 and len(rates) == 8
+    wl = WORKLOADS["code"]
+    assert all(t.workload == "code" for t in g.traces)
+    assert all((c.ttft_slo_us, c.tpot_slo_us) == (125_000, 200_000) for c in g.chains)
+    o = g.traces[0].output_len
+    assert abs(np.median(o) - wl.p50[1]) <= 2
+    assert {c.mode for c in g.chains} == {0, 1, 2, 3}
+    # arrivals differ from config 6's chat traces (own workload id in the counter)
+    assert not np.array_equal(g.traces[0].arrival_us, build_config(6, n=2000).traces[0].arrival_us)

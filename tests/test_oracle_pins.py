@@ -140,6 +140,30 @@ def test_mix64_splitmix_published_vectors():
         assert O.mix64(0, 0, f - 2**64 if f >= 2**63 else f) == out
 
 
+def test_carbon_per_token_closed_form_and_argmin_equivalence():
+    """Carbon per token: S:73-74's Eq. 3 example (0.4 kWh + 3600 s on an
+    A100 at CI 261, 7 y) = 104.82954990215... g spread over 1,000 tokens; and R33 --
+    a row's cells share one trace, so Alg. 1 on per-token carbon (explicit matrices,
+    fractional attainment) picks exactly what the integer Alg. 1 on totals picks."""
+    lt7 = 7 * 365 * 24 * 3600.0
+    st = _stats(e_new=1.44e12, busy_new=3600e6)
+    st["tokens"] = 1000
+    tot = O.carbon(st, 26340.0, 10300.0, 261.0, lt7, lt7)[2]
+    assert O.carbon_per_token(st, tot) == pytest.approx(0.10482954990215264, rel=1e-13)
+    assert O.carbon_per_token(st, tot) == tot / 1000.0
+    st["tokens"] = 0  # void statistics (R55): IEEE total / 0
+    assert O.carbon_per_token(st, tot) == math.inf
+    from paper_2412_20322_b200.inputs import build_config
+    g = build_config(4, n=600)
+    ref = O.evaluate_grid(g)
+    att = np.array([[ref["stats"][int(k)]["slo_ok"] / ref["stats"][int(k)]["n"] for k in row]
+                    for row in g.cell_chain.reshape(g.rows, g.cols)])
+    ch, fb = O.alg1_matrices(ref["carbon_per_token"], att, ref["present"], 0.9, g.priority,
+                             g.default_col)
+    assert np.array_equal(ch, ref["choice"]) and np.array_equal(fb, ref["via_fallback"])
+    assert np.unique(ref["choice"]).size > 1  # the rows do not all pick one column
+
+
 # ----------------------------------------------------- worked examples A.1/A.2
 def _a1_chain(cap):
     ex = WE["A1_dpd_cap2"]
