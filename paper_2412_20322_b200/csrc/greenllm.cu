@@ -495,7 +495,14 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             ++launches;
         }
     }
-    if (e == cudaSuccess) {
+    if (e == cudaSuccess && extra == 0) {
+        // no helper warps (many chains): each leader walks its chain alone, one segment
+        prof_begin("k_segments", stream);
+        gl::k_segments_single<<<(unsigned)((n_chains + 127) / 128), 128, 0, stream>>>(dc, n_chains);
+        e = cudaGetLastError();
+        prof_end(stream);
+        ++launches;
+    } else if (e == cudaSuccess) {
         prof_begin("k_segments", stream);
         // k_segments: 1024-thread blocks, one per SM; S per chain while they fit in a wave
         const int seg_split = std::max(1, std::min(4, n_sm / std::max(1, (int)n_chains)));

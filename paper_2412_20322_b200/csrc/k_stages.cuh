@@ -646,4 +646,19 @@ __global__ void __launch_bounds__(1024)
     }
 }
 
+// Launches without helper warps (many chains: every chain's leader walks it alone)
+// need no idle-point candidates: one segment [0, M) per chain.  One thread per chain.
+__global__ void __launch_bounds__(128) k_segments_single(const DChain *__restrict__ chains, int32_t n_chains)
+{
+    const int32_t c = (int32_t)(blockIdx.x * blockDim.x + threadIdx.x);
+    if (c >= n_chains) return;
+    const DChain &ch = chains[c];
+    const int32_t M = ch.x->M;
+    ch.seg_start[0] = 0;
+    ch.seg_start[M > 0 ? 1 : 0] = M;
+    ch.x->nseg = M > 0 ? 1 : 0;
+    ch.x->leader_pos = 0;
+    ch.x->next_seg = 1;
+}
+
 }  // namespace gl
