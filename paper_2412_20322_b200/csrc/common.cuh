@@ -113,6 +113,22 @@ struct DGroup {
     uint64_t thr[GL_MAX_GAMMA];
 };
 
+// A DSD demand FAMILY: the groups that share (output lengths, n, seed) -- so the same
+// acceptance draws u(j, s) -- and differ in (alpha, gamma).  Laid out as a table of
+// alpha-sets (distinct threshold sequences, ascending alpha) x gamma = 1..FAM_GM;
+// K[a][g] is the K array of group (a, gamma = g + 1), null if no chain uses it.
+constexpr int FAM_NA = 5;  // alpha-sets per family (a family with more goes per group)
+constexpr int FAM_GM = 8;  // largest gamma in a family
+struct DFamily {
+    const uint32_t *o;
+    int64_t n;
+    uint64_t seed;
+    uint32_t thr[FAM_NA][FAM_GM];  // floor(alpha^c 2^32) < 2^32 (alpha < 1)
+    uint32_t all[FAM_NA];          // alpha = 1: every draft token accepted
+    int32_t na, pad;
+    uint32_t *K[FAM_NA][FAM_GM];
+};
+
 struct DCarbon {
     double ce_new, ce_old;
     int32_t cap_ok, pad;

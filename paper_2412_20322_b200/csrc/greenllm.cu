@@ -246,6 +246,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     std::vector<DGroup> groups;
     std::map<std::tuple<const uint32_t *, int64_t, int32_t, uint64_t, std::vector<uint64_t>>, int> gid;
     std::vector<int> chain_group(n_chains, -1);
+    std::vector<double> group_alpha;
     int max_cap = 1;
     size_t smem_st = 0;
     int64_t rows_total = 0, maxn = 0;
@@ -271,8 +272,60 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         if (it == gid.end()) {
             it = gid.emplace(key, (int)groups.size()).first;
             groups.push_back(g);
+            group_alpha.push_back(c.alpha);
         }
         chain_group[i] = it->second;
+    }
+    // Families: groups drawing the same acceptance words (equal output lengths, n and
+    // seed), differing in (alpha, gamma); one kernel pass evaluates each word once for
+    // all of them (k_dsd_family).  Up to FAM_NA alphas and gamma <= FAM_GM; any other
+    // group (and a family of one) keeps the per-group kernel.
+    std::vector<gl::DFamily> fams;
+    std::vector<std::vector<std::pair<int, int>>> fam_slots;  // (group, slot a * GM + g)
+    std::vector<int> solo;
+    {
+        std::map<std::tuple<const uint32_t *, int64_t, uint64_t>, std::vector<int>> fam_of;
+        for (size_t g = 0; g < groups.size(); ++g)
+            fam_of[std::make_tuple(groups[g].o, groups[g].n, groups[g].seed)].push_back((int)g);
+        for (auto &kv : fam_of) {
+            const std::vector<int> &L = kv.second;
+            // alpha-sets: the threshold sequence up to FAM_GM (repeated products, R22)
+            std::map<std::vector<uint64_t>, int> aset;
+            bool ok = L.size() >= 2;
+            for (int g : L) {
+                if (groups[g].gamma > gl::FAM_GM) ok = false;
+                uint64_t t[GL_MAX_GAMMA];
+                accept_thresholds(group_alpha[g], GL_MAX_GAMMA, t);
+                aset.emplace(std::vector<uint64_t>(t, t + gl::FAM_GM), 0);
+            }
+            if (aset.size() > (size_t)gl::FAM_NA) ok = false;
+            if (!ok) {
+                solo.insert(solo.end(), L.begin(), L.end());
+                continue;
+            }
+            gl::DFamily f{};
+            f.o = groups[L[0]].o;
+            f.n = groups[L[0]].n;
+            f.seed = groups[L[0]].seed;
+            f.na = (int32_t)aset.size();
+            int a = 0;  // std::map orders the sequences ascending: smallest alpha first
+            for (auto &av : aset) {
+                av.second = a;
+                const bool one = av.first[0] == (uint64_t)1 << 32;
+                f.all[a] = one ? 1u : 0u;
+                for (int c = 0; c < gl::FAM_GM; ++c) f.thr[a][c] = one ? 0u : (uint32_t)av.first[c];
+                ++a;
+            }
+            std::vector<std::pair<int, int>> slots;
+            for (int g : L) {
+                uint64_t t[GL_MAX_GAMMA];
+                accept_thresholds(group_alpha[g], GL_MAX_GAMMA, t);
+                const int ai = aset[std::vector<uint64_t>(t, t + gl::FAM_GM)];
+                slots.emplace_back(g, ai * gl::FAM_GM + (groups[g].gamma - 1));
+            }
+            fams.push_back(f);
+            fam_slots.push_back(slots);
+        }
     }
     const size_t smem_dec = gl::decode_smem_bytes(max_cap);
     int dev = 0, n_sm = 0, smem_optin = 0;
@@ -286,7 +339,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     // buffers: helpers x (n + 512) per chain][candidates]
     // [segment results][per-chain bookkeeping].  The last two are zeroed.
     const size_t off_groups = align256(sizeof(DChain) * n_chains);
-    size_t total = off_groups + align256(sizeof(DGroup) * groups.size());
+    const size_t off_fams = off_groups + align256(sizeof(DGroup) * groups.size());
+    size_t total = off_fams + align256(sizeof(gl::DFamily) * fams.size());
     std::vector<size_t> k_off(groups.size());
     for (size_t g = 0; g < groups.size(); ++g) {
         k_off[g] = total;
@@ -398,6 +452,11 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     std::vector<gl::DLink> dl(lk ? n_chains : 0);
     for (size_t g = 0; g < groups.size(); ++g)
         groups[g].K = reinterpret_cast<uint32_t *>(scratch + k_off[g]);
+    for (size_t fi = 0; fi < fams.size(); ++fi)
+        for (auto &gs : fam_slots[fi])
+            fams[fi].K[gs.second / gl::FAM_GM][gs.second % gl::FAM_GM] = groups[gs.first].K;
+    std::vector<DGroup> solo_groups;  // the per-group kernel's share
+    for (int g : solo) solo_groups.push_back(groups[g]);
 
     std::vector<DChain> dch(n_chains);
     int64_t out_off = 0;
@@ -455,8 +514,11 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     const DChain *dc = reinterpret_cast<const DChain *>(scratch);
     cudaError_t e = cudaMemcpyAsync(scratch, dch.data(), sizeof(DChain) * n_chains,
                                     cudaMemcpyHostToDevice, stream);
-    if (e == cudaSuccess && !groups.empty())
-        e = cudaMemcpyAsync(scratch + off_groups, groups.data(), sizeof(DGroup) * groups.size(),
+    if (e == cudaSuccess && !solo_groups.empty())
+        e = cudaMemcpyAsync(scratch + off_groups, solo_groups.data(),
+                            sizeof(DGroup) * solo_groups.size(), cudaMemcpyHostToDevice, stream);
+    if (e == cudaSuccess && !fams.empty())
+        e = cudaMemcpyAsync(scratch + off_fams, fams.data(), sizeof(gl::DFamily) * fams.size(),
                             cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess && lk)
         e = cudaMemcpyAsync(scratch + off_links, dl.data(), sizeof(gl::DLink) * n_chains,
@@ -465,14 +527,29 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     if (e == cudaSuccess && lk)  // log sentinels: every byte 0xFF -> (T, b) = (-1, -1)
         e = cudaMemsetAsync(scratch + off_ev, 0xFF, sizeof(longlong2) * (size_t)ev_total, stream);
     int launches = 0;
-    if (e == cudaSuccess && !groups.empty()) {
+    if (e == cudaSuccess && !fams.empty()) {
+        // persistent threads: about 8 resident blocks of 128 threads per SM in total,
+        // spread over the families, never more than one thread per request
+        int64_t fmax = 0;
+        for (auto &f : fams) fmax = std::max(fmax, f.n);
+        const int64_t want = std::max<int64_t>(1, (8 * (int64_t)n_sm) / (int64_t)fams.size());
+        const int64_t need_b = (fmax + 127) / 128;
+        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, need_b)), (unsigned)fams.size());
+        prof_begin("k_dsd_family", stream);
+        gl::k_dsd_family<<<grid, 128, 0, stream>>>(
+            reinterpret_cast<const gl::DFamily *>(scratch + off_fams));
+        e = cudaGetLastError();
+        prof_end(stream);
+        ++launches;
+    }
+    if (e == cudaSuccess && !solo_groups.empty()) {
         // persistent quads: about 16 resident blocks of 256 threads per SM in total,
         // spread over the groups, never more than one quad per request
         int64_t gmax = 0;
-        for (auto &g : groups) gmax = std::max(gmax, g.n);
-        const int64_t want = std::max<int64_t>(1, (16 * (int64_t)n_sm) / (int64_t)groups.size());
+        for (auto &g : solo_groups) gmax = std::max(gmax, g.n);
+        const int64_t want = std::max<int64_t>(1, (16 * (int64_t)n_sm) / (int64_t)solo_groups.size());
         const int64_t need_b = (gmax * gl::DSD_QL + 255) / 256;
-        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, need_b)), (unsigned)groups.size());
+        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, need_b)), (unsigned)solo_groups.size());
         prof_begin("k_dsd_demand", stream);
         gl::k_dsd_demand<<<grid, 256, 0, stream>>>(
             reinterpret_cast<const DGroup *>(scratch + off_groups));

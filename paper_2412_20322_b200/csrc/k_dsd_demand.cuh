@@ -122,4 +122,89 @@ __global__ void __launch_bounds__(256) k_dsd_demand(const DGroup *__restrict__ g
     }
 }
 
+// Families (several (alpha, gamma) groups on one set of draws; configs 2 and 5 have one
+// family of 5 alphas x 8 gammas): one thread per request evaluates each Philox word
+// ONCE for every group.  Per draft step s and alpha-set a, m_a = #{c : u_s < thr_a[c]}
+// (thresholds decrease in c, so the accepted drafts are a prefix); group (a, gamma)
+// accepts 1 + min(gamma, m_a) tokens, and its K is the first step whose running total
+// reaches o - 1.  Running totals grow with alpha and gamma (thresholds grow with
+// alpha), so the group (smallest alpha, gamma = 1) is the last to finish: the loop for
+// a request ends when it has.  Threads are persistent: a lane whose request is done
+// takes its next one (stride = all threads of the family) in the same loop trip.
+__global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ fams)
+{
+    const DFamily *f = fams + blockIdx.y;
+    uint32_t thr[FAM_NA][FAM_GM];
+    bool all[FAM_NA];
+#pragma unroll
+    for (int a = 0; a < FAM_NA; ++a) {
+        all[a] = __ldg(&f->all[a]) != 0u;
+#pragma unroll
+        for (int c = 0; c < FAM_GM; ++c) thr[a][c] = __ldg(&f->thr[a][c]);
+    }
+    const int na = __ldg(&f->na);
+    const int64_t n = __ldg(&f->n);
+    const uint64_t seed = __ldg(&f->seed);
+    const uint32_t k0 = (uint32_t)seed, k1 = (uint32_t)(seed >> 32);
+    const uint32_t *const o = f->o;
+    const int64_t Q = (int64_t)gridDim.x * blockDim.x;
+    int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    uint32_t tok[FAM_NA][FAM_GM];
+    int64_t need = 0;
+    uint32_t call = 0;
+    // next request with demand > 0 (requests with o = 1 get K = 0 right away)
+    auto take = [&]() {
+        for (; j < n; j += Q) {
+            uint32_t ov = __ldg(o + j);
+            if (ov >= O_LIMIT) ov = O_LIMIT - 1;
+            need = (int64_t)ov - 1;
+            if (need > 0) break;
+#pragma unroll
+            for (int a = 0; a < FAM_NA; ++a)
+#pragma unroll
+                for (int g = 0; g < FAM_GM; ++g) {
+                    uint32_t *K = f->K[a][g];
+                    if (a < na && K) K[j] = 0u;
+                }
+        }
+#pragma unroll
+        for (int a = 0; a < FAM_NA; ++a)
+#pragma unroll
+            for (int g = 0; g < FAM_GM; ++g) tok[a][g] = 0u;
+        call = 0;
+    };
+    take();
+    while (__any_sync(FULL, j < n)) {
+        if (j < n) {
+            const uint4 w = philox4x32_10(make_uint4(call, (uint32_t)j, ACCEPT_STREAM, 0u), k0, k1);
+            const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+            for (int q = 0; q < 4; ++q) {
+                const uint32_t u = ws[q];
+                const uint32_t step = 4u * call + (uint32_t)q + 1u;  // K if this step crosses
+#pragma unroll
+                for (int a = 0; a < FAM_NA; ++a) {
+                    if (a >= na) continue;
+                    uint32_t m = 0;
+#pragma unroll
+                    for (int c = 0; c < FAM_GM; ++c) m += u < thr[a][c] ? 1u : 0u;
+                    if (all[a]) m = FAM_GM;
+#pragma unroll
+                    for (int g = 0; g < FAM_GM; ++g) {
+                        const uint32_t t = tok[a][g] + 1u + min((uint32_t)(g + 1), m);
+                        uint32_t *K = f->K[a][g];
+                        if ((int64_t)tok[a][g] < need && (int64_t)t >= need && K) K[j] = step;
+                        tok[a][g] = t;
+                    }
+                }
+            }
+            ++call;
+            if ((int64_t)tok[0][0] >= need) {  // the last group has crossed: next request
+                j += Q;
+                take();
+            }
+        }
+    }
+}
+
 }  // namespace gl

@@ -519,3 +519,35 @@ def test_eval_grid_on_copied_traces():
     copies[1][0][5:] += 1000  # shift trace 1 (chains 8..15) by 1 ms after request 5
     moved = api.stats_numpy(api.eval_grid(dg, 8, 24, traces=copies)[0])
     assert moved[:8].tobytes() != want[:8].tobytes() and moved[8:].tobytes() == want[8:].tobytes()
+
+
+def test_dsd_demand_families():
+    """k_dsd_family: chains on ONE trace with several (alpha, gamma) -- including alpha 0
+    and 1, gamma 1..8, absent table cells, o = 1 requests and a gamma-16 chain that
+    stays on the per-group kernel -- draw the same words once for all groups; every
+    request's finish must equal the oracle's (which draws per member-step)."""
+    rng = np.random.default_rng(77)
+    n = 3000
+    a = np.cumsum(rng.exponential(400.0, n)).astype(np.int64)
+    p = rng.integers(1, 9, n)
+    o = rng.integers(1, 400, n)
+    o[rng.random(n) < 0.1] = 1
+    tr = custom_trace(a, p, o)
+    chains = []
+    for alpha in (0.0, 0.3, 0.65, 0.9, 1.0):
+        for gamma in (1, 3, 8):
+            if (alpha, gamma) == (0.3, 3):
+                continue  # an absent cell of the family table
+            tab = make_tables(8, 16, lambda q: 30 * q, lambda q: 7 * q,
+                              [0] + [40 + 10 * b for b in range(1, 17)], b2=lambda q: q,
+                              sbn=[0] + [3] * 16, sbo=[0] + [4] * 16, sen=[0] + [5] * 16,
+                              seo=[0] + [6] * 16)
+            chains.append(make_chain(tab, MODE_DSD, 16, gamma, alpha, seed=0xABCDEF,
+                                     ttft_slo=5000, tpot_slo=600))
+    chains.append(dataclasses.replace(chains[0], gamma=16, alpha=0.8))  # per-group kernel
+    chains.append(dataclasses.replace(chains[1], mode=MODE_SPEC_COLO))  # co-located, same draws
+    k = len(chains)
+    lt = 7 * 365 * 24 * 3600.0
+    g = GridSpec("families", [tr], chains, np.array([[261.0, lt, lt]]), np.zeros(k, np.int32),
+                 np.arange(k, dtype=np.int32), k, 1)
+    assert_parity(g)
