@@ -134,6 +134,9 @@ __global__ void __launch_bounds__(256) k_dsd_demand(const DGroup *__restrict__ g
 __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ fams)
 {
     const DFamily *f = fams + blockIdx.y;
+    __shared__ uint32_t *s_K[FAM_NA * FAM_GM];
+    if (threadIdx.x < FAM_NA * FAM_GM) s_K[threadIdx.x] = f->K[threadIdx.x / FAM_GM][threadIdx.x % FAM_GM];
+    __syncthreads();
     uint32_t thr[FAM_NA][FAM_GM];
     bool all[FAM_NA];
 #pragma unroll
@@ -149,28 +152,25 @@ __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ 
     const uint32_t *const o = f->o;
     const int64_t Q = (int64_t)gridDim.x * blockDim.x;
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t tok[FAM_NA][FAM_GM];
-    int64_t need = 0;
-    uint32_t call = 0;
+    uint32_t tok[FAM_NA][FAM_GM], kk[FAM_NA][FAM_GM];  // running totals, K once crossed
+    uint32_t need = 0, call = 0;
     // next request with demand > 0 (requests with o = 1 get K = 0 right away)
     auto take = [&]() {
         for (; j < n; j += Q) {
             uint32_t ov = __ldg(o + j);
             if (ov >= O_LIMIT) ov = O_LIMIT - 1;
-            need = (int64_t)ov - 1;
+            need = ov > 0 ? ov - 1 : 0;
             if (need > 0) break;
-#pragma unroll
-            for (int a = 0; a < FAM_NA; ++a)
-#pragma unroll
-                for (int g = 0; g < FAM_GM; ++g) {
-                    uint32_t *K = f->K[a][g];
-                    if (a < na && K) K[j] = 0u;
-                }
+            for (int i = 0; i < na * FAM_GM; ++i)
+                if (s_K[i]) s_K[i][j] = 0u;
         }
 #pragma unroll
         for (int a = 0; a < FAM_NA; ++a)
 #pragma unroll
-            for (int g = 0; g < FAM_GM; ++g) tok[a][g] = 0u;
+            for (int g = 0; g < FAM_GM; ++g) {
+                tok[a][g] = 0u;
+                kk[a][g] = 0u;
+            }
         call = 0;
     };
     take();
@@ -184,7 +184,6 @@ __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ 
                 const uint32_t step = 4u * call + (uint32_t)q + 1u;  // K if this step crosses
 #pragma unroll
                 for (int a = 0; a < FAM_NA; ++a) {
-                    if (a >= na) continue;
                     uint32_t m = 0;
 #pragma unroll
                     for (int c = 0; c < FAM_GM; ++c) m += u < thr[a][c] ? 1u : 0u;
@@ -192,14 +191,20 @@ __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ 
 #pragma unroll
                     for (int g = 0; g < FAM_GM; ++g) {
                         const uint32_t t = tok[a][g] + 1u + min((uint32_t)(g + 1), m);
-                        uint32_t *K = f->K[a][g];
-                        if ((int64_t)tok[a][g] < need && (int64_t)t >= need && K) K[j] = step;
+                        kk[a][g] = (kk[a][g] == 0u && t >= need) ? step : kk[a][g];
                         tok[a][g] = t;
                     }
                 }
             }
             ++call;
-            if ((int64_t)tok[0][0] >= need) {  // the last group has crossed: next request
+            if (tok[0][0] >= need) {  // the last group has crossed: write K, next request
+#pragma unroll
+                for (int a = 0; a < FAM_NA; ++a)
+#pragma unroll
+                    for (int g = 0; g < FAM_GM; ++g) {
+                        uint32_t *K = s_K[a * FAM_GM + g];
+                        if (a < na && K) K[j] = kk[a][g];
+                    }
                 j += Q;
                 take();
             }
