@@ -416,6 +416,30 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     total += align256(sizeof(gl::DSegOut) * (size_t)seg_total);
     const size_t off_x = total;
     total += align256(sizeof(gl::DChainX) * (size_t)n_chains);
+    // Stage groups: disaggregated chains of one mode on the same trace with the same
+    // prompt-indexed tables run identical stage-1/2 scans; the first (primary) runs
+    // k_stages, the others (secondaries) take its results in k_stage_clone.
+    std::vector<int32_t> prim_of(n_chains), prim_ids, sec_ids;
+    {
+        std::map<std::tuple<int32_t, int32_t, const void *, const void *, const void *,
+                            const void *, const void *, int32_t>, int32_t> first;
+        for (int32_t i = 0; i < n_chains; ++i) {
+            const gl_chain &c = chains[i];
+            prim_of[i] = i;
+            if (c.mode == GL_MODE_DPD || c.mode == GL_MODE_DSD) {
+                auto key = std::make_tuple(c.trace_idx, c.mode, (const void *)c.t1_us,
+                                           (const void *)c.t2_us, (const void *)c.b2_old_us,
+                                           (const void *)c.e1_new_uj, (const void *)c.e2_old_uj,
+                                           c.max_prompt);
+                auto it = first.find(key);
+                if (it == first.end()) first.emplace(key, i);
+                else prim_of[i] = it->second;
+            }
+            if (prim_of[i] == i) prim_ids.push_back(i);
+            else sec_ids.push_back(i);
+        }
+    }
+    const int32_t n_prim = (int32_t)prim_ids.size(), n_sec = (int32_t)sec_ids.size();
     // k_stages: S blocks per chain (decoupled look-back between them), S <= 4 chosen
     // to minimise the waves per chain's work, ceil(chains S / resident) / S (ties to
     // the smaller S): 2 on config 4's 64 chains, 3 on config 6's 80, 4 on config 5's 320
@@ -428,9 +452,9 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                                                           smem_st) == cudaSuccess &&
             per_sm > 0) {
             const int64_t slots = (int64_t)per_sm * n_sm;
-            int64_t best_w = (n_chains + slots - 1) / slots;
+            int64_t best_w = (n_prim + slots - 1) / slots;
             for (int S = 2; S <= gl::ST_MAX_SPLIT; ++S) {
-                const int64_t w = ((int64_t)n_chains * S + slots - 1) / slots;
+                const int64_t w = ((int64_t)n_prim * S + slots - 1) / slots;
                 if (w * stage_split < best_w * S) {
                     best_w = w;
                     stage_split = S;
@@ -443,6 +467,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     total += align256(sizeof(gl::DStagePart) * (size_t)n_chains * stage_split);
     const size_t off_ticket = total;
     total += 256;
+    const size_t off_ids = total;  // primaries, secondaries, primary of each chain
+    total += align256(sizeof(int32_t) * ((size_t)n_chains * 2 + 2));
     const size_t zero_bytes = total - off_zero;
     unsigned char *scratch = nullptr;
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
@@ -511,7 +537,11 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         d.max_prompt = c.max_prompt;
         d.capacity_ok = c.capacity_ok ? 1 : 0;
     }
+    for (int32_t i : sec_ids) dch[i].dec_r = dch[prim_of[i]].dec_r;  // shared ready times
     const DChain *dc = reinterpret_cast<const DChain *>(scratch);
+    int32_t *d_prim_ids = reinterpret_cast<int32_t *>(scratch + off_ids);
+    int32_t *d_sec_ids = d_prim_ids + n_prim;
+    int32_t *d_prim_of = d_sec_ids + n_sec;
     cudaError_t e = cudaMemcpyAsync(scratch, dch.data(), sizeof(DChain) * n_chains,
                                     cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess && !solo_groups.empty())
@@ -524,6 +554,14 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         e = cudaMemcpyAsync(scratch + off_links, dl.data(), sizeof(gl::DLink) * n_chains,
                             cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(scratch + off_zero, 0, zero_bytes, stream);
+    std::vector<int32_t> idv;  // (kept alive until the copy is enqueued: pageable, synchronous staging)
+    if (e == cudaSuccess && n_sec > 0) {  // after the memset: the ids live in the zeroed region
+        idv = prim_ids;
+        idv.insert(idv.end(), sec_ids.begin(), sec_ids.end());
+        idv.insert(idv.end(), prim_of.begin(), prim_of.end());
+        e = cudaMemcpyAsync(d_prim_ids, idv.data(), sizeof(int32_t) * idv.size(),
+                            cudaMemcpyHostToDevice, stream);
+    }
     if (e == cudaSuccess && lk)  // log sentinels: every byte 0xFF -> (T, b) = (-1, -1)
         e = cudaMemsetAsync(scratch + off_ev, 0xFF, sizeof(longlong2) * (size_t)ev_total, stream);
     int launches = 0;
@@ -565,12 +603,24 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                                  (int)smem_st);
         if (e == cudaSuccess) {
             prof_begin("k_stages", stream);
-            gl::k_stages<<<n_chains * stage_split, 32 * gl::ST_WARPS, smem_st, stream>>>(
-                dc, stats_out, rows, stage_split, reinterpret_cast<int32_t *>(scratch + off_ticket));
+            gl::k_stages<<<n_prim * stage_split, 32 * gl::ST_WARPS, smem_st, stream>>>(
+                dc, stats_out, rows, stage_split, reinterpret_cast<int32_t *>(scratch + off_ticket),
+                n_sec > 0 ? d_prim_ids : nullptr);
             e = cudaGetLastError();
             prof_end(stream);
             ++launches;
         }
+    }
+    // rows are an output (or feed the link analysis): secondaries get full copies
+    const bool copy_rows = per_request_out != nullptr || lk != nullptr;
+    if (e == cudaSuccess && n_sec > 0) {
+        const int bpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, (8 * (int64_t)n_sm + n_sec - 1) / n_sec));
+        prof_begin("k_stage_clone", stream);
+        gl::k_stage_clone<<<dim3((unsigned)bpc, (unsigned)n_sec), 256, 0, stream>>>(
+            dc, stats_out, rows, d_sec_ids, d_prim_of, stage_split, copy_rows ? 1 : 0);
+        e = cudaGetLastError();
+        prof_end(stream);
+        ++launches;
     }
     if (e == cudaSuccess && extra == 0) {
         // no helper warps (many chains): each leader walks its chain alone, one segment
@@ -654,7 +704,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         const int per_thread = 8;
         dim3 grid((unsigned)((maxn + 256 * per_thread - 1) / (256 * per_thread)), (unsigned)n_chains);
         prof_begin("k_finalize", stream);
-        gl::k_finalize<<<grid, 256, 0, stream>>>(dc, stats_out, rows, per_thread);
+        gl::k_finalize<<<grid, 256, 0, stream>>>(dc, stats_out, rows, per_thread,
+                                                 (n_sec > 0 && !copy_rows) ? d_prim_of : nullptr);
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;

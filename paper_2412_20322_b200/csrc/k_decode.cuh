@@ -865,23 +865,33 @@ __host__ __device__ inline size_t decode_smem_bytes(int cap)
 // Integer atomics commute, so the result is deterministic.
 __global__ void __launch_bounds__(256)
     k_finalize(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
-               const int64_t *__restrict__ perreq, int per_thread)
+               const int64_t *__restrict__ perreq, int per_thread,
+               const int32_t *__restrict__ prim_of)  // NULL: every chain has its own rows
 {
     __shared__ unsigned long long s_ok[8], s_hash[8];
     const DChain &ch = chains[blockIdx.y];
     if (stats[blockIdx.y].status != 0) return;  // invalid input: only n and status (R55)
     const int64_t n = ch.n;
     const int64_t *rows = perreq + 2 * ch.out_off;
+    // a secondary chain (k_stage_clone without row copies) reads its TTFTs and the
+    // finish times of o = 1 requests from its primary's rows
+    const int32_t pr = prim_of ? prim_of[blockIdx.y] : (int32_t)blockIdx.y;
+    const int64_t *prow = perreq + 2 * chains[pr].out_off;
+    const bool own = pr == (int32_t)blockIdx.y;
     const int64_t ttft_slo = ch.ttft_slo, tpot_slo = ch.tpot_slo;
     unsigned long long ok = 0, hash = 0;
     const int64_t base = (int64_t)blockIdx.x * blockDim.x * per_thread;
     for (int q = 0; q < per_thread; ++q) {
         const int64_t j = base + (int64_t)q * blockDim.x + threadIdx.x;
         if (j < n) {
-            const longlong2 tf = __ldg(reinterpret_cast<const longlong2 *>(rows) + j);
+            longlong2 tf = __ldg(reinterpret_cast<const longlong2 *>(rows) + j);
             const int64_t a = __ldg(ch.a + j);
             uint32_t o = __ldg(ch.o + j);
             o = min(max(o, 1u), O_LIMIT - 1);
+            if (!own) {
+                tf.x = __ldg(prow + 2 * j);
+                if (o == 1) tf.y = __ldg(prow + 2 * j + 1);
+            }
             const int64_t c = a + tf.x;
             const bool good = tf.x <= ttft_slo &&
                               (o == 1 || tf.y - c <= tpot_slo * (int64_t)(o - 1));

@@ -182,7 +182,8 @@ __device__ __forceinline__ void stage_lookback(const DChain &ch, int s, bool sec
 
 __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     k_stages(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
-             int64_t *__restrict__ perreq, int32_t S, int32_t *__restrict__ ticket)
+             int64_t *__restrict__ perreq, int32_t S, int32_t *__restrict__ ticket,
+             const int32_t *__restrict__ ids)  // chains to run (primaries), NULL = all
 {
     __shared__ int32_t s_vid;
     __shared__ int64_t s_carry;
@@ -198,7 +199,7 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     // with smaller ids, which are already running (no assumption on dispatch order)
     if (threadIdx.x == 0) s_vid = S > 1 ? atomicAdd(ticket, 1) : (int32_t)blockIdx.x;
     __syncthreads();
-    const int32_t chain = s_vid / S, sblk = s_vid % S;
+    const int32_t chain = ids ? ids[s_vid / S] : s_vid / S, sblk = s_vid % S;
     const DChain ch = chains[chain];
     const int P = ch.max_prompt, cap = ch.cap;
     const int p1pad = round_up4(P + 1);
@@ -218,12 +219,17 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     }
     __syncthreads();
 
+    // invalid tables (GL_ST_TABLE): prompt-indexed ones skip the passes; a step table
+    // does not (the passes never read it), so chains cloning this one's stage results
+    // (k_stage_clone) get valid partials whatever this chain's own step table holds
     uint32_t status = 0;
+    bool step_bad;
     {
-        bool bad = false;
+        bool bad = false, sbad = false;
         for (int i = 1 + threadIdx.x; i <= P; i += blockDim.x) bad |= (t1s[i] < 0) | (t2s[i] < 0);
-        for (int b = 1 + threadIdx.x; b <= cap; b += blockDim.x) bad |= __ldg(ch.step + b) < 1;
+        for (int b = 1 + threadIdx.x; b <= cap; b += blockDim.x) sbad |= __ldg(ch.step + b) < 1;
         if (__syncthreads_or(bad)) status |= GL_ST_TABLE;
+        step_bad = __syncthreads_or(sbad);
     }
     const bool skip = status & GL_ST_TABLE;
 
@@ -457,6 +463,7 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
             s[5] = max(s[5], __ldcg(&q.sums[5]));
             st |= __ldcg(&q.status);
         }
+        if (step_bad) st |= GL_ST_TABLE;
         // a chain with invalid input (any status bit) keeps only n and its status;
         // its decode stage is empty (M = 0) and k_finalize skips it, so every other
         // field is 0, as in the oracle, and Alg. 1 treats it as infeasible (R55)
@@ -643,6 +650,78 @@ __global__ void __launch_bounds__(1024)
             ch.x->leader_pos = 0;
             ch.x->next_seg = 1;
         }
+    }
+}
+
+// Stage results of a SECONDARY chain -- same trace and prompt-indexed tables as its
+// primary (so identical stage-1/2 scans, TTFT rows and stage sums), its own mode,
+// step table and demand -- taken from the primary's k_stages partials instead of
+// re-running the scans (configuration 5: 320 chains, 8 primaries).  Per secondary:
+// the statistics (its own step-table check and capacity flag, R55 if any status
+// bit), the decode count, its decode stream's (demand, request) half over the
+// primary's ready times (shared: DChain.dec_r points at the primary's), and, when the
+// per-request rows are an output, the primary's (ttft, finish-of-o = 1) rows.
+// Grid: (blocks per chain, secondaries) x 256.
+__global__ void __launch_bounds__(256)
+    k_stage_clone(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
+                  int64_t *__restrict__ perreq, const int32_t *__restrict__ sec,
+                  const int32_t *__restrict__ prim_of, int32_t S, int32_t copy_rows)
+{
+    const int32_t c = sec[blockIdx.y], pi = prim_of[c];
+    const DChain &ch = chains[c];
+    const DChain &pc = chains[pi];
+    bool sbad = false;
+    for (int b = 1 + threadIdx.x; b <= ch.cap; b += blockDim.x) sbad |= __ldg(ch.step + b) < 1;
+    const bool step_bad = __syncthreads_or(sbad);
+    int64_t sm[6] = {0, 0, 0, 0, 0, 0};
+    uint32_t st = step_bad ? GL_ST_TABLE : 0u;
+    int32_t M = 0;
+    for (int p = 0; p < S; ++p) {
+        const DStagePart &q = pc.stp[p];
+        for (int i = 0; i < 5; ++i) sm[i] += __ldcg(&q.sums[i]);
+        sm[5] = max(sm[5], __ldcg(&q.sums[5]));
+        st |= __ldcg(&q.status);
+        M += __ldcg(&q.dcount);
+    }
+    const bool valid = st == 0;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {  // R55 as in k_stages
+        gl_chain_stats o;
+        o.n = ch.n;
+        o.slo_ok = 0;
+        o.tokens = valid ? sm[4] : 0;
+        o.busy_new_us = valid ? sm[0] : 0;
+        o.busy_old_us = valid ? sm[1] : 0;
+        o.e_new_uj = valid ? sm[2] : 0;
+        o.e_old_uj = valid ? sm[3] : 0;
+        o.makespan_us = valid ? sm[5] : 0;
+        o.req_hash = 0;
+        o.status = st;
+        o.capacity_ok = (uint32_t)ch.capacity_ok;
+        stats[c] = o;
+        ch.x->M = valid ? M : 0;
+    }
+    const bool dsd = ch.mode == GL_MODE_DSD;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t q = t0; q < (int64_t)M + DEC_TAIL; q += stride) {
+        uint2 v = make_uint2(0u, 0u);  // tail: "no request" (dec_r's sentinels are shared)
+        if (q < M) {
+            const uint32_t j = __ldcg(&pc.dec_dj[q].y);
+            uint32_t d;
+            if (dsd) {
+                d = __ldg(ch.K + j);
+            } else {
+                const uint32_t o = min(max(__ldg(ch.o + j), 1u), O_LIMIT - 1);
+                d = o - 1u;
+            }
+            v = make_uint2(d, j);
+        }
+        ch.dec_dj[q] = v;
+    }
+    if (copy_rows) {  // the primary's (ttft, finish of o = 1 requests) rows
+        const longlong2 *src = reinterpret_cast<const longlong2 *>(perreq + 2 * pc.out_off);
+        longlong2 *dst = reinterpret_cast<longlong2 *>(perreq + 2 * ch.out_off);
+        for (int64_t j = t0; j < ch.n; j += stride) dst[j] = __ldcg(src + j);
     }
 }
 

@@ -551,3 +551,27 @@ def test_dsd_demand_families():
     g = GridSpec("families", [tr], chains, np.array([[261.0, lt, lt]]), np.zeros(k, np.int32),
                  np.arange(k, dtype=np.int32), k, 1)
     assert_parity(g)
+
+
+@pytest.mark.parametrize("per_request", [True, False])
+def test_stage_groups_clone(per_request):
+    """k_stage_clone: chains of one mode on one trace with the same prompt-indexed
+    tables share one k_stages run (the primary) -- the secondaries differ in gamma,
+    alpha, step table (one invalid: step[2] = 0), batch cap and capacity flag.  With
+    per-request rows they get copies; without, k_finalize reads the primary's."""
+    g = build_config(5, n=4000)
+    chains = list(g.chains[:24])
+    bad = make_tables(4096, 16, lambda q: 1, lambda q: 1, [0, 5, 0] + [9] * 14)
+    chains[5] = dataclasses.replace(chains[5], tables=dataclasses.replace(
+        chains[5].tables, step_us=bad.step_us))
+    chains[7] = dataclasses.replace(chains[7], cap=8, capacity_ok=1)
+    cells = np.arange(24, dtype=np.int32)
+    gg = GridSpec("clone", g.traces, chains, g.scenarios, np.zeros(3, np.int32), cells, 3, 8)
+    st, pr, _, _, _ = run_gpu(gg, per_request=per_request)
+    assert st[5]["status"] & N.ST_TABLE
+    ids = [i for i in range(24) if i != 5]
+    ref = oracle_pool.evaluate_grid(gg, chain_ids=ids, gpu_per_request=pr if per_request else None)
+    for ci in ids:
+        for f in INT_FIELDS:
+            assert int(st[ci][f]) == int(ref["stats"][ci][f]), (ci, f)
+    assert not ref["mismatch"]
