@@ -1,12 +1,17 @@
-"""Build variants of libgreenllm.so for same-box A/B timing (kernel experiments).
+"""Build A/B variants of libgreenllm.so for same-box timing (kernel experiments).
 
-Each variant is a list of (old, new) source replacements applied to a copy of
-paper_2412_20322_b200/csrc; the result goes to build/ab/<name>.so.  Time them
-with  GL_LIB_PATH=build/ab/<name>.so python scripts/quick_times.py ...
+A variant is the tree's csrc/ with some -D macro settings (e.g. GL_SAT2_MIN in older
+revisions) or a patch file of (old, new) replacements; the result goes to
+build/ab/<name>.so.  Time variants with  scripts/ab_times.sh <name>...
 
-usage: python scripts/ab_build.py [variant ...]   (default: all in VARIANTS)
+    python scripts/ab_build.py <name> [-Dmacro=value ...] [--patch file.py]
+
+A patch file defines EDITS = [(csrc file name, old text, new text), ...].  The
+round-2 experiments and their outcomes are in profiles/r02_decode_ab.md; their
+sources are in the git history of k_decode.cuh.
 """
 import os
+import runpy
 import shutil
 import subprocess
 import sys
@@ -14,11 +19,9 @@ import sys
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 SRC = os.path.join(ROOT, "paper_2412_20322_b200", "csrc")
 OUT = os.path.join(ROOT, "build", "ab")
-sys.path.insert(0, ROOT)
-from scripts.ab_variants import VARIANTS  # noqa: E402
 
 
-def build(name, edits):
+def build(name, defines=(), edits=()):
     tmp = os.path.join("/tmp", f"ab_{name}")
     shutil.rmtree(tmp, ignore_errors=True)
     shutil.copytree(SRC, tmp)
@@ -29,14 +32,19 @@ def build(name, edits):
         open(p, "w").write(s.replace(old, new))
     os.makedirs(OUT, exist_ok=True)
     cmd = ["nvcc", "-gencode", "arch=compute_100a,code=sm_100a", "-O3", "-lineinfo", "-std=c++17",
-           "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"),
+           "-Xcompiler", "-fPIC", "-shared", "-I", os.path.join(ROOT, "include"), *defines,
            "-o", os.path.join(OUT, f"{name}.so"), os.path.join(tmp, "greenllm.cu")]
-    cmd[1:1] = os.environ.get("AB_FLAGS", "").split()  # e.g. AB_FLAGS="-Xptxas -O2"
     subprocess.check_call(cmd)
     print("built", name)
 
 
-names = sys.argv[1:] or list(VARIANTS)
-for n in names:
-    base_name = n.split("@")[0]  # "<variant>@<tag>": the same edits under AB_FLAGS
-    build(n, VARIANTS[base_name])
+if __name__ == "__main__":
+    args = sys.argv[1:]
+    if not args:
+        sys.exit(__doc__)
+    name, rest = args[0], args[1:]
+    defines = [a for a in rest if a.startswith("-D")]
+    edits = []
+    if "--patch" in rest:
+        edits = runpy.run_path(rest[rest.index("--patch") + 1])["EDITS"]
+    build(name, defines, edits)
