@@ -1,9 +1,17 @@
+# One GPU session's measurements (run under gpurun from the repo root):
+#   the GPU test suite, smoke, the microbenchmarked latencies, the bench line for
+#   configs 4 / 5 / 7, the ncu launch list of the bench step, and --set full captures
+#   of the dominant kernel (k_decode, config 4) and of the config-5 prologue kernels.
+# Everything lands in gpurun_out/ with the prefix $TAG (e.g. r02c).
 set -x
-python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err
-cat gpurun_out/bench.json
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/b_ncu.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_decode -s 3 -c 1 -o gpurun_out/kdec python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/kdec.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:k_stages -s 3 -c 1 -o gpurun_out/kst python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/kst.log 2>&1
-ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_an.csv python scripts/prof_analysis.py > gpurun_out/an_ncu.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_link_window|k_savings|k_als|k_dsd_demand" -c 8 -o gpurun_out/an python scripts/prof_analysis.py > gpurun_out/an_full.log 2>&1
+TAG=${TAG:-run}
+python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
+timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/${TAG}_pytest_gpu.log
+nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/lat scripts/ubench/lat.cu && /tmp/lat > gpurun_out/${TAG}_lat.txt 2>&1
+python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
+python bench.py --config 5 --steps 5 > gpurun_out/${TAG}_bench_cfg5.json 2> gpurun_out/${TAG}_bench_cfg5.err
+python bench.py --config 7 --steps 10 > gpurun_out/${TAG}_bench_cfg7.json 2> gpurun_out/${TAG}_bench_cfg7.err
+ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/${TAG}_b_ncu.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:k_decode -s 3 -c 1 -f -o gpurun_out/${TAG}_kdec python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/${TAG}_kdec.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_dsd_family|k_stages|k_stage_clone|k_finalize" -s 4 -c 4 -f -o gpurun_out/${TAG}_cfg5pro python bench.py --config 5 --steps 1 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/${TAG}_cfg5pro.log 2>&1
 ls -la gpurun_out
