@@ -1,4 +1,4 @@
-"""Per-chain decode time of config 4, one launch per chain: the speculative
+"""Per-chain decode time of a config (default 4), one launch per chain: the speculative
 k_decode (gl_eval_grid) and the leader-only serial walk k_decode_log
 (gl_link_demand), plus the request count of the chain's decode stream."""
 import sys
@@ -8,6 +8,7 @@ sys.path.insert(0, '.')
 from paper_2412_20322_b200 import api, native as N
 from paper_2412_20322_b200.inputs import build_config
 cfg = int(sys.argv[1]) if len(sys.argv) > 1 else 4
+walk_too = "--no-walk" not in sys.argv
 g = build_config(cfg)
 dg = api.DeviceGrid(g)
 N.profile_enable(True)
@@ -19,9 +20,11 @@ for ci in range(len(g.chains)):
     api.eval_grid(dg, ci, ci + 1, stats=st)
     torch.cuda.synchronize()
     kt = dict(N.kernel_times())
-    api.link_demand(dg, chain_lo=ci, chain_hi=ci + 1)
-    torch.cuda.synchronize()
-    kl = dict(N.kernel_times())
+    kl = {}
+    if walk_too:
+        api.link_demand(dg, chain_lo=ci, chain_hi=ci + 1)
+        torch.cuda.synchronize()
+        kl = dict(N.kernel_times())
     ch = g.chains[ci]
     M = int((g.traces[ch.trace_idx].output_len > 1).sum())
     dec = kt.get('k_decode', kt.get('k_decode_colo', 0.0))
