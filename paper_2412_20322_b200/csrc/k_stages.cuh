@@ -703,18 +703,27 @@ __global__ void __launch_bounds__(256)
     const bool dsd = ch.mode == GL_MODE_DSD;
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    for (int64_t q = t0; q < (int64_t)M + DEC_TAIL; q += stride) {
+    auto demand = [&](uint32_t j) -> uint32_t {
+        if (dsd) return __ldg(ch.K + j);
+        return min(max(__ldg(ch.o + j), 1u), O_LIMIT - 1) - 1u;
+    };
+    // four entries per thread and trip (two 16-B loads of the primary's (d, j), four
+    // independent demand loads, two 16-B stores): the stream is 16-B aligned (entry
+    // offsets are multiples of 32), so only the sentinel tail is written one by one
+    const int64_t Q = (int64_t)M + DEC_TAIL, Q4 = (int64_t)M / 4;
+    const uint4 *src4 = reinterpret_cast<const uint4 *>(pc.dec_dj);
+    uint4 *dst4 = reinterpret_cast<uint4 *>(ch.dec_dj);
+    for (int64_t q4 = t0; q4 < Q4; q4 += stride) {
+        const uint4 a = __ldcg(src4 + 2 * q4), b = __ldcg(src4 + 2 * q4 + 1);
+        const uint32_t d0 = demand(a.y), d1 = demand(a.w), d2 = demand(b.y), d3 = demand(b.w);
+        dst4[2 * q4] = make_uint4(d0, a.y, d1, a.w);
+        dst4[2 * q4 + 1] = make_uint4(d2, b.y, d3, b.w);
+    }
+    for (int64_t q = 4 * Q4 + t0; q < Q; q += stride) {
         uint2 v = make_uint2(0u, 0u);  // tail: "no request" (dec_r's sentinels are shared)
         if (q < M) {
             const uint32_t j = __ldcg(&pc.dec_dj[q].y);
-            uint32_t d;
-            if (dsd) {
-                d = __ldg(ch.K + j);
-            } else {
-                const uint32_t o = min(max(__ldg(ch.o + j), 1u), O_LIMIT - 1);
-                d = o - 1u;
-            }
-            v = make_uint2(d, j);
+            v = make_uint2(demand(j), j);
         }
         ch.dec_dj[q] = v;
     }

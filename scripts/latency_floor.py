@@ -10,8 +10,8 @@ Inputs (both reproducible from committed sources):
   * the SASS of k_decode<1, false, false> from the built libgreenllm.so.
 
 The light loop (decode_run's "light-load fast path", k_decode.cuh) of the LEADER warp is
-located in the SASS (the first loop block holding the two IMAD.HI.U32 of the Lemire
-ceil-division), and its two event paths are walked through the control flow:
+located in the SASS (the first loop head whose block holds the IMAD.HI.U32 of the
+reciprocal ceil-division and whose body stores finish times and reduces with CREDUX), and its two event paths are walked through the control flow:
   J  the head joins at T + kJ * step[b]   (decision branch taken)
   L  one member leaves at iteration fmin  (decision branch not taken, one-leave branch taken)
 Every other conditional branch on a path takes its common-case direction (no exit, no
@@ -226,29 +226,29 @@ def parse(ins):
 
 # ---------------------------------------------------------------- the light loop's paths
 def find_loop(sass):
-    addrs = [a for a, _ in sass]
-    targets = set()
+    """The leader's light loop: the first innermost loop (a branch target t with a
+    backward branch to it from past the instruction) around an IMAD.HI.U32 that is
+    small (< 200 instructions) and holds both paths: the leave's VOTE / POPC / CREDUX
+    and the finish-time store to the rows (STG)."""
+    back = collections.defaultdict(list)  # target -> addresses branching back to it
     for a, s in sass:
-        _, _, _, _, tgt = parse(s)
-        if tgt is not None:
-            targets.add(tgt)
-    his = [i for i, (_, s) in enumerate(sass) if opcode(s) == "IMAD.HI.U32"]
-    for i0, i1 in zip(his, his[1:]):
-        if i1 - i0 > 8:
+        tgt = parse(s)[4]
+        if tgt is not None and tgt <= a:
+            back[tgt].append(a)
+    for x, s in sass:
+        if opcode(s) != "IMAD.HI.U32":
             continue
-        # block start: the closest branch target at or before the pair
-        cands = [t for t in targets if t <= sass[i0][0]]
-        if not cands:
+        # innermost: the smallest span [t, last back branch] holding x (jumps back from
+        # the divergence stubs at the end of the function span far more)
+        spans = [(max(srcs) - t, t) for t, srcs in back.items() if t <= x < max(srcs)]
+        if not spans:
             continue
-        head = max(cands)
-        # a backward branch to `head` must exist (it is a loop head)
-        back = [a for a, s in sass if parse(s)[4] == head and a > head]
-        # the leader's light loop: the loop body stores finish times with STG (rows)
-        hi = max(back) if back else head
-        body = [s for a, s in sass if head <= a <= hi]
-        if back and any(opcode(s).startswith("STG") for s in body) and \
-                any(opcode(s).startswith("CREDUX") for s in body):
-            return head, addrs
+        head = min(spans)[1]
+        hi = max(back[head])
+        body = {opcode(s2) for a2, s2 in sass if head <= a2 <= hi}
+        n = sum(1 for a2, _ in sass if head <= a2 <= hi)
+        if n < 200 and {"STG.E.64", "CREDUX.MIN", "VOTE.ANY", "POPC"} <= body:
+            return head, [a2 for a2, _ in sass]
     raise SystemExit("light loop not found")
 
 
