@@ -19,7 +19,7 @@
  *    implements the same rules independently.
  *  - "device" = CUDA device memory of the current device; "host" = CPU memory.
  *  - The caller owns every buffer.  The library keeps no global state besides
- *    a cached device-capability check and, per host thread and device, two side
+ *    a cached device-capability check and, per host thread and device, four side
  *    streams with their events (created on first use, kept for the process);
  *    it allocates only stream-ordered scratch (cudaMallocAsync / cudaFreeAsync
  *    on `stream`) and never synchronises except in gl_evaluate_host.  When one
@@ -48,7 +48,7 @@
 extern "C" {
 #endif
 
-#define GL_VERSION 2  /* 2: carbon_per_token_out in gl_argmin_feasible */
+#define GL_VERSION 3  /* 2: carbon_per_token_out in gl_argmin_feasible; 3: gl_schedule hints */
 #define GL_MAX_CAP 256        /* batch cap: 8 active-set slots per lane x 32 lanes */
 #define GL_MAX_GAMMA 16       /* DSD draft length */
 #define GL_MAX_PROMPT 16384   /* prompt-indexed tables live in shared memory */
@@ -180,6 +180,29 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
                        void *stream);
 
 /*
+ * Launch-order hint.  The step lasts as long as its slowest chain's serial decode
+ * walk, and that walk can only start once the chain's DSD demand and
+ * stage scans exist.  With a hint, the chains [first_lo, first_hi) -- e.g. the
+ * trace predicted to hold the slowest chain -- run first: their DSD demand, stage
+ * scans (and those of the primaries they copy from) and segment starts, then their
+ * decode on a side stream forked from `stream`, while the other chains' prologue
+ * kernels and decodes follow on `stream` (and a second side stream); both are
+ * joined back before the per-request SLO pass, so the call stays ordered on
+ * `stream`.  Results never depend on the hint (outputs are bit-identical with or
+ * without it).  Ignored when the call holds co-located chains, for gl_link_demand,
+ * and for an empty or full range.
+ *   first_lo, first_hi   0 <= first_lo <= first_hi <= n_chains, else GL_E_INVALID
+ */
+typedef struct {
+    int32_t first_lo, first_hi;
+} gl_schedule;
+
+/* gl_eval_grid with an optional launch-order hint (NULL: as gl_eval_grid). */
+gl_status gl_eval_grid_sched(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
+                             int32_t n_chains, gl_chain_stats *stats_out,
+                             int64_t *per_request_out, const gl_schedule *sched, void *stream);
+
+/*
  * Alg. 1 on the carbon matrix of Eqs. 1-3:
  *   total = ((e_new/3.6e12) + (e_old/3.6e12)) * CI
  *         + ((busy_new/1e6)/LT_new)*Ce_new + ((busy_old/1e6)/LT_old)*Ce_old
@@ -229,6 +252,16 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces,
                            gl_chain_stats *stats_host, double *carbon_host,
                            double *carbon_per_token_host, int32_t *choice_host,
                            uint8_t *via_fallback_host, void *stream);
+
+/* gl_evaluate_host with an optional launch-order hint (as gl_eval_grid_sched). */
+gl_status gl_evaluate_host_sched(const gl_trace *host_traces, int32_t n_traces,
+                                 const gl_chain *chains, int32_t n_chains,
+                                 const gl_scenario *scen, int32_t n_scen, const gl_grid *grid,
+                                 int32_t slo_num, int32_t slo_den, int32_t priority,
+                                 int32_t default_col, gl_chain_stats *stats_host,
+                                 double *carbon_host, double *carbon_per_token_host,
+                                 int32_t *choice_host, uint8_t *via_fallback_host,
+                                 const gl_schedule *sched, void *stream);
 
 /* ---- Link bandwidth demand (Fig. 4, "bandwidth
  * requirement"; "peak bandwidth demand over a 1 s sliding window").
@@ -357,6 +390,10 @@ int32_t gl_last_launch_count(void);
  * many it wrote (names are static strings).  Disabled by default. */
 gl_status gl_profile_enable(int32_t on);
 int32_t gl_kernel_times(const char **names_out, float *ms_out, int32_t max);
+/* As gl_kernel_times, plus each kernel's start in milliseconds after the first
+ * recorded kernel's (the launches of one call may overlap on several streams). */
+int32_t gl_kernel_timeline(const char **names_out, float *start_ms_out, float *ms_out,
+                           int32_t max);
 const char *gl_strerror(gl_status status);
 int32_t gl_version(void);
 

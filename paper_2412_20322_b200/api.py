@@ -10,6 +10,7 @@ import numpy as np
 import torch
 
 from . import native as N
+from . import schedule as S
 from .inputs.grids import GridSpec
 
 
@@ -66,6 +67,14 @@ class DeviceGrid:
         self._arr_cache = {}  # ctypes descriptor arrays, built once per (kind, lo, hi)
         self.chain_n = np.array([grid.traces[c.trace_idx].n for c in grid.chains], np.int64)
         self.last_launches = 0
+        self._sched = {}
+
+    def first_range(self, lo: int = 0, hi: int | None = None):
+        """The launch-order hint for chains [lo, hi) (schedule.first_range), cached."""
+        hi = self.n_chains if hi is None else hi
+        if (lo, hi) not in self._sched:
+            self._sched[(lo, hi)] = S.first_range(self.grid, lo, hi)
+        return self._sched[(lo, hi)]
 
     def chain_arr(self, lo: int = 0, hi: int | None = None):
         """gl_chain[lo:hi] as a cached ctypes array (the descriptors never change)."""
@@ -103,11 +112,14 @@ def _stream_ptr(stream) -> int:
 
 
 def eval_grid(dg: DeviceGrid, chain_lo: int = 0, chain_hi: int | None = None, stats=None,
-              per_request: bool = False, stream=None, traces=None):
+              per_request: bool = False, stream=None, traces=None, schedule=False):
     """Simulate chains [chain_lo, chain_hi) -> (stats uint8 tensor [k, 80], per-request
     int64 tensor [sum n, 2] or None).  ``stats`` may be a preallocated view.
     ``traces`` = [(arrival, prompt, output) device tensors] per trace replaces the
-    grid's resident copies (e.g. buffers just copied from the host)."""
+    grid's resident copies (e.g. buffers just copied from the host).  ``schedule``:
+    False = no launch-order hint (the default: measured no faster, see schedule.py),
+    True = the predicted hint (schedule.first_range), or an explicit (first_lo,
+    first_hi) relative to chain_lo; results never depend on it."""
     hi = dg.n_chains if chain_hi is None else chain_hi
     chains = dg.chain_arr(chain_lo, hi)
     k = len(chains)
@@ -126,8 +138,10 @@ def eval_grid(dg: DeviceGrid, chain_lo: int = 0, chain_hi: int | None = None, st
             assert a.is_cuda and p.is_cuda and o.is_cuda
         tr = [N.GlTrace(a.data_ptr(), p.data_ptr(), o.data_ptr(), a.numel())
               for (a, p, o) in traces]
+    sched = dg.first_range(chain_lo, hi) if schedule is True else (schedule or None)
     dg.last_launches = N.eval_grid(tr, chains, stats.data_ptr(),
-                                   pr.data_ptr() if pr is not None else None, _stream_ptr(stream))
+                                   pr.data_ptr() if pr is not None else None, _stream_ptr(stream),
+                                   sched=sched)
     return stats, pr
 
 
@@ -255,8 +269,10 @@ class HostResult:
 
 
 def evaluate_host(dg: DeviceGrid, host_traces, want_carbon: bool = False, stream=None,
-                  out: HostResult | None = None, want_per_token: bool = False) -> HostResult:
-    """End to end through gl_evaluate_host: pinned host traces in, host results out."""
+                  out: HostResult | None = None, want_per_token: bool = False,
+                  schedule=False) -> HostResult:
+    """End to end through gl_evaluate_host_sched: pinned host traces in, host results
+    out (``schedule`` as for eval_grid)."""
     g = dg.grid
     gl_tr = [N.GlTrace(a.data_ptr(), p.data_ptr(), o.data_ptr(), a.shape[0])
              for (a, p, o) in host_traces]
@@ -273,7 +289,8 @@ def evaluate_host(dg: DeviceGrid, host_traces, want_carbon: bool = False, stream
                                    g.row_scenario, g.cell_chain, g.slo_num, g.slo_den, g.priority,
                                    g.default_col, out.stats, out.carbon, out.choice,
                                    out.via_fallback, _stream_ptr(stream),
-                                   per_token_out=out.carbon_per_token)
+                                   per_token_out=out.carbon_per_token,
+                                   sched=dg.first_range() if schedule is True else (schedule or None))
     seen = set()
     h2d = 0
     for arrs in host_traces:

@@ -187,7 +187,7 @@ struct SideStream {
 };
 bool side_fork(int slot, cudaStream_t from, cudaStream_t &side, cudaEvent_t &join)
 {
-    thread_local SideStream tl[16][2];  // [device][slot]
+    thread_local SideStream tl[16][4];  // [device][slot]
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) {
         cudaGetLastError();
@@ -227,7 +227,8 @@ struct LinkReq {
 gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
                     int32_t n_chains, gl_chain_stats *stats_out, int64_t *per_request_out,
                     cudaStream_t stream, const LinkReq *lk,
-                    cudaEvent_t stages_wait = nullptr)  // k_stages waits for it (host path)
+                    cudaEvent_t stages_wait = nullptr,  // k_stages waits for it (host path)
+                    const gl_schedule *sched = nullptr)
 {
     gl_status st = validate_traces(traces, n_traces);
     if (st) return st;
@@ -440,6 +441,42 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         }
     }
     const int32_t n_prim = (int32_t)prim_ids.size(), n_sec = (int32_t)sec_ids.size();
+    // Two-phase launch order (gl_schedule): phase A = the hinted chain range
+    // [s_lo, s_hi) for the decode, plus, for the prologue, the primaries its
+    // secondaries copy from and every DSD group / family those chains use.  Not for
+    // co-located chains (their decode overlaps on a side stream already) or the link
+    // analysis; an empty or full range is one phase.
+    const int32_t s_lo = sched ? sched->first_lo : 0, s_hi = sched ? sched->first_hi : 0;
+    const bool phased = sched && !lk && !has_colo && s_lo < s_hi && !(s_lo == 0 && s_hi == n_chains);
+    int32_t fam_a = 0, solo_a = 0, prim_a = 0, sec_a = 0;
+    if (phased) {
+        std::vector<char> stage_a(n_chains, 0), group_a(groups.size(), 0);
+        for (int32_t c = s_lo; c < s_hi; ++c) stage_a[c] = stage_a[prim_of[c]] = 1;
+        for (int32_t c = 0; c < n_chains; ++c)
+            if (stage_a[c] && chain_group[c] >= 0) group_a[chain_group[c]] = 1;
+        auto is_a = [&](int32_t c) { return stage_a[c] != 0; };
+        prim_a = (int32_t)(std::stable_partition(prim_ids.begin(), prim_ids.end(), is_a) - prim_ids.begin());
+        sec_a = (int32_t)(std::stable_partition(sec_ids.begin(), sec_ids.end(), is_a) - sec_ids.begin());
+        solo_a = (int32_t)(std::stable_partition(solo.begin(), solo.end(),
+                                                 [&](int g) { return group_a[g] != 0; }) - solo.begin());
+        std::vector<size_t> order(fams.size());
+        for (size_t f = 0; f < fams.size(); ++f) order[f] = f;
+        auto fam_in_a = [&](size_t f) {
+            for (auto &gs : fam_slots[f])
+                if (group_a[gs.first]) return true;
+            return false;
+        };
+        fam_a = (int32_t)(std::stable_partition(order.begin(), order.end(), fam_in_a) - order.begin());
+        std::vector<gl::DFamily> f2;
+        std::vector<std::vector<std::pair<int, int>>> s2;
+        for (size_t f : order) {
+            f2.push_back(fams[f]);
+            s2.push_back(fam_slots[f]);
+        }
+        fams.swap(f2);
+        fam_slots.swap(s2);
+    }
+    const bool use_ids = phased || n_sec > 0;  // k_stages reads its primaries from a list
     // k_stages: S blocks per chain (decoupled look-back between them), S <= 4 chosen
     // to minimise the waves per chain's work, ceil(chains S / resident) / S (ties to
     // the smaller S): 2 on config 4's 64 chains, 3 on config 6's 80, 4 on config 5's 320
@@ -555,7 +592,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                             cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess) e = cudaMemsetAsync(scratch + off_zero, 0, zero_bytes, stream);
     std::vector<int32_t> idv;  // (kept alive until the copy is enqueued: pageable, synchronous staging)
-    if (e == cudaSuccess && n_sec > 0) {  // after the memset: the ids live in the zeroed region
+    if (e == cudaSuccess && use_ids) {  // after the memset: the ids live in the zeroed region
         idv = prim_ids;
         idv.insert(idv.end(), sec_ids.begin(), sec_ids.end());
         idv.insert(idv.end(), prim_of.begin(), prim_of.end());
@@ -565,104 +602,106 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     if (e == cudaSuccess && lk)  // log sentinels: every byte 0xFF -> (T, b) = (-1, -1)
         e = cudaMemsetAsync(scratch + off_ev, 0xFF, sizeof(longlong2) * (size_t)ev_total, stream);
     int launches = 0;
-    if (e == cudaSuccess && !fams.empty()) {
+    // ---- kernels over a phase: families [f0, f1), solo groups [g0, g1), primaries
+    // [p0, p1) and secondaries [s0, s1) of the device id lists, chains [c0, c1)
+    auto launch_family = [&](int32_t f0, int32_t f1) {
+        if (e != cudaSuccess || f1 <= f0) return;
         // persistent threads: about 8 resident blocks of 128 threads per SM in total,
         // spread over the families, never more than one thread per request
         int64_t fmax = 0;
-        for (auto &f : fams) fmax = std::max(fmax, f.n);
-        const int64_t want = std::max<int64_t>(1, (8 * (int64_t)n_sm) / (int64_t)fams.size());
+        for (int32_t f = f0; f < f1; ++f) fmax = std::max(fmax, fams[f].n);
+        const int64_t want = std::max<int64_t>(1, (8 * (int64_t)n_sm) / (int64_t)(f1 - f0));
         const int64_t need_b = (fmax + 127) / 128;
-        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, need_b)), (unsigned)fams.size());
+        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, need_b)), (unsigned)(f1 - f0));
         prof_begin("k_dsd_family", stream);
         gl::k_dsd_family<<<grid, 128, 0, stream>>>(
-            reinterpret_cast<const gl::DFamily *>(scratch + off_fams));
+            reinterpret_cast<const gl::DFamily *>(scratch + off_fams) + f0);
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;
-    }
-    if (e == cudaSuccess && !solo_groups.empty()) {
+    };
+    auto launch_solo = [&](int32_t g0, int32_t g1) {
+        if (e != cudaSuccess || g1 <= g0) return;
         // persistent quads: about 16 resident blocks of 256 threads per SM in total,
         // spread over the groups, never more than one quad per request
         int64_t gmax = 0;
-        for (auto &g : solo_groups) gmax = std::max(gmax, g.n);
-        const int64_t want = std::max<int64_t>(1, (16 * (int64_t)n_sm) / (int64_t)solo_groups.size());
+        for (int32_t g = g0; g < g1; ++g) gmax = std::max(gmax, solo_groups[g].n);
+        const int64_t want = std::max<int64_t>(1, (16 * (int64_t)n_sm) / (int64_t)(g1 - g0));
         const int64_t need_b = (gmax * gl::DSD_QL + 255) / 256;
-        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, need_b)), (unsigned)solo_groups.size());
+        dim3 grid((unsigned)std::max<int64_t>(1, std::min(want, need_b)), (unsigned)(g1 - g0));
         prof_begin("k_dsd_demand", stream);
         gl::k_dsd_demand<<<grid, 256, 0, stream>>>(
-            reinterpret_cast<const DGroup *>(scratch + off_groups));
+            reinterpret_cast<const DGroup *>(scratch + off_groups) + g0);
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;
-    }
-    // gl_evaluate_host: the arrival arrays may still be in flight on a copy stream
-    // (k_dsd_demand above needs only the output lengths)
-    if (e == cudaSuccess && stages_wait) e = cudaStreamWaitEvent(stream, stages_wait, 0);
-    if (e == cudaSuccess) {
+    };
+    bool waited = false;  // gl_evaluate_host: the arrival arrays may still be in flight
+    auto launch_stages = [&](int32_t p0, int32_t p1, int32_t ticket_slot) {
+        if (e == cudaSuccess && stages_wait && !waited) {
+            e = cudaStreamWaitEvent(stream, stages_wait, 0);
+            waited = true;
+        }
+        if (e != cudaSuccess || p1 <= p0) return;
         e = cudaFuncSetAttribute(gl::k_stages, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_st);
-        if (e == cudaSuccess) {
-            prof_begin("k_stages", stream);
-            gl::k_stages<<<n_prim * stage_split, 32 * gl::ST_WARPS, smem_st, stream>>>(
-                dc, stats_out, rows, stage_split, reinterpret_cast<int32_t *>(scratch + off_ticket),
-                n_sec > 0 ? d_prim_ids : nullptr);
-            e = cudaGetLastError();
-            prof_end(stream);
-            ++launches;
-        }
-    }
+        if (e != cudaSuccess) return;
+        prof_begin("k_stages", stream);
+        gl::k_stages<<<(p1 - p0) * stage_split, 32 * gl::ST_WARPS, smem_st, stream>>>(
+            dc, stats_out, rows, stage_split,
+            reinterpret_cast<int32_t *>(scratch + off_ticket) + ticket_slot,
+            use_ids ? d_prim_ids + p0 : nullptr);
+        e = cudaGetLastError();
+        prof_end(stream);
+        ++launches;
+    };
     // rows are an output (or feed the link analysis): secondaries get full copies
     const bool copy_rows = per_request_out != nullptr || lk != nullptr;
-    if (e == cudaSuccess && n_sec > 0) {
-        const int bpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, (8 * (int64_t)n_sm + n_sec - 1) / n_sec));
+    auto launch_clone = [&](int32_t s0, int32_t s1) {
+        if (e != cudaSuccess || s1 <= s0) return;
+        const int32_t ns = s1 - s0;
+        const int bpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, (8 * (int64_t)n_sm + ns - 1) / ns));
         prof_begin("k_stage_clone", stream);
-        gl::k_stage_clone<<<dim3((unsigned)bpc, (unsigned)n_sec), 256, 0, stream>>>(
-            dc, stats_out, rows, d_sec_ids, d_prim_of, stage_split, copy_rows ? 1 : 0);
+        gl::k_stage_clone<<<dim3((unsigned)bpc, (unsigned)ns), 256, 0, stream>>>(
+            dc, stats_out, rows, d_sec_ids + s0, d_prim_of, stage_split, copy_rows ? 1 : 0);
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;
-    }
-    if (e == cudaSuccess && extra == 0) {
-        // no helper warps (many chains): each leader walks its chain alone, one segment
+    };
+    auto launch_segments = [&](int32_t c0, int32_t c1) {
+        if (e != cudaSuccess || c1 <= c0) return;
         prof_begin("k_segments", stream);
-        gl::k_segments_single<<<(unsigned)((n_chains + 127) / 128), 128, 0, stream>>>(dc, n_chains);
+        if (extra == 0) {
+            // no helper warps (many chains): each leader walks its chain alone, one segment
+            gl::k_segments_single<<<(unsigned)((c1 - c0 + 127) / 128), 128, 0, stream>>>(dc + c0, c1 - c0);
+        } else {
+            // 1024-thread blocks, one per SM; S per chain while they fit in a wave
+            const int seg_split = std::max(1, std::min(4, n_sm / std::max(1, (int)n_chains)));
+            gl::k_segments<<<(c1 - c0) * seg_split, 1024, 0, stream>>>(
+                dc + c0, seg_split, (int64_t)((off_segwc - off_segs) / sizeof(int32_t)));
+        }
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;
-    } else if (e == cudaSuccess) {
-        prof_begin("k_segments", stream);
-        // k_segments: 1024-thread blocks, one per SM; S per chain while they fit in a wave
-        const int seg_split = std::max(1, std::min(4, n_sm / std::max(1, (int)n_chains)));
-        gl::k_segments<<<n_chains * seg_split, 1024, 0, stream>>>(
-            dc, seg_split, (int64_t)((off_segwc - off_segs) / sizeof(int32_t)));
-        e = cudaGetLastError();
-        prof_end(stream);
-        ++launches;
-    }
-    if (e == cudaSuccess) {
-        const unsigned blocks = (unsigned)(n_chains * (1 + extra));
-        cudaStream_t dec_stream = stream;  // the co-located launch may run on a side stream
+    };
+    // decode launches over chains [c0, c1) on `dstream`: disaggregated chains, then
+    // co-located ones (each launch skips the other family's chains)
+    auto launch_decode = [&](int32_t c0, int32_t c1, cudaStream_t dstream, cudaStream_t colo_stream) {
+        if (e != cudaSuccess || c1 <= c0) return;
+        const int32_t nc = c1 - c0;
+        const unsigned blocks = (unsigned)(nc * (1 + extra));
+        cudaStream_t ds = dstream;
         auto launch = [&](auto kern, const char *name) {
             cudaError_t r = cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem_dec);
             if (r != cudaSuccess) return r;
-            prof_begin(name, dec_stream);
-            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, dec_stream>>>(dc, stats_out, rows,
-                                                                      (int32_t)n_chains);
+            prof_begin(name, ds);
+            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, ds>>>(dc + c0, stats_out + c0, rows, nc);
             r = cudaGetLastError();
-            prof_end(dec_stream);
+            prof_end(ds);
             ++launches;
             return r;
         };
-        // Both families present (configuration 6): the co-located launch goes to a
-        // side stream forked from `stream` and joined back, so the two launches
-        // (disjoint chains) overlap; the call stays stream-ordered on `stream`.
-        cudaStream_t side = nullptr;
-        cudaEvent_t ev_join = nullptr;
-        if (has_disg && has_colo && !lk && !side_fork(0, stream, side, ev_join)) {
-            side = nullptr;  // no fork: both launches stay on `stream` (serialised)
-        }
-        // disaggregated chains, then co-located ones (each launch skips the others)
         if (has_disg && lk) {  // runs that also log the batch size
             if (max_cap <= 31)
                 e = launch(gl::k_decode<1, false, true>, "k_decode_log");
@@ -683,7 +722,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                 e = launch(gl::k_decode<8, false>, "k_decode");
         }
         if (has_colo && e == cudaSuccess) {
-            if (side) dec_stream = side;
+            ds = colo_stream;
             if (max_cap <= 31)  // the one-row fast paths need b < 32
                 e = launch(gl::k_decode<1, true>, "k_decode_colo");
             else if (max_cap <= 64)
@@ -692,13 +731,55 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                 e = launch(gl::k_decode<4, true>, "k_decode_colo");
             else
                 e = launch(gl::k_decode<8, true>, "k_decode_colo");
-            dec_stream = stream;
         }
-        if (side) {  // join the side stream back into `stream`
-            cudaError_t r = cudaEventRecord(ev_join, side);
-            if (r == cudaSuccess) r = cudaStreamWaitEvent(stream, ev_join, 0);
-            if (e == cudaSuccess) e = r;
-        }
+    };
+    auto join = [&](cudaStream_t side, cudaEvent_t ev) {
+        if (!side) return;
+        cudaError_t r = cudaEventRecord(ev, side);
+        if (r == cudaSuccess) r = cudaStreamWaitEvent(stream, ev, 0);
+        if (e == cudaSuccess) e = r;
+    };
+    if (!phased) {
+        launch_family(0, (int32_t)fams.size());
+        launch_solo(0, (int32_t)solo_groups.size());
+        launch_stages(0, n_prim, 0);
+        launch_clone(0, n_sec);
+        launch_segments(0, n_chains);
+        // Both families present (configurations 6 and 7): the co-located launch goes
+        // to a side stream forked from `stream` and joined back, so the two launches
+        // (disjoint chains) overlap; the call stays stream-ordered on `stream`.
+        cudaStream_t side = nullptr;
+        cudaEvent_t ev_join = nullptr;
+        if (e == cudaSuccess && has_disg && has_colo && !lk && !side_fork(0, stream, side, ev_join))
+            side = nullptr;  // no fork: both launches stay on `stream` (serialised)
+        launch_decode(0, n_chains, stream, side ? side : stream);
+        join(side, ev_join);
+    } else {
+        // Phase A (the hinted chains and the primaries they copy from): DSD demand,
+        // stage scans, clones, segments, then its decode on a side stream; phase B's
+        // prologue runs on `stream` meanwhile, its decodes on `stream` and a second
+        // side stream; both joined before k_finalize.
+        launch_family(0, fam_a);
+        launch_solo(0, solo_a);
+        launch_stages(0, prim_a, 0);
+        launch_clone(0, sec_a);
+        launch_segments(s_lo, s_hi);
+        cudaStream_t sa = nullptr, sb = nullptr;
+        cudaEvent_t ja = nullptr, jb = nullptr;
+        if (e == cudaSuccess && !side_fork(2, stream, sa, ja)) sa = nullptr;
+        launch_decode(s_lo, s_hi, sa ? sa : stream, nullptr);
+        launch_family(fam_a, (int32_t)fams.size());
+        launch_solo(solo_a, (int32_t)solo_groups.size());
+        launch_stages(prim_a, n_prim, 1);
+        launch_clone(sec_a, n_sec);
+        launch_segments(0, s_lo);
+        launch_segments(s_hi, n_chains);
+        if (e == cudaSuccess && s_hi < n_chains && s_lo > 0 && !side_fork(3, stream, sb, jb))
+            sb = nullptr;
+        launch_decode(s_hi, n_chains, sb ? sb : stream, nullptr);
+        launch_decode(0, s_lo, stream, nullptr);
+        join(sa, ja);
+        join(sb, jb);
     }
     if (e == cudaSuccess) {
         const int per_thread = 8;
@@ -749,10 +830,21 @@ gl_status gl_eval_grid(const gl_trace *traces, int32_t n_traces, const gl_chain 
                        int32_t n_chains, gl_chain_stats *stats_out, int64_t *per_request_out,
                        void *stream_)
 {
+    return gl_eval_grid_sched(traces, n_traces, chains, n_chains, stats_out, per_request_out,
+                              nullptr, stream_);
+}
+
+gl_status gl_eval_grid_sched(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
+                             int32_t n_chains, gl_chain_stats *stats_out,
+                             int64_t *per_request_out, const gl_schedule *sched, void *stream_)
+{
     g_last_launches = 0;
     if (!stats_out) return GL_E_INVALID;
+    if (sched && (sched->first_lo < 0 || sched->first_lo > sched->first_hi ||
+                  sched->first_hi > n_chains))
+        return GL_E_INVALID;
     return eval_impl(traces, n_traces, chains, n_chains, stats_out, per_request_out,
-                     static_cast<cudaStream_t>(stream_), nullptr);
+                     static_cast<cudaStream_t>(stream_), nullptr, nullptr, sched);
 }
 
 gl_status gl_link_demand(const gl_trace *traces, int32_t n_traces, const gl_chain *chains,
@@ -1041,6 +1133,24 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
                            double *carbon_host, double *per_token_host, int32_t *choice_host,
                            uint8_t *via_fallback_host, void *stream_)
 {
+    return gl_evaluate_host_sched(host_traces, n_traces, chains, n_chains, scen, n_scen, grid,
+                                  slo_num, slo_den, priority, default_col, stats_host,
+                                  carbon_host, per_token_host, choice_host, via_fallback_host,
+                                  nullptr, stream_);
+}
+
+gl_status gl_evaluate_host_sched(const gl_trace *host_traces, int32_t n_traces,
+                                 const gl_chain *chains, int32_t n_chains,
+                                 const gl_scenario *scen, int32_t n_scen, const gl_grid *grid,
+                                 int32_t slo_num, int32_t slo_den, int32_t priority,
+                                 int32_t default_col, gl_chain_stats *stats_host,
+                                 double *carbon_host, double *per_token_host,
+                                 int32_t *choice_host, uint8_t *via_fallback_host,
+                                 const gl_schedule *sched, void *stream_)
+{
+    if (sched && (sched->first_lo < 0 || sched->first_lo > sched->first_hi ||
+                  sched->first_hi > n_chains))
+        return GL_E_INVALID;
     cudaStream_t stream = static_cast<cudaStream_t>(stream_);
     gl_status st = validate_traces(host_traces, n_traces);
     if (st) return st;
@@ -1116,7 +1226,7 @@ gl_status gl_evaluate_host(const gl_trace *host_traces, int32_t n_traces, const 
         gl_chain_stats *dstats = reinterpret_cast<gl_chain_stats *>(dev + o_stats);
         g_last_launches = 0;
         st = eval_impl(dtr.data(), n_traces, chains, n_chains, dstats, nullptr, stream, nullptr,
-                       side ? ev_arr : nullptr);
+                       side ? ev_arr : nullptr, sched);
         launches += g_last_launches;
         if (st == GL_OK) {
             st = gl_argmin_feasible(dstats, n_chains, chains, scen, n_scen, grid, slo_num, slo_den,
@@ -1170,19 +1280,29 @@ gl_status gl_profile_enable(int32_t on)
     return GL_OK;
 }
 
-int32_t gl_kernel_times(const char **names_out, float *ms_out, int32_t max)
+int32_t gl_kernel_timeline(const char **names_out, float *start_ms_out, float *ms_out,
+                           int32_t max)
 {
     int32_t k = 0;
     for (int i = 0; i < g_prof.used && k < max; ++i) {
-        float ms = 0.f;
+        float ms = 0.f, t0 = 0.f;
         if (cudaEventElapsedTime(&ms, g_prof.ev[2 * i], g_prof.ev[2 * i + 1]) != cudaSuccess)
             ms = -1.f;
+        if (i > 0 && cudaEventElapsedTime(&t0, g_prof.ev[0], g_prof.ev[2 * i]) != cudaSuccess)
+            t0 = -1.f;
         if (names_out) names_out[k] = g_prof.names[i];
+        if (start_ms_out) start_ms_out[k] = t0;
         if (ms_out) ms_out[k] = ms;
         ++k;
     }
+    cudaGetLastError();
     g_prof.used = 0;
     return k;
+}
+
+int32_t gl_kernel_times(const char **names_out, float *ms_out, int32_t max)
+{
+    return gl_kernel_timeline(names_out, nullptr, ms_out, max);
 }
 
 const char *gl_strerror(gl_status s)

@@ -78,9 +78,16 @@ class GlSavingsPair(C.Structure):
 
 SCEN_DTYPE = np.dtype([("ci", "<f8"), ("lt_new", "<f8"), ("lt_old", "<f8")])
 
-EXPORTS = ("gl_eval_grid", "gl_argmin_feasible", "gl_evaluate_host", "gl_link_demand",
+
+class GlSchedule(C.Structure):
+    """Launch-order hint (greenllm.h gl_schedule): chains [first_lo, first_hi) first."""
+    _fields_ = [("first_lo", C.c_int32), ("first_hi", C.c_int32)]
+
+EXPORTS = ("gl_eval_grid", "gl_eval_grid_sched", "gl_argmin_feasible", "gl_evaluate_host",
+           "gl_evaluate_host_sched", "gl_link_demand",
            "gl_savings_surface", "gl_complete_matrices", "gl_argmin_matrices", "gl_last_launch_count",
-           "gl_profile_enable", "gl_kernel_times", "gl_strerror", "gl_version")
+           "gl_profile_enable", "gl_kernel_times", "gl_kernel_timeline", "gl_strerror",
+           "gl_version")
 
 _lib = None
 
@@ -102,6 +109,9 @@ def lib():
         vp, i32 = C.c_void_p, C.c_int32
         L.gl_eval_grid.restype = i32
         L.gl_eval_grid.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32, vp, vp, vp]
+        L.gl_eval_grid_sched.restype = i32
+        L.gl_eval_grid_sched.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32, vp, vp,
+                                         C.POINTER(GlSchedule), vp]
         L.gl_argmin_feasible.restype = i32
         L.gl_argmin_feasible.argtypes = [vp, i32, C.POINTER(GlChain), C.POINTER(GlScenario), i32,
                                          C.POINTER(GlGrid), i32, i32, i32, i32, vp, vp, vp, vp,
@@ -110,6 +120,11 @@ def lib():
         L.gl_evaluate_host.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
                                        C.POINTER(GlScenario), i32, C.POINTER(GlGrid), i32, i32,
                                        i32, i32, vp, vp, vp, vp, vp, vp]
+        L.gl_evaluate_host_sched.restype = i32
+        L.gl_evaluate_host_sched.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
+                                             C.POINTER(GlScenario), i32, C.POINTER(GlGrid), i32,
+                                             i32, i32, i32, vp, vp, vp, vp, vp,
+                                             C.POINTER(GlSchedule), vp]
         L.gl_link_demand.restype = i32
         L.gl_link_demand.argtypes = [C.POINTER(GlTrace), i32, C.POINTER(GlChain), i32,
                                      C.POINTER(GlLinkParams), C.c_int64, vp, vp, vp]
@@ -127,6 +142,9 @@ def lib():
         L.gl_profile_enable.argtypes = [i32]
         L.gl_kernel_times.restype = i32
         L.gl_kernel_times.argtypes = [C.POINTER(C.c_char_p), C.POINTER(C.c_float), i32]
+        L.gl_kernel_timeline.restype = i32
+        L.gl_kernel_timeline.argtypes = [C.POINTER(C.c_char_p), C.POINTER(C.c_float),
+                                         C.POINTER(C.c_float), i32]
         L.gl_strerror.restype = C.c_char_p
         L.gl_strerror.argtypes = [i32]
         L.gl_version.restype = i32
@@ -151,11 +169,19 @@ def _scen_arr(scen):
     return s, s.ctypes.data_as(C.POINTER(GlScenario))
 
 
-def eval_grid(traces, chains, stats_ptr: int, per_request_ptr: int | None, stream: int):
+def eval_grid(traces, chains, stats_ptr: int, per_request_ptr: int | None, stream: int,
+              sched=None):
+    """sched: (first_lo, first_hi) launch-order hint (gl_eval_grid_sched) or None."""
     t_arr = _arr(GlTrace, traces)
     c_arr = _arr(GlChain, chains)
-    check(lib().gl_eval_grid(t_arr, len(traces), c_arr, len(chains), stats_ptr,
-                             per_request_ptr or None, stream or None), "gl_eval_grid")
+    if sched is None:
+        check(lib().gl_eval_grid(t_arr, len(traces), c_arr, len(chains), stats_ptr,
+                                 per_request_ptr or None, stream or None), "gl_eval_grid")
+    else:
+        sc = GlSchedule(int(sched[0]), int(sched[1]))
+        check(lib().gl_eval_grid_sched(t_arr, len(traces), c_arr, len(chains), stats_ptr,
+                                       per_request_ptr or None, C.byref(sc), stream or None),
+              "gl_eval_grid_sched")
     return lib().gl_last_launch_count()
 
 
@@ -217,25 +243,36 @@ def argmin_feasible(stats_ptr: int, chains, scen: np.ndarray, rows: int, cols: i
 def evaluate_host(host_traces, chains, scen, rows, cols, row_scenario, cell_chain, slo_num,
                   slo_den, priority, default_col, stats_out: np.ndarray, carbon_out,
                   choice_out: np.ndarray, fb_out: np.ndarray, stream: int,
-                  per_token_out: np.ndarray | None = None):
+                  per_token_out: np.ndarray | None = None, sched=None):
     t_arr = _arr(GlTrace, host_traces)
     c_arr = _arr(GlChain, chains)
     s, s_arr = _scen_arr(scen)
     rs = np.ascontiguousarray(row_scenario, dtype=np.int32)
     cc = np.ascontiguousarray(cell_chain, dtype=np.int32)
     g = GlGrid(rows, cols, rs.ctypes.data, cc.ctypes.data)
-    check(lib().gl_evaluate_host(t_arr, len(host_traces), c_arr, len(chains), s_arr, len(s),
-                                 C.byref(g), slo_num, slo_den, priority, default_col,
-                                 stats_out.ctypes.data,
-                                 None if carbon_out is None else carbon_out.ctypes.data,
-                                 None if per_token_out is None else per_token_out.ctypes.data,
-                                 choice_out.ctypes.data, fb_out.ctypes.data, stream or None),
-          "gl_evaluate_host")
+    sc = None if sched is None else GlSchedule(int(sched[0]), int(sched[1]))
+    check(lib().gl_evaluate_host_sched(t_arr, len(host_traces), c_arr, len(chains), s_arr,
+                                       len(s), C.byref(g), slo_num, slo_den, priority,
+                                       default_col, stats_out.ctypes.data,
+                                       None if carbon_out is None else carbon_out.ctypes.data,
+                                       None if per_token_out is None else per_token_out.ctypes.data,
+                                       choice_out.ctypes.data, fb_out.ctypes.data,
+                                       None if sc is None else C.byref(sc), stream or None),
+          "gl_evaluate_host_sched")
     return lib().gl_last_launch_count()
 
 
 def profile_enable(on: bool):
     check(lib().gl_profile_enable(1 if on else 0), "gl_profile_enable")
+
+
+def kernel_timeline(max_n: int = 256):
+    """[(kernel name, start ms after the first, ms)] since the last read (synchronised)."""
+    names = (C.c_char_p * max_n)()
+    t0 = (C.c_float * max_n)()
+    ms = (C.c_float * max_n)()
+    k = lib().gl_kernel_timeline(names, t0, ms, max_n)
+    return [(names[i].decode(), float(t0[i]), float(ms[i])) for i in range(k)]
 
 
 def kernel_times(max_n: int = 256):

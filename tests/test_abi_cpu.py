@@ -26,11 +26,14 @@ def declared_functions():
 
 
 def test_header_declares_expected_calls():
-    assert declared_functions() == sorted(["gl_eval_grid", "gl_argmin_feasible",
-                                           "gl_evaluate_host", "gl_link_demand", "gl_savings_surface",
+    assert declared_functions() == sorted(["gl_eval_grid", "gl_eval_grid_sched",
+                                           "gl_argmin_feasible", "gl_evaluate_host",
+                                           "gl_evaluate_host_sched", "gl_link_demand",
+                                           "gl_savings_surface",
                                            "gl_complete_matrices", "gl_argmin_matrices",
                                            "gl_last_launch_count",
                                            "gl_profile_enable", "gl_kernel_times",
+                                           "gl_kernel_timeline",
                                            "gl_strerror", "gl_version"])
 
 
@@ -47,7 +50,7 @@ def test_library_exports_every_declared_symbol(built):
 
 def test_version_and_strerror_without_gpu(built):
     lib = built.lib()
-    assert lib.gl_version() == 2
+    assert lib.gl_version() == 3
     assert lib.gl_strerror(0) == b"ok"
     assert b"invalid" in lib.gl_strerror(-1)
 
@@ -68,6 +71,7 @@ int main(void){
         offsetof(gl_link_stats, peak_t_us));
  printf("%zu %zu %zu\n", sizeof(gl_savings_pair), sizeof(gl_savings),
         offsetof(gl_savings, eq4_energy_less));
+ printf("%zu %zu\n", sizeof(gl_schedule), offsetof(gl_schedule, first_hi));
  return 0;}
 """
     import tempfile
@@ -92,6 +96,8 @@ int main(void){
     sv = list(map(int, lines[4].split()))
     assert sv == [C.sizeof(N.GlSavingsPair), N.SAVINGS_DTYPE.itemsize,
                   N.SAVINGS_DTYPE.fields["eq4_energy_less"][1]]
+    sc = list(map(int, lines[5].split()))
+    assert sc == [C.sizeof(N.GlSchedule), N.GlSchedule.first_hi.offset]
 
 
 def test_calls_fail_loudly_without_gpu(built):

@@ -575,3 +575,41 @@ def test_stage_groups_clone(per_request):
         for f in INT_FIELDS:
             assert int(st[ci][f]) == int(ref["stats"][ci][f]), (ci, f)
     assert not ref["mismatch"]
+
+
+@pytest.mark.parametrize("cfg,n", [(4, 6000), (5, 2500), (3, 3000), (2, 2000)])
+def test_schedule_hint_never_changes_results(cfg, n):
+    """gl_eval_grid_sched / gl_evaluate_host_sched (greenllm.h gl_schedule): any hinted
+    range -- the predicted one, single chains, ranges that split a stage group (their
+    primary outside the range) or a trace, the first / last chains, a shard-relative
+    range -- gives byte-identical statistics and per-request rows; a bad range is
+    GL_E_INVALID and launches nothing."""
+    g = build_config(cfg, n=n)
+    dg = api.DeviceGrid(g)
+    nc = dg.n_chains
+    st0, pr0 = api.eval_grid(dg, per_request=True, schedule=False)
+    st0, pr0 = st0.cpu().numpy(), pr0.cpu().numpy()
+    ranges = [dg.first_range(), (0, 1), (nc - 1, nc), (min(3, nc - 1), min(17, nc)),
+              (nc // 2, nc), (0, nc // 3), (0, nc), (2, 2)]
+    for r in ranges:
+        if r is None:
+            continue
+        st, pr = api.eval_grid(dg, per_request=True, schedule=r)
+        assert np.array_equal(st.cpu().numpy(), st0), (cfg, r)
+        assert np.array_equal(pr.cpu().numpy(), pr0), (cfg, r)
+    if nc >= 6:  # a shard with a shard-relative hint
+        lo, hi = 1, nc - 1
+        st, _ = api.eval_grid(dg, lo, hi, schedule=(1, 3))
+        assert np.array_equal(st.cpu().numpy(), st0[lo:hi])
+    for bad in [(3, 2), (-1, 2), (0, nc + 1)]:
+        with pytest.raises(N.GreenLLMError) as ei:
+            api.eval_grid(dg, schedule=bad)
+        assert ei.value.status == N.GL_E_INVALID
+    # end to end with and without the hint
+    host = dg.pinned_traces()
+    a = api.evaluate_host(dg, host, want_carbon=True, schedule=False)
+    sa, ca, cha = a.stats.copy(), a.carbon.copy(), a.choice.copy()
+    b = api.evaluate_host(dg, host, want_carbon=True, schedule=dg.first_range() or (0, 1))
+    assert np.array_equal(b.stats, sa) and np.array_equal(b.carbon, ca)
+    assert np.array_equal(b.choice, cha)
+    assert np.array_equal(sa.view(np.uint8).reshape(nc, -1), st0)
