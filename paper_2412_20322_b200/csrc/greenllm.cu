@@ -476,7 +476,25 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         fams.swap(f2);
         fam_slots.swap(s2);
     }
-    const bool use_ids = phased || n_sec > 0;  // k_stages reads its primaries from a list
+    // Deferred DSD demand: when DSD demand kernels run, k_stages of the disaggregated
+    // DSD primaries does not wait for them -- it runs on a side stream alongside, with
+    // demand 0 in their decode streams, and k_stage_clone's fill pass writes K_j there
+    // once both are done (the stage scans never read K).  The primaries to fill, by phase.
+    std::vector<int32_t> fill_ids;
+    int32_t fill_a = 0;
+    // (co-located SpecDecode chains read K inside k_stages: no deferral with them)
+    bool any_spec_colo = false;
+    for (int32_t i = 0; i < n_chains; ++i) any_spec_colo |= chains[i].mode == GL_MODE_SPEC_COLO;
+    const bool defer = (!fams.empty() || !solo.empty()) && !any_spec_colo;
+    if (defer) {
+        for (int32_t i = 0; i < n_prim; ++i)
+            if (chains[prim_ids[i]].mode == GL_MODE_DSD) {
+                fill_ids.push_back(prim_ids[i]);
+                if (i < prim_a) ++fill_a;  // prim_ids holds phase A's primaries first
+            }
+    }
+    const int32_t n_fill = (int32_t)fill_ids.size();
+    const bool use_ids = phased || n_sec > 0 || n_fill > 0;  // kernels read chain id lists
     // k_stages: S blocks per chain (decoupled look-back between them), S <= 4 chosen
     // to minimise the waves per chain's work, ceil(chains S / resident) / S (ties to
     // the smaller S): 2 on config 4's 64 chains, 3 on config 6's 80, 4 on config 5's 320
@@ -504,8 +522,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     total += align256(sizeof(gl::DStagePart) * (size_t)n_chains * stage_split);
     const size_t off_ticket = total;
     total += 256;
-    const size_t off_ids = total;  // primaries, secondaries, primary of each chain
-    total += align256(sizeof(int32_t) * ((size_t)n_chains * 2 + 2));
+    const size_t off_ids = total;  // primaries, secondaries, primary of each chain, fills
+    total += align256(sizeof(int32_t) * ((size_t)n_chains * 3 + 2));
     const size_t zero_bytes = total - off_zero;
     unsigned char *scratch = nullptr;
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
@@ -579,6 +597,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     int32_t *d_prim_ids = reinterpret_cast<int32_t *>(scratch + off_ids);
     int32_t *d_sec_ids = d_prim_ids + n_prim;
     int32_t *d_prim_of = d_sec_ids + n_sec;
+    int32_t *d_fill_ids = d_prim_of + n_chains;
     cudaError_t e = cudaMemcpyAsync(scratch, dch.data(), sizeof(DChain) * n_chains,
                                     cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess && !solo_groups.empty())
@@ -596,6 +615,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         idv = prim_ids;
         idv.insert(idv.end(), sec_ids.begin(), sec_ids.end());
         idv.insert(idv.end(), prim_of.begin(), prim_of.end());
+        idv.insert(idv.end(), fill_ids.begin(), fill_ids.end());
         e = cudaMemcpyAsync(d_prim_ids, idv.data(), sizeof(int32_t) * idv.size(),
                             cudaMemcpyHostToDevice, stream);
     }
@@ -606,8 +626,9 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     // [p0, p1) and secondaries [s0, s1) of the device id lists, chains [c0, c1)
     auto launch_family = [&](int32_t f0, int32_t f1) {
         if (e != cudaSuccess || f1 <= f0) return;
-        // persistent threads: about 8 resident blocks of 128 threads per SM in total,
-        // spread over the families, never more than one thread per request
+        // persistent threads: about 8 blocks of 128 threads per SM in total (two waves
+        // at the register limit of 4 resident; one wave measured the same), spread
+        // over the families, never more than one thread per request
         int64_t fmax = 0;
         for (int32_t f = f0; f < f1; ++f) fmax = std::max(fmax, fams[f].n);
         const int64_t want = std::max<int64_t>(1, (8 * (int64_t)n_sm) / (int64_t)(f1 - f0));
@@ -637,36 +658,59 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         ++launches;
     };
     bool waited = false;  // gl_evaluate_host: the arrival arrays may still be in flight
-    auto launch_stages = [&](int32_t p0, int32_t p1, int32_t ticket_slot) {
+    auto launch_stages = [&](int32_t p0, int32_t p1, int32_t ticket_slot, cudaStream_t ss) {
         if (e == cudaSuccess && stages_wait && !waited) {
-            e = cudaStreamWaitEvent(stream, stages_wait, 0);
+            e = cudaStreamWaitEvent(ss, stages_wait, 0);
             waited = true;
         }
         if (e != cudaSuccess || p1 <= p0) return;
         e = cudaFuncSetAttribute(gl::k_stages, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                  (int)smem_st);
         if (e != cudaSuccess) return;
-        prof_begin("k_stages", stream);
-        gl::k_stages<<<(p1 - p0) * stage_split, 32 * gl::ST_WARPS, smem_st, stream>>>(
+        prof_begin("k_stages", ss);
+        gl::k_stages<<<(p1 - p0) * stage_split, 32 * gl::ST_WARPS, smem_st, ss>>>(
             dc, stats_out, rows, stage_split,
             reinterpret_cast<int32_t *>(scratch + off_ticket) + ticket_slot,
-            use_ids ? d_prim_ids + p0 : nullptr);
+            use_ids ? d_prim_ids + p0 : nullptr, defer ? 1 : 0);
         e = cudaGetLastError();
-        prof_end(stream);
+        prof_end(ss);
         ++launches;
     };
     // rows are an output (or feed the link analysis): secondaries get full copies
     const bool copy_rows = per_request_out != nullptr || lk != nullptr;
-    auto launch_clone = [&](int32_t s0, int32_t s1) {
+    // secondaries [s0, s1) of d_sec_ids, or (fill) DSD primaries [s0, s1) of d_fill_ids
+    auto launch_clone = [&](int32_t s0, int32_t s1, bool fill) {
         if (e != cudaSuccess || s1 <= s0) return;
         const int32_t ns = s1 - s0;
         const int bpc = (int)std::max<int64_t>(1, std::min<int64_t>(64, (8 * (int64_t)n_sm + ns - 1) / ns));
-        prof_begin("k_stage_clone", stream);
+        prof_begin(fill ? "k_stage_fill" : "k_stage_clone", stream);
         gl::k_stage_clone<<<dim3((unsigned)bpc, (unsigned)ns), 256, 0, stream>>>(
-            dc, stats_out, rows, d_sec_ids + s0, d_prim_of, stage_split, copy_rows ? 1 : 0);
+            dc, stats_out, rows, (fill ? d_fill_ids : d_sec_ids) + s0, d_prim_of, stage_split,
+            copy_rows ? 1 : 0, fill ? 1 : 0);
         e = cudaGetLastError();
         prof_end(stream);
         ++launches;
+    };
+    // a phase's prologue: with deferred demand, k_stages on a side stream (slot 0)
+    // alongside the DSD demand kernels, joined before the fill and the clones
+    auto prologue = [&](int32_t f0, int32_t f1, int32_t g0, int32_t g1, int32_t p0, int32_t p1,
+                        int32_t l0, int32_t l1, int32_t s0, int32_t s1, int32_t ticket_slot) {
+        cudaStream_t ss = nullptr;
+        cudaEvent_t js = nullptr;
+        if (e == cudaSuccess && defer && p1 > p0 && (f1 > f0 || g1 > g0) &&
+            !side_fork(0, stream, ss, js))
+            ss = nullptr;
+        if (defer) launch_stages(p0, p1, ticket_slot, ss ? ss : stream);
+        launch_family(f0, f1);
+        launch_solo(g0, g1);
+        if (!defer) launch_stages(p0, p1, ticket_slot, stream);  // it reads K
+        if (ss) {
+            cudaError_t r = cudaEventRecord(js, ss);
+            if (r == cudaSuccess) r = cudaStreamWaitEvent(stream, js, 0);
+            if (e == cudaSuccess) e = r;
+        }
+        launch_clone(l0, l1, true);
+        launch_clone(s0, s1, false);
     };
     auto launch_segments = [&](int32_t c0, int32_t c1) {
         if (e != cudaSuccess || c1 <= c0) return;
@@ -740,10 +784,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         if (e == cudaSuccess) e = r;
     };
     if (!phased) {
-        launch_family(0, (int32_t)fams.size());
-        launch_solo(0, (int32_t)solo_groups.size());
-        launch_stages(0, n_prim, 0);
-        launch_clone(0, n_sec);
+        prologue(0, (int32_t)fams.size(), 0, (int32_t)solo_groups.size(), 0, n_prim, 0, n_fill,
+                 0, n_sec, 0);
         launch_segments(0, n_chains);
         // Both families present (configurations 6 and 7): the co-located launch goes
         // to a side stream forked from `stream` and joined back, so the two launches
@@ -759,19 +801,14 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         // stage scans, clones, segments, then its decode on a side stream; phase B's
         // prologue runs on `stream` meanwhile, its decodes on `stream` and a second
         // side stream; both joined before k_finalize.
-        launch_family(0, fam_a);
-        launch_solo(0, solo_a);
-        launch_stages(0, prim_a, 0);
-        launch_clone(0, sec_a);
+        prologue(0, fam_a, 0, solo_a, 0, prim_a, 0, fill_a, 0, sec_a, 0);
         launch_segments(s_lo, s_hi);
         cudaStream_t sa = nullptr, sb = nullptr;
         cudaEvent_t ja = nullptr, jb = nullptr;
         if (e == cudaSuccess && !side_fork(2, stream, sa, ja)) sa = nullptr;
         launch_decode(s_lo, s_hi, sa ? sa : stream, nullptr);
-        launch_family(fam_a, (int32_t)fams.size());
-        launch_solo(solo_a, (int32_t)solo_groups.size());
-        launch_stages(prim_a, n_prim, 1);
-        launch_clone(sec_a, n_sec);
+        prologue(fam_a, (int32_t)fams.size(), solo_a, (int32_t)solo_groups.size(), prim_a, n_prim,
+                 fill_a, n_fill, sec_a, n_sec, 1);
         launch_segments(0, s_lo);
         launch_segments(s_hi, n_chains);
         if (e == cudaSuccess && s_hi < n_chains && s_lo > 0 && !side_fork(3, stream, sb, jb))

@@ -126,17 +126,29 @@ __global__ void __launch_bounds__(256) k_dsd_demand(const DGroup *__restrict__ g
 // family of 5 alphas x 8 gammas): one thread per request evaluates each Philox word
 // ONCE for every group.  Per draft step s and alpha-set a, m_a = #{c : u_s < thr_a[c]}
 // (thresholds decrease in c, so the accepted drafts are a prefix); group (a, gamma)
-// accepts 1 + min(gamma, m_a) tokens, and its K is the first step whose running total
-// reaches o - 1.  Running totals grow with alpha and gamma (thresholds grow with
-// alpha), so the group (smallest alpha, gamma = 1) is the last to finish: the loop for
-// a request ends when it has.  Threads are persistent: a lane whose request is done
-// takes its next one (stride = all threads of the family) in the same loop trip.
+// accepts 1 + min(gamma, m_a) tokens, and its K is the number of steps taken while
+// its running total is still below o - 1.  Running totals grow with alpha and gamma
+// (thresholds grow with alpha), so the group (smallest alpha, gamma = 1) is the last
+// to finish: the loop for a request ends when it has.  Threads are persistent: a lane
+// whose request is done takes its next one (stride = all threads of the family) in
+// the same loop trip.
+//
+// m_a for all alpha-sets comes from one shared-memory table indexed by the top
+// FAM_LUT_BITS bits of u: entry .x packs m_a (4 bits per set) at the bucket's top
+// value; a bucket holding exactly one threshold thr_a[c] stores it in .y and its set
+// a in bits 28-30 of .x, so m_a(u) = m_a(top) + (u < .y) (.y = 0 elsewhere: never
+// true); a bucket holding more thresholds sets bit 31 and the lane counts by compares.
+// Per group and step: r -= 1 + min(gamma, m) and K += (r > 0) before it (r = tokens
+// still needed).
+constexpr int FAM_LUT_BITS = 11;
+constexpr int FAM_LUT = 1 << FAM_LUT_BITS;
+
 __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ fams)
 {
     const DFamily *f = fams + blockIdx.y;
     __shared__ uint32_t *s_K[FAM_NA * FAM_GM];
+    __shared__ uint2 s_lut[FAM_LUT];
     if (threadIdx.x < FAM_NA * FAM_GM) s_K[threadIdx.x] = f->K[threadIdx.x / FAM_GM][threadIdx.x % FAM_GM];
-    __syncthreads();
     uint32_t thr[FAM_NA][FAM_GM];
     bool all[FAM_NA];
 #pragma unroll
@@ -145,6 +157,32 @@ __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ 
 #pragma unroll
         for (int c = 0; c < FAM_GM; ++c) thr[a][c] = __ldg(&f->thr[a][c]);
     }
+    auto count = [&](int a, uint32_t u) -> uint32_t {
+        uint32_t m = 0;
+#pragma unroll
+        for (int c = 0; c < FAM_GM; ++c) m += u < thr[a][c] ? 1u : 0u;
+        return all[a] ? (uint32_t)FAM_GM : m;
+    };
+    for (int bkt = threadIdx.x; bkt < FAM_LUT; bkt += blockDim.x) {
+        const uint32_t lo = (uint32_t)bkt << (32 - FAM_LUT_BITS);
+        const uint32_t hi = lo + ((1u << (32 - FAM_LUT_BITS)) - 1u);
+        uint32_t x = 0, y = 0, nbreak = 0;
+#pragma unroll
+        for (int a = 0; a < FAM_NA; ++a) {
+            const uint32_t mh = count(a, hi), ml = count(a, lo);
+            x |= mh << (4 * a);
+            nbreak += ml - mh;
+            if (ml != mh) {
+                x |= (uint32_t)a << 28;
+#pragma unroll
+                for (int c = 0; c < FAM_GM; ++c)
+                    if (thr[a][c] > lo && thr[a][c] <= hi) y = thr[a][c];
+            }
+        }
+        if (nbreak > 1) x |= 0x80000000u;  // several thresholds in the bucket: compares
+        s_lut[bkt] = make_uint2(x, nbreak == 1 ? y : 0u);
+    }
+    __syncthreads();
     const int na = __ldg(&f->na);
     const int64_t n = __ldg(&f->n);
     const uint64_t seed = __ldg(&f->seed);
@@ -152,10 +190,12 @@ __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ 
     const uint32_t *const o = f->o;
     const int64_t Q = (int64_t)gridDim.x * blockDim.x;
     int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    uint32_t tok[FAM_NA][FAM_GM], kk[FAM_NA][FAM_GM];  // running totals, K once crossed
-    uint32_t need = 0, call = 0;
+    int32_t r[FAM_NA][FAM_GM];   // tokens still needed (the request's o - 1 at first)
+    uint32_t kk[FAM_NA][FAM_GM];  // steps taken while r > 0
+    uint32_t call = 0;
     // next request with demand > 0 (requests with o = 1 get K = 0 right away)
     auto take = [&]() {
+        uint32_t need = 0;
         for (; j < n; j += Q) {
             uint32_t ov = __ldg(o + j);
             if (ov >= O_LIMIT) ov = O_LIMIT - 1;
@@ -168,7 +208,7 @@ __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ 
         for (int a = 0; a < FAM_NA; ++a)
 #pragma unroll
             for (int g = 0; g < FAM_GM; ++g) {
-                tok[a][g] = 0u;
+                r[a][g] = (int32_t)need;
                 kk[a][g] = 0u;
             }
         call = 0;
@@ -181,23 +221,25 @@ __global__ void __launch_bounds__(128) k_dsd_family(const DFamily *__restrict__ 
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
                 const uint32_t u = ws[q];
-                const uint32_t step = 4u * call + (uint32_t)q + 1u;  // K if this step crosses
+                const uint2 e = s_lut[u >> (32 - FAM_LUT_BITS)];
+                uint32_t pk = (e.x & 0x0FFFFFFFu) + ((u < e.y) ? (1u << (4 * ((e.x >> 28) & 7u))) : 0u);
+                if (e.x & 0x80000000u) {  // several thresholds in this bucket
+                    pk = 0;
+#pragma unroll
+                    for (int a = 0; a < FAM_NA; ++a) pk |= count(a, u) << (4 * a);
+                }
 #pragma unroll
                 for (int a = 0; a < FAM_NA; ++a) {
-                    uint32_t m = 0;
-#pragma unroll
-                    for (int c = 0; c < FAM_GM; ++c) m += u < thr[a][c] ? 1u : 0u;
-                    if (all[a]) m = FAM_GM;
+                    const int32_t m1 = (int32_t)((pk >> (4 * a)) & 15u) + 1;
 #pragma unroll
                     for (int g = 0; g < FAM_GM; ++g) {
-                        const uint32_t t = tok[a][g] + 1u + min((uint32_t)(g + 1), m);
-                        kk[a][g] = (kk[a][g] == 0u && t >= need) ? step : kk[a][g];
-                        tok[a][g] = t;
+                        kk[a][g] += r[a][g] > 0 ? 1u : 0u;
+                        r[a][g] -= min(g + 2, m1);
                     }
                 }
             }
             ++call;
-            if (tok[0][0] >= need) {  // the last group has crossed: write K, next request
+            if (r[0][0] <= 0) {  // the last group has crossed: write K, next request
 #pragma unroll
                 for (int a = 0; a < FAM_NA; ++a)
 #pragma unroll

@@ -183,7 +183,8 @@ __device__ __forceinline__ void stage_lookback(const DChain &ch, int s, bool sec
 __global__ void __launch_bounds__(32 * ST_WARPS, 1)
     k_stages(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
              int64_t *__restrict__ perreq, int32_t S, int32_t *__restrict__ ticket,
-             const int32_t *__restrict__ ids)  // chains to run (primaries), NULL = all
+             const int32_t *__restrict__ ids,  // chains to run (primaries), NULL = all
+             int32_t defer_dsd)  // DSD chains: demand 0 in the stream, filled in later
 {
     __shared__ int32_t s_vid;
     __shared__ int64_t s_carry;
@@ -235,7 +236,9 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
 
     const int32_t n = (int32_t)ch.n;
     const bool colo = ch.mode == GL_MODE_STANDALONE || ch.mode == GL_MODE_SPEC_COLO;
-    const bool dsd = ch.mode == GL_MODE_DSD || ch.mode == GL_MODE_SPEC_COLO;  // demand K_j
+    // demand K_j -- or, deferred (disaggregated DSD while k_dsd_family / k_dsd_demand
+    // still run on another stream), 0 now and k_stage_clone's fill pass writes K_j
+    const bool dsd = (ch.mode == GL_MODE_DSD && !defer_dsd) || ch.mode == GL_MODE_SPEC_COLO;
     const int32_t nchunks = (n + CHUNK - 1) / CHUNK;
     const int32_t runs = ST_WARPS * S, run = sblk * ST_WARPS + warp;
     const int32_t per = (nchunks + runs - 1) / runs;
@@ -665,9 +668,10 @@ __global__ void __launch_bounds__(1024)
 __global__ void __launch_bounds__(256)
     k_stage_clone(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
                   int64_t *__restrict__ perreq, const int32_t *__restrict__ sec,
-                  const int32_t *__restrict__ prim_of, int32_t S, int32_t copy_rows)
+                  const int32_t *__restrict__ prim_of, int32_t S, int32_t copy_rows,
+                  int32_t fill_only)  // DSD primaries after a deferred k_stages: demands only
 {
-    const int32_t c = sec[blockIdx.y], pi = prim_of[c];
+    const int32_t c = sec[blockIdx.y], pi = fill_only ? c : prim_of[c];
     const DChain &ch = chains[c];
     const DChain &pc = chains[pi];
     bool sbad = false;
@@ -684,7 +688,7 @@ __global__ void __launch_bounds__(256)
         M += __ldcg(&q.dcount);
     }
     const bool valid = st == 0;
-    if (blockIdx.x == 0 && threadIdx.x == 0) {  // R55 as in k_stages
+    if (blockIdx.x == 0 && threadIdx.x == 0 && !fill_only) {  // R55 as in k_stages
         gl_chain_stats o;
         o.n = ch.n;
         o.slo_ok = 0;
@@ -710,7 +714,8 @@ __global__ void __launch_bounds__(256)
     // four entries per thread and trip (two 16-B loads of the primary's (d, j), four
     // independent demand loads, two 16-B stores): the stream is 16-B aligned (entry
     // offsets are multiples of 32), so only the sentinel tail is written one by one
-    const int64_t Q = (int64_t)M + DEC_TAIL, Q4 = (int64_t)M / 4;
+    // (fill_only: in place over the primary's own stream; its tail is already written)
+    const int64_t Q = (int64_t)M + (fill_only ? 0 : DEC_TAIL), Q4 = (int64_t)M / 4;
     const uint4 *src4 = reinterpret_cast<const uint4 *>(pc.dec_dj);
     uint4 *dst4 = reinterpret_cast<uint4 *>(ch.dec_dj);
     for (int64_t q4 = t0; q4 < Q4; q4 += stride) {
@@ -727,7 +732,7 @@ __global__ void __launch_bounds__(256)
         }
         ch.dec_dj[q] = v;
     }
-    if (copy_rows) {  // the primary's (ttft, finish of o = 1 requests) rows
+    if (copy_rows && !fill_only) {  // the primary's (ttft, finish of o = 1 requests) rows
         const longlong2 *src = reinterpret_cast<const longlong2 *>(perreq + 2 * pc.out_off);
         longlong2 *dst = reinterpret_cast<longlong2 *>(perreq + 2 * ch.out_off);
         for (int64_t j = t0; j < ch.n; j += stride) dst[j] = __ldcg(src + j);
