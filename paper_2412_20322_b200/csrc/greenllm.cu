@@ -196,7 +196,14 @@ bool side_fork(int slot, cudaStream_t from, cudaStream_t &side, cudaEvent_t &joi
     SideStream &ss = tl[dev][slot];
     if (!ss.s) {
         SideStream n;
-        if (cudaStreamCreateWithFlags(&n.s, cudaStreamNonBlocking) == cudaSuccess &&
+        // slot 0 carries short kernels that must not queue behind a whole-GPU kernel
+        // on `from` (k_stages beside the DSD demand): the highest stream priority
+        int least = 0, greatest = 0;
+        if (slot != 0 || cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
+            cudaGetLastError();
+            greatest = 0;
+        }
+        if (cudaStreamCreateWithPriority(&n.s, cudaStreamNonBlocking, greatest) == cudaSuccess &&
             cudaEventCreateWithFlags(&n.fork, cudaEventDisableTiming) == cudaSuccess &&
             cudaEventCreateWithFlags(&n.join, cudaEventDisableTiming) == cudaSuccess) {
             ss = n;

@@ -438,6 +438,7 @@ def test_evaluate_host_matches_device_path():
     g = build_config(4, n=4000)
     dg = api.DeviceGrid(g)
     stats, _ = api.eval_grid(dg)
+    eval_launches = dg.last_launches
     carbon, choice, fb = api.argmin_feasible(dg, stats)
     torch.cuda.synchronize()
     ptok = torch.empty((g.rows, g.cols), dtype=torch.float64, device="cuda")
@@ -449,7 +450,9 @@ def test_evaluate_host_matches_device_path():
     assert np.array_equal(res.via_fallback, fb.cpu().numpy())
     assert np.array_equal(res.carbon, carbon.cpu().numpy())
     assert np.array_equal(res.carbon_per_token, ptok.cpu().numpy())
-    assert res.launches == 6 and res.h2d_bytes > 0
+    # the same kernels as gl_eval_grid (DSD demand, stages, fill, segments, decode,
+    # finalize) plus k_argmin
+    assert res.launches == eval_launches + 1 == 7 and res.h2d_bytes > 0
 
 
 def test_evaluate_host_pageable_inputs_other_stream_both_families():
