@@ -884,13 +884,15 @@ __global__ void __launch_bounds__(256)
     for (int q = 0; q < per_thread; ++q) {
         const int64_t j = base + (int64_t)q * blockDim.x + threadIdx.x;
         if (j < n) {
-            longlong2 tf = __ldg(reinterpret_cast<const longlong2 *>(rows) + j);
             const int64_t a = __ldg(ch.a + j);
             uint32_t o = __ldg(ch.o + j);
             o = min(max(o, 1u), O_LIMIT - 1);
-            if (!own) {
+            longlong2 tf;
+            if (own) {
+                tf = __ldg(reinterpret_cast<const longlong2 *>(rows) + j);
+            } else {  // the own row holds only the finish of a decode request
                 tf.x = __ldg(prow + 2 * j);
-                if (o == 1) tf.y = __ldg(prow + 2 * j + 1);
+                tf.y = __ldg((o == 1 ? prow : rows) + 2 * j + 1);
             }
             const int64_t c = a + tf.x;
             const bool good = tf.x <= ttft_slo &&

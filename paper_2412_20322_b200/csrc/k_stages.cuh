@@ -408,8 +408,9 @@ __global__ void __launch_bounds__(32 * ST_WARPS, 1)
                     *reinterpret_cast<longlong2 *>(out + 2 * (int64_t)j) =
                         make_longlong2(cv[q] - c.av[q], cv[q]);
                     acc_mk = max(acc_mk, cv[q]);
-                } else {
-                    out[2 * (int64_t)j] = cv[q] - c.av[q];
+                } else {  // finish 0 until k_decode writes it (rows always initialised)
+                    *reinterpret_cast<longlong2 *>(out + 2 * (int64_t)j) =
+                        make_longlong2(cv[q] - c.av[q], 0);
                     const int64_t e = (int64_t)produced + pos;
                     ch.dec_r[e] = rv[q];
                     ch.dec_dj[e] = make_uint2(dsd ? c.kv[q] : c.oc[q] - 1, (uint32_t)j);

@@ -3,7 +3,9 @@
 
 usage: compute-sanitizer --tool memcheck python scripts/sanitize_run.py
 Exercises: gl_eval_grid (DPD, DSD, Standalone, co-located SpecDecode chains; caps
-<= 31 and > 31; k_stages split widths 1-4; side-stream fork), gl_argmin_feasible,
+<= 31 and > 31; k_stages split widths 1-4; side-stream fork; deferred DSD demand with
+k_stages on a side stream and the fill pass; DSD families; the two-phase launch
+order of gl_eval_grid_sched / gl_evaluate_host_sched), gl_argmin_feasible,
 gl_link_demand, gl_savings_surface, gl_complete_matrices (cooperative and
 one-CTA paths), gl_argmin_matrices, gl_evaluate_host.
 """
@@ -31,6 +33,17 @@ def main():
         torch.cuda.synchronize()
         api.check_status(api.stats_numpy(stats))
         print(g.name, "chains", len(g.chains), "ok", flush=True)
+    # deferred DSD demand (solo groups and a family) and the two-phase launch order
+    for g, hints in ((build_config(4, n=1000), [(32, 40), (3, 17)]),
+                     (subset_chains(build_config(5, n=600), list(range(0, 120))), [(0, 40), (45, 50)])):
+        dg = api.DeviceGrid(g)
+        base, _ = api.eval_grid(dg, per_request=True)
+        for h in hints:
+            st, _ = api.eval_grid(dg, per_request=True, schedule=h)
+            torch.cuda.synchronize()
+            assert torch.equal(st, base), (g.name, h)
+        host = api.evaluate_host(dg, dg.pinned_traces(), schedule=hints[0])
+        print(g.name, "deferred demand + hints", hints, "ok", flush=True)
     g6 = build_config(6, n=1500)
     dg6 = api.DeviceGrid(g6)
     st6, _ = api.eval_grid(dg6)
