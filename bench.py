@@ -433,6 +433,7 @@ def run_ours(args):
     sbytes = stream_bytes(grid, lo, hi)
     prof = load_profile_json("k_decode_dram_bytes.json", args.config)
     traffic = prof.get("dram_bytes_per_launch")
+    l2_traffic = prof.get("l2_bytes_per_launch")
     winst = prof.get("warp_inst_per_launch")
     step_total = {k: sum(v) / max(1, len(v)) for k, v in kt.items()}
     cpu = None
@@ -466,7 +467,8 @@ def run_ours(args):
         "chain_request_sims_per_s": chain_req,
         "kernel_ms_per_step": step_total,
         "roofline": {"bound": "latency", "achieved": achieved, "peak": hbm_peak, "unit": "GB/s",
-                     "frac": achieved / hbm_peak, "traffic": traffic, "peak_source": peak_src,
+                     "frac": achieved / hbm_peak, "traffic": traffic, "l2_traffic": l2_traffic,
+                     "peak_source": peak_src,
                      "kernel": kname, "algorithmic_bytes_per_launch": alg_bytes,
                      "bytes_per_unit": BYTES_PER_CHAIN_REQUEST,
                      "unit_name": "(timing chain, request): arrival i64 + prompt u32 + output u32 "

@@ -79,7 +79,9 @@ def num(n):
 
 
 dram = num("dram__bytes_read.sum") + num("dram__bytes_write.sum")
+l2 = num("lts__t_sectors.sum") * 32 if "lts__t_sectors.sum" in m else None
 json.dump({"round": tag, "kernel": kern, "dram_bytes_per_launch": dram,
+           "l2_bytes_per_launch": l2,
            "warp_inst_per_launch": num("smsp__inst_executed.sum"),
            "source": f"profiles/{tag}_{kern}_ncu.md"},
           open(os.path.join(out_dir, f"{kern}_dram_bytes.json"), "w"), indent=1)
