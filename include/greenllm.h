@@ -19,8 +19,8 @@
  *    implements the same rules independently.
  *  - "device" = CUDA device memory of the current device; "host" = CPU memory.
  *  - The caller owns every buffer.  The library keeps no global state besides
- *    a cached device-capability check and, per host thread and device, four side
- *    streams with their events (created on first use, kept for the process);
+ *    a cached device-capability check and, per host thread and device, up to five
+ *    side streams with their events (created on first use, kept for the process);
  *    it allocates only stream-ordered scratch (cudaMallocAsync / cudaFreeAsync
  *    on `stream`) and never synchronises except in gl_evaluate_host.  When one
  *    gl_eval_grid call holds both disaggregated and co-located chains, it forks

@@ -187,7 +187,7 @@ struct SideStream {
 };
 bool side_fork(int slot, cudaStream_t from, cudaStream_t &side, cudaEvent_t &join)
 {
-    thread_local SideStream tl[16][4];  // [device][slot]
+    thread_local SideStream tl[16][5];  // [device][slot]
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) {
         cudaGetLastError();
@@ -196,10 +196,10 @@ bool side_fork(int slot, cudaStream_t from, cudaStream_t &side, cudaEvent_t &joi
     SideStream &ss = tl[dev][slot];
     if (!ss.s) {
         SideStream n;
-        // slot 0 carries short kernels that must not queue behind a whole-GPU kernel
+        // slot 4 carries short kernels that must not queue behind a whole-GPU kernel
         // on `from` (k_stages beside the DSD demand): the highest stream priority
         int least = 0, greatest = 0;
-        if (slot != 0 || cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
+        if (slot != 4 || cudaDeviceGetStreamPriorityRange(&least, &greatest) != cudaSuccess) {
             cudaGetLastError();
             greatest = 0;
         }
@@ -698,14 +698,14 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         prof_end(stream);
         ++launches;
     };
-    // a phase's prologue: with deferred demand, k_stages on a side stream (slot 0)
+    // a phase's prologue: with deferred demand, k_stages on a side stream (slot 4)
     // alongside the DSD demand kernels, joined before the fill and the clones
     auto prologue = [&](int32_t f0, int32_t f1, int32_t g0, int32_t g1, int32_t p0, int32_t p1,
                         int32_t l0, int32_t l1, int32_t s0, int32_t s1, int32_t ticket_slot) {
         cudaStream_t ss = nullptr;
         cudaEvent_t js = nullptr;
         if (e == cudaSuccess && defer && p1 > p0 && (f1 > f0 || g1 > g0) &&
-            !side_fork(0, stream, ss, js))
+            !side_fork(4, stream, ss, js))
             ss = nullptr;
         if (defer) launch_stages(p0, p1, ticket_slot, ss ? ss : stream);
         launch_family(f0, f1);

@@ -1,7 +1,7 @@
 # r02m: the round's measurement session after the prologue work (tests, smoke,
 # bench configs 4 / 5 / 7, launch list, k_decode and config-5 prologue captures)
 set -x
-TAG=${TAG:-r02m}
+TAG=${TAG:-r02s}
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/${TAG}_smoke.log 2>&1
 timeout 1500 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest_gpu.log 2>&1; echo "exit $?" >> gpurun_out/${TAG}_pytest_gpu.log
 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
