@@ -616,3 +616,45 @@ def test_schedule_hint_never_changes_results(cfg, n):
     assert np.array_equal(b.stats, sa) and np.array_equal(b.carbon, ca)
     assert np.array_equal(b.choice, cha)
     assert np.array_equal(sa.view(np.uint8).reshape(nc, -1), st0)
+
+
+def test_deferred_demand_random_disaggregated():
+    """Only disaggregated chains (no co-located SpecDecode), so the DSD demand is
+    deferred: k_stages of the DSD primaries runs beside the demand kernels and the
+    fill pass writes K_j.  Random traces (chunk and block boundaries, o = 1 requests)
+    each carry stage groups -- DSD chains with identical tables and several
+    (alpha, gamma) (one primary, secondaries cloned; a family when >= 2 groups share
+    the draws) -- next to a DPD chain and a lone DSD chain (per-group kernel); every
+    request against the oracle, with and without launch-order hints."""
+    rng = np.random.default_rng(424242)
+    traces, chains = [], []
+    for t in range(10):
+        n = int(rng.choice([1, 5, 129, 600, 2049, 4500]))
+        a = np.sort(rng.integers(0, int(rng.integers(50, 400)) * n + 1, n))
+        p = rng.integers(1, 9, n)
+        o = rng.integers(1, 60, n)
+        o[rng.random(n) < 0.1] = 1
+        traces.append(custom_trace(a, p, o))
+        cap = int(rng.choice([3, 8, 16, 40]))
+        tab = make_tables(8, cap, lambda q: 30 * q, lambda q: 7 * q,
+                          [0] + [40 + 10 * b for b in range(1, cap + 1)], b2=lambda q: q,
+                          sbn=[0] + [3] * cap, sbo=[0] + [4] * cap, sen=[0] + [5] * cap,
+                          seo=[0] + [6] * cap)
+        for alpha, gamma in [(0.5, 1), (0.8, 4), (0.95, 8), (0.0, 2)][: int(rng.integers(1, 5))]:
+            chains.append(make_chain(tab, MODE_DSD, cap, gamma, alpha, seed=0xC0FFEE + t,
+                                     ttft_slo=4000, tpot_slo=500, trace_idx=t))
+        chains.append(make_chain(tab, MODE_DPD, cap, ttft_slo=4000, tpot_slo=500, trace_idx=t))
+        lone = make_tables(8, cap, lambda q: 20 * q, lambda q: 5 * q,
+                           [0] + [35 + 9 * b for b in range(1, cap + 1)], b2=lambda q: q)
+        chains.append(make_chain(lone, MODE_DSD, cap, 12, 0.7, seed=77 + t, ttft_slo=4000,
+                                 tpot_slo=500, trace_idx=t))
+    k = len(chains)
+    lt = 7 * 365 * 24 * 3600.0
+    g = GridSpec("deferred", traces, chains, np.array([[261.0, lt, lt]]), np.zeros(k, np.int32),
+                 np.arange(k, dtype=np.int32), k, 1)
+    st = assert_parity(g)
+    dg = api.DeviceGrid(g)
+    base, pr0 = api.eval_grid(dg, per_request=True)
+    for h in [(0, 3), (k // 2, k), (5, k - 5)]:
+        st2, pr2 = api.eval_grid(dg, per_request=True, schedule=h)
+        assert torch.equal(st2, base) and torch.equal(pr2, pr0), h
