@@ -216,6 +216,17 @@ def host_cores():
         return os.cpu_count() or 1
 
 
+def host_cpu_model():
+    """The host CPU model (lscpu's "Model name"), SURVEY 8(d)."""
+    try:
+        for ln in open("/proc/cpuinfo"):
+            if ln.startswith("model name"):
+                return ln.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    return None
+
+
 def cpu_baseline_all_cores(grid, cfg, n, max_rounds=2):
     """The same single-threaded oracle, one chain per process across every host core
     (per-core rate, aggregate, nproc).  Timing chains only (the
@@ -240,6 +251,7 @@ def cpu_baseline_all_cores(grid, cfg, n, max_rounds=2):
             "kind": "oracle", "sample": f"{len(jobs)} of {len(all_ids)} timing chains x {reqs} "
             f"requests (all {cells} of their grid cells), one process per chain on {procs} of "
             f"{cores} host cores, {wall:.1f} s wall",
+            "cpu_model": host_cpu_model(),
             "chain_request_sims_per_s": len(jobs) * reqs / wall,
             "per_core_chain_request_sims_per_s": reqs / (sum(per) / len(per))}
 
