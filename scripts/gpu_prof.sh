@@ -1,7 +1,10 @@
 # One GPU session's measurements (run under gpurun from the repo root):
 #   the GPU test suite, smoke, the microbenchmarked latencies, the bench line for
-#   configs 4 / 5 / 7, the ncu launch list of the bench step, and --set full captures
-#   of the dominant kernel (k_decode, config 4) and of the config-5 prologue kernels.
+#   configs 4 / 5 / 7 and the reference arm, the ncu launch list of the bench step, and
+#   --set full captures of the dominant kernel (k_decode, config 4) and of the config-5
+#   prologue kernels (k_dsd_family, k_stages, the fill and clone passes, k_finalize).
+# Other GPU scripts: gpu_ab.sh (same-box A/B of build/ab variants), gpu_sanitize.sh
+# (compute-sanitizer over every entry point).
 # Everything lands in gpurun_out/ with the prefix $TAG (e.g. r02c).
 set -x
 TAG=${TAG:-run}
@@ -11,7 +14,8 @@ nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/lat scripts/ubench/lat.
 python bench.py > gpurun_out/${TAG}_bench.json 2> gpurun_out/${TAG}_bench.err
 python bench.py --config 5 --steps 5 > gpurun_out/${TAG}_bench_cfg5.json 2> gpurun_out/${TAG}_bench_cfg5.err
 python bench.py --config 7 --steps 10 > gpurun_out/${TAG}_bench_cfg7.json 2> gpurun_out/${TAG}_bench_cfg7.err
+python bench.py --impl reference --steps 3 --warmup 3 > gpurun_out/${TAG}_bench_ref.json 2> gpurun_out/${TAG}_bench_ref.err
 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/${TAG}_launches.csv python bench.py --steps 3 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/${TAG}_b_ncu.log 2>&1
 ncu --set full --clock-control none --import-source on -k regex:k_decode -s 3 -c 1 -f -o gpurun_out/${TAG}_kdec python bench.py --steps 1 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/${TAG}_kdec.log 2>&1
-ncu --set full --clock-control none --import-source on -k regex:"k_dsd_family|k_stages|k_stage_clone|k_finalize" -s 4 -c 4 -f -o gpurun_out/${TAG}_cfg5pro python bench.py --config 5 --steps 1 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/${TAG}_cfg5pro.log 2>&1
+ncu --set full --clock-control none --import-source on -k regex:"k_dsd_family|k_stages|k_stage_clone|k_finalize" -s 5 -c 5 -f -o gpurun_out/${TAG}_cfg5pro python bench.py --config 5 --steps 1 --warmup 3 --no-cpu-baseline --no-analysis > gpurun_out/${TAG}_cfg5pro.log 2>&1
 ls -la gpurun_out
