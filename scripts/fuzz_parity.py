@@ -1,0 +1,104 @@
+"""Randomised parity campaign on a B200 (test infrastructure: imports oracle/ through
+tests/oracle_pool.py): random grids mixing every mode, caps on both sides of the
+32-lane boundary, stage groups (chains with identical tables on one trace, so
+secondaries are cloned), DSD families (several (alpha, gamma) on one set of draws),
+bursts, o = 1 requests, far gaps, with or without co-located chains (which switches
+the deferred DSD demand off), and a random launch-order hint.  Every request's
+(TTFT, finish) and every chain statistic must equal the oracle's.
+
+usage: python scripts/fuzz_parity.py [seconds] [seed]
+"""
+import sys
+import time
+
+import numpy as np
+import torch
+
+sys.path.insert(0, '.')
+from paper_2412_20322_b200 import api  # noqa: E402
+from paper_2412_20322_b200.inputs import GridSpec, custom_trace  # noqa: E402
+from tests import oracle_pool  # noqa: E402
+from tests.helpers import make_chain, make_tables  # noqa: E402
+
+INT_FIELDS = ("n", "slo_ok", "tokens", "busy_new_us", "busy_old_us", "e_new_uj", "e_old_uj",
+              "makespan_us", "req_hash", "status", "capacity_ok")
+
+
+def random_grid(rng):
+    traces, chains = [], []
+    colo = rng.random() < 0.3
+    for t in range(int(rng.integers(1, 6))):
+        n = int(rng.choice([1, 2, 31, 128, 129, 700, 2500, 6000]))
+        gaps = rng.exponential(float(rng.choice([20, 200, 2000, 20000])), n)
+        if rng.random() < 0.2:
+            gaps[rng.integers(0, n)] += 3e9  # a gap beyond 2^31 us
+        a = np.cumsum(gaps).astype(np.int64)
+        if rng.random() < 0.3:
+            a[: n // 3] = a[0]  # a burst
+            a = np.sort(a)
+        P = 8
+        p = rng.integers(1, P + 1, n)
+        o = rng.integers(1, int(rng.choice([4, 40, 300])), n)
+        o[rng.random(n) < 0.1] = 1
+        traces.append(custom_trace(a, p, o))
+        for _ in range(int(rng.integers(1, 4))):  # stage groups: shared tables
+            cap = int(rng.choice([1, 2, 5, 16, 31, 32, 40]))
+            tab = make_tables(P, cap, rng.integers(1, 400, P + 1), rng.integers(0, 300, P + 1),
+                              np.sort(rng.integers(5, 900, cap + 1)),
+                              b2=rng.integers(0, 50, P + 1), e1=rng.integers(0, 999, P + 1),
+                              e2=rng.integers(0, 999, P + 1), sbn=rng.integers(0, 50, cap + 1),
+                              sbo=rng.integers(0, 50, cap + 1), sen=rng.integers(0, 9999, cap + 1),
+                              seo=rng.integers(0, 9999, cap + 1))
+            slo = dict(ttft_slo=int(rng.integers(100, 50000)), tpot_slo=int(rng.integers(10, 2000)))
+            modes = [0, 1] + ([2, 3] if colo else [])
+            for _ in range(int(rng.integers(1, 5))):
+                mode = int(rng.choice(modes))
+                spec = mode in (1, 3)
+                gamma = int(rng.integers(1, 9)) if spec else 0
+                alpha = float(rng.choice([0.0, 0.5, 0.6, 0.8, 0.9, 1.0])) if spec else 0.0
+                chains.append(make_chain(tab, mode, cap, gamma, alpha, seed=0xF00D + t,
+                                         trace_idx=t, **slo))
+    k = len(chains)
+    lt = 7 * 365 * 24 * 3600.0
+    return GridSpec("fuzz", traces, chains, np.array([[261.0, lt, lt]]), np.zeros(k, np.int32),
+                    np.arange(k, dtype=np.int32), k, 1)
+
+
+def main():
+    budget = float(sys.argv[1]) if len(sys.argv) > 1 else 600.0
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
+    rng = np.random.default_rng(seed)
+    t0 = time.time()
+    grids = chains = reqs = 0
+    while time.time() - t0 < budget:
+        g = random_grid(rng)
+        dg = api.DeviceGrid(g)
+        nc = len(g.chains)
+        hint = None
+        if nc >= 2 and rng.random() < 0.5:
+            lo = int(rng.integers(0, nc - 1))
+            hint = (lo, int(rng.integers(lo + 1, nc + 1)))
+        stats, pr = api.eval_grid(dg, per_request=True, schedule=hint or False)
+        torch.cuda.synchronize()
+        st = api.stats_numpy(stats)
+        ref = oracle_pool.evaluate_grid(g, gpu_per_request=pr.cpu().numpy())
+        for ci in range(nc):
+            for f in INT_FIELDS:
+                if int(st[ci][f]) != int(ref["stats"][ci][f]):
+                    raise SystemExit(f"MISMATCH grid {grids} seed {seed} chain {ci} {f}: "
+                                     f"{int(st[ci][f])} != {int(ref['stats'][ci][f])} (hint {hint})")
+        if ref["mismatch"]:
+            raise SystemExit(f"MISMATCH grid {grids} seed {seed} rows: "
+                             f"{dict(list(ref['mismatch'].items())[:2])} (hint {hint})")
+        grids += 1
+        chains += nc
+        reqs += sum(g.traces[c.trace_idx].n for c in g.chains)
+        if grids % 20 == 0:
+            print(f"{time.time() - t0:7.1f} s: {grids} grids, {chains} chains, {reqs} chain-requests, "
+                  "all equal", flush=True)
+    print(f"fuzz_parity seed {seed}: {grids} random grids, {chains} chains, {reqs} chain-requests: "
+          "every request and statistic equal to the oracle")
+
+
+if __name__ == "__main__":
+    main()
