@@ -3,8 +3,10 @@ tests/oracle_pool.py): random grids mixing every mode, caps on both sides of the
 32-lane boundary, stage groups (chains with identical tables on one trace, so
 secondaries are cloned), DSD families (several (alpha, gamma) on one set of draws),
 bursts, o = 1 requests, far gaps, with or without co-located chains (which switches
-the deferred DSD demand off), and a random launch-order hint.  Every request's
-(TTFT, finish) and every chain statistic must equal the oracle's.
+the deferred DSD demand off), and a random launch-order hint; some grids also go
+through gl_link_demand (random payloads and windows) against oracle_link_demand.
+Every request's (TTFT, finish), every chain statistic and every link field must
+equal the oracle's.
 
 usage: python scripts/fuzz_parity.py [seconds] [seed]
 """
@@ -15,6 +17,7 @@ import numpy as np
 import torch
 
 sys.path.insert(0, '.')
+from oracle import oracle as O  # noqa: E402
 from paper_2412_20322_b200 import api  # noqa: E402
 from paper_2412_20322_b200.inputs import GridSpec, custom_trace  # noqa: E402
 from tests import oracle_pool  # noqa: E402
@@ -42,7 +45,7 @@ def random_grid(rng):
         o[rng.random(n) < 0.1] = 1
         traces.append(custom_trace(a, p, o))
         for _ in range(int(rng.integers(1, 4))):  # stage groups: shared tables
-            cap = int(rng.choice([1, 2, 5, 16, 31, 32, 40]))
+            cap = int(rng.choice([1, 2, 5, 16, 31, 32, 40, 64, 100, 256]))
             tab = make_tables(P, cap, rng.integers(1, 400, P + 1), rng.integers(0, 300, P + 1),
                               np.sort(rng.integers(5, 900, cap + 1)),
                               b2=rng.integers(0, 50, P + 1), e1=rng.integers(0, 999, P + 1),
@@ -69,7 +72,7 @@ def main():
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     rng = np.random.default_rng(seed)
     t0 = time.time()
-    grids = chains = reqs = 0
+    grids = chains = reqs = links = 0
     while time.time() - t0 < budget:
         g = random_grid(rng)
         dg = api.DeviceGrid(g)
@@ -90,14 +93,29 @@ def main():
         if ref["mismatch"]:
             raise SystemExit(f"MISMATCH grid {grids} seed {seed} rows: "
                              f"{dict(list(ref['mismatch'].items())[:2])} (hint {hint})")
+        if rng.random() < 0.15 and not any(c.mode in (2, 3) for c in g.chains):
+            # gl_link_demand (NEXT #2) with random payloads and window, chain by chain
+            window = int(rng.choice([1, 1000, 250_000, 1_000_000]))
+            params = [(int(rng.integers(0, 5000)), int(rng.integers(0, 9000))) for _ in range(nc)]
+            _, link = api.link_demand(dg, window, params=params)
+            torch.cuda.synchronize()
+            lk = api.link_numpy(link)
+            for ci, ch in enumerate(g.chains):
+                want = O.link_demand(g.traces[ch.trace_idx], ch, window, *params[ci])
+                for f in ("total_bytes", "peak_bytes", "peak_t_us", "n_impulses"):
+                    if int(lk[ci][f]) != want[f]:
+                        raise SystemExit(f"LINK MISMATCH grid {grids} seed {seed} chain {ci} {f}: "
+                                         f"{int(lk[ci][f])} != {want[f]}")
+            links += 1
         grids += 1
         chains += nc
         reqs += sum(g.traces[c.trace_idx].n for c in g.chains)
         if grids % 20 == 0:
             print(f"{time.time() - t0:7.1f} s: {grids} grids, {chains} chains, {reqs} chain-requests, "
                   "all equal", flush=True)
-    print(f"fuzz_parity seed {seed}: {grids} random grids, {chains} chains, {reqs} chain-requests: "
-          "every request and statistic equal to the oracle")
+    print(f"fuzz_parity seed {seed}: {grids} random grids ({links} also through gl_link_demand), "
+          f"{chains} chains, {reqs} chain-requests: every request, statistic and link field "
+          "equal to the oracle")
 
 
 if __name__ == "__main__":
