@@ -5,8 +5,11 @@ secondaries are cloned), DSD families (several (alpha, gamma) on one set of draw
 bursts, o = 1 requests, far gaps, with or without co-located chains (which switches
 the deferred DSD demand off), and a random launch-order hint; some grids also go
 through gl_link_demand (random payloads and windows) against oracle_link_demand.
-Every request's (TTFT, finish), every chain statistic and every link field must
-equal the oracle's.
+Each grid also carries a random Alg. 1 matrix (scenarios, absent cells, capacity
+flags, SLO targets from easy to impossible, both fallback priorities) for
+gl_argmin_feasible, and some go end to end through gl_evaluate_host.  Every request's
+(TTFT, finish), every chain statistic, every link field, every carbon cell (bit for
+bit), choice and fallback flag must equal the oracle's.
 
 usage: python scripts/fuzz_parity.py [seconds] [seed]
 """
@@ -61,10 +64,25 @@ def random_grid(rng):
                 alpha = float(rng.choice([0.0, 0.5, 0.6, 0.8, 0.9, 1.0])) if spec else 0.0
                 chains.append(make_chain(tab, mode, cap, gamma, alpha, seed=0xF00D + t,
                                          trace_idx=t, **slo))
+    # an Alg. 1 grid over the chains: random scenarios (CI, lifetimes), rows x cols cells
+    # (absent ones included), random capacity flags, both fallback priorities, and SLO
+    # targets from easy to impossible (the fallback path)
     k = len(chains)
-    lt = 7 * 365 * 24 * 3600.0
-    return GridSpec("fuzz", traces, chains, np.array([[261.0, lt, lt]]), np.zeros(k, np.int32),
-                    np.arange(k, dtype=np.int32), k, 1)
+    for c in chains:
+        c.capacity_ok = int(rng.random() < 0.9)
+    S = int(rng.integers(1, 5))
+    yr = 365 * 24 * 3600.0
+    scen = np.stack([rng.choice([0.0, 17.0, 261.0, 501.0, 1000.0], S),
+                     rng.uniform(1, 10, S) * yr, rng.uniform(1, 10, S) * yr], axis=1)
+    cols = int(rng.integers(1, 7))
+    rows = int(rng.integers(1, 9))
+    cells = rng.integers(0, k, rows * cols).astype(np.int32)
+    cells[rng.random(rows * cols) < 0.15] = -1
+    target = [(9, 10), (1, 2), (1, 1), (0, 1)][int(rng.integers(0, 4))]
+    prio = int(rng.integers(0, 2))
+    return GridSpec("fuzz", traces, chains, scen, rng.integers(0, S, rows).astype(np.int32),
+                    cells, rows, cols, slo_num=target[0], slo_den=target[1], priority=prio,
+                    default_col=int(rng.integers(-1, cols)))
 
 
 def main():
@@ -72,7 +90,7 @@ def main():
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 1
     rng = np.random.default_rng(seed)
     t0 = time.time()
-    grids = chains = reqs = links = 0
+    grids = chains = reqs = links = e2e = 0
     while time.time() - t0 < budget:
         g = random_grid(rng)
         dg = api.DeviceGrid(g)
@@ -93,6 +111,20 @@ def main():
         if ref["mismatch"]:
             raise SystemExit(f"MISMATCH grid {grids} seed {seed} rows: "
                              f"{dict(list(ref['mismatch'].items())[:2])} (hint {hint})")
+        # Alg. 1 on the grid (gl_argmin_feasible): carbon bit for bit, choice, fallback
+        carbon, choice, fb = api.argmin_feasible(dg, stats)
+        m = ref["present"].astype(bool)
+        if not (np.array_equal(carbon.cpu().numpy()[m], ref["carbon"][m]) and
+                np.array_equal(choice.cpu().numpy(), ref["choice"]) and
+                np.array_equal(fb.cpu().numpy(), ref["via_fallback"])):
+            raise SystemExit(f"ALG1 MISMATCH grid {grids} seed {seed}")
+        if rng.random() < 0.1:  # end to end from host buffers, same answers
+            res = api.evaluate_host(dg, dg.pinned_traces(), want_carbon=True,
+                                    schedule=hint or False)
+            if not (np.array_equal(res.stats.view(np.uint8).reshape(nc, -1), stats.cpu().numpy())
+                    and np.array_equal(res.choice, ref["choice"])):
+                raise SystemExit(f"E2E MISMATCH grid {grids} seed {seed}")
+            e2e += 1
         if rng.random() < 0.15 and not any(c.mode in (2, 3) for c in g.chains):
             # gl_link_demand (NEXT #2) with random payloads and window, chain by chain
             window = int(rng.choice([1, 1000, 250_000, 1_000_000]))
@@ -113,8 +145,9 @@ def main():
         if grids % 20 == 0:
             print(f"{time.time() - t0:7.1f} s: {grids} grids, {chains} chains, {reqs} chain-requests, "
                   "all equal", flush=True)
-    print(f"fuzz_parity seed {seed}: {grids} random grids ({links} also through gl_link_demand), "
-          f"{chains} chains, {reqs} chain-requests: every request, statistic and link field "
+    print(f"fuzz_parity seed {seed}: {grids} random grids ({links} also through gl_link_demand, "
+          f"{e2e} through gl_evaluate_host), {chains} chains, {reqs} chain-requests: every "
+          "request, statistic, link field, carbon cell (bit for bit), choice and fallback flag "
           "equal to the oracle")
 
 
