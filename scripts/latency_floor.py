@@ -58,6 +58,26 @@ def sass_lines(binary, fun=None):
     return first
 
 
+def control_stalls(binary, fun):
+    """{address: the stall count ptxas encoded in the instruction's control bits} (bits
+    41-44 of the high 64-bit word: the cycles the scheduler waits before issuing the
+    warp's next instruction, the static part of the schedule)."""
+    out = subprocess.run(["cuobjdump", "-sass", "-fun", fun, binary], capture_output=True,
+                         text=True).stdout.splitlines()
+    res = {}
+    for i, ln in enumerate(out):
+        m = re.match(r"\s*/\*([0-9a-f]{4,})\*/\s*.*?;\s*/\*\s*0x[0-9a-f]+\s*\*/", ln)
+        if not m:
+            continue
+        a = int(m.group(1), 16)
+        if a in res:
+            break
+        m2 = re.match(r"\s*/\*\s*(0x[0-9a-f]+)\s*\*/", out[i + 1]) if i + 1 < len(out) else None
+        if m2:
+            res[a] = (int(m2.group(1), 16) >> 41) & 0xF
+    return res
+
+
 def opcode(ins):
     t = ins.split()
     return t[1] if t[0].startswith("@") else t[0]
@@ -252,8 +272,9 @@ def find_loop(sass):
     raise SystemExit("light loop not found")
 
 
-def walk(sass, head, decisions):
-    """Instructions executed from `head` until the path branches back to `head`.
+def walk(sass, head, decisions, addrs=None):
+    """Instructions executed from `head` until the path branches back to `head`
+    (their addresses appended to `addrs` if given).
     decisions: one 'T'/'N' per conditional branch met (BRA.DIV: never taken)."""
     pos = {a: i for i, (a, _) in enumerate(sass)}
     i, path, d = pos[head], [], list(decisions)
@@ -261,6 +282,8 @@ def walk(sass, head, decisions):
         a, s = sass[i]
         op, dst, src, guard, tgt = parse(s)
         path.append(s)
+        if addrs is not None:
+            addrs.append(a)
         if op.startswith("BRA"):
             if op == "BRA.DIV":
                 taken = False
@@ -317,13 +340,18 @@ def main():
     ap.add_argument("--crit", action="append", default=[],
                     help="cfgN:chain:kernel_ms:decode_requests:sm_mhz -- a config's critical chain "
                          "(one launch of that chain alone), reported with its cycles per event")
+    ap.add_argument("--loop-measured", action="append", default=[],
+                    help="cfgN:cycles -- the light loop's measured cycles per event "
+                         "(scripts/loop_stalls.py on an ncu source-level capture)")
     ap.add_argument("--join", default="NTNT", help="branch decisions of the J path")
     ap.add_argument("--leave", default="NNTT", help="branch decisions of the L path")
     a = ap.parse_args()
     L, raw = latencies(a.lat)
     sass = sass_lines(a.so, KDEC)
     head, _ = find_loop(sass)
-    paths = {"J": walk(sass, head, a.join), "L": walk(sass, head, a.leave)}
+    addrs = {"J": [], "L": []}
+    paths = {"J": walk(sass, head, a.join, addrs["J"]), "L": walk(sass, head, a.leave, addrs["L"])}
+    ctl = control_stalls(a.so, KDEC)
     res = {"source": "scripts/latency_floor.py: measured latencies (scripts/ubench/lat.cu on a B200) "
                      "along the SASS of k_decode<1,0,0>'s leader light-load loop",
            "latencies_cycles": {k: round(v, 2) for k, v in L.items()},
@@ -341,6 +369,10 @@ def main():
                       for m in ("dep", "inorder")}
     # the critical chain alternates join / leave: the floor is the alternating sequence's
     # dataflow time with free branches (the loop's minimal dependent-instruction cycles)
+    # the schedule ptxas encoded: control-code stall counts summed along each path (the
+    # static part of the issue time; scoreboard waits on LDS / VOTE / REDUX come on top)
+    res["scheduled_stalls"] = {k: sum(ctl.get(x, 0) for x in v) for k, v in addrs.items()}
+    res["scheduled_stalls"]["JL_mean"] = (res["scheduled_stalls"]["J"] + res["scheduled_stalls"]["L"]) / 2
     res["min_cycles_per_event"] = res["no_branch_cost"]["dep"]["JL_alternating"]
     res["issue_bound_cycles_per_event"] = res["no_branch_cost"]["inorder"]["JL_alternating"]
     if a.measured_cycles:
@@ -353,6 +385,10 @@ def main():
         crit[cfg] = {"chain": int(chain), "kernel_ms_alone": float(ms), "decode_requests": int(m),
                      "sm_mhz": float(mhz), "cycles_per_event": round(cyc, 1),
                      "frac": round(res["min_cycles_per_event"] / cyc, 3)}
+    for c in a.loop_measured:
+        cfg, cyc = c.split(":")
+        crit.setdefault(cfg, {})["light_loop_cycles_per_event"] = float(cyc)
+        crit[cfg]["light_loop_frac"] = round(res["min_cycles_per_event"] / float(cyc), 3)
     if crit:
         res["critical_chain"] = crit
     res["command"] = "python scripts/latency_floor.py " + " ".join(sys.argv[1:])
