@@ -115,6 +115,11 @@ def test_calls_fail_loudly_without_gpu(built):
         setattr(ch, f, 16)
     with pytest.raises(built.GreenLLMError):
         built.eval_grid([tr], [ch], 16, None, 0)
+    with pytest.raises(built.GreenLLMError):  # the launch-order hint changes nothing here
+        built.eval_grid([tr], [ch], 16, None, 0, sched=(0, 1))
+    with pytest.raises(built.GreenLLMError) as ei:  # a bad hint is caught before the device
+        built.eval_grid([tr], [ch], 16, None, 0, sched=(0, 2))
+    assert ei.value.status == built.GL_E_INVALID
     with pytest.raises(built.GreenLLMError):
         built.link_demand([tr], [ch], [(4, 100)], 1_000_000, None, 16, 0)
     # host validation precedes the device check: a bad window is GL_E_INVALID, a
