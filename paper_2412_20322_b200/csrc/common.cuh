@@ -42,8 +42,11 @@ struct DChainX {
     int32_t n_ev;        // LOG launches: batch-size log entries written
     int32_t stage_done;  // k_stages CTAs of this chain that have finished
     int32_t seg_done;    // k_segments CTAs of this chain that have finished
-    int32_t pad;
+    int32_t pad;         // k_relax race: slot + 1 (RX_SLOT_MASK), RX_SERIAL, RX_RELAXED
 };
+constexpr int32_t RX_SLOT_MASK = 0xFFFF;
+constexpr int32_t RX_SERIAL = 1 << 16;   // k_decode's leader finished the chain first
+constexpr int32_t RX_RELAXED = 1 << 17;  // k_relax solved the chain first
 
 // one k_stages CTA's share of a chain (k_stages splits a chain over S CTAs): its
 // aggregates are published with release flags for the CTAs after it, its partial

@@ -33,6 +33,7 @@
 #include <atomic>
 #include <cmath>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <map>
@@ -49,6 +50,7 @@
 #include "k_link.cuh"
 #include "k_savings.cuh"
 #include "k_als.cuh"
+#include "k_relax.cuh"
 
 namespace {
 
@@ -531,7 +533,52 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     total += 256;
     const size_t off_ids = total;  // primaries, secondaries, primary of each chain, fills
     total += align256(sizeof(int32_t) * ((size_t)n_chains * 3 + 2));
+    // k_relax (exact parallel decode of heavily loaded chains, k_relax.cuh): slots for
+    // the chains k_relax_pick selects on the device by load factor.  Not with the link
+    // analysis (it needs the batch-size log) or a launch-order hint.  Opt-in: it races
+    // k_decode for SM issue slots and measured no net gain on the five configurations
+    // (DESIGN.md §10).  GL_RELAX=1 turns it on; GL_RELAX=force (tests) makes every
+    // one-row chain eligible at any load.
+    const char *rx_env = std::getenv("GL_RELAX");
+    const bool rx_off = !rx_env || (rx_env[0] != '1' && rx_env[0] != 'f' && rx_env[0] != 's');
+    const bool rx_force = rx_env && (rx_env[0] == 'f' || rx_env[0] == 's');
+    // GL_RELAX=solo (tests): k_relax runs first on `stream`, so it wins every chain it
+    // solves and k_decode walks only the rest
+    const bool rx_solo = rx_env && rx_env[0] == 's';
+    int64_t rx_ncap = 0;
+    int32_t rx_elig = 0;
+    if (!lk && !phased && !rx_off)
+        for (int32_t i = 0; i < n_chains; ++i) {
+            const gl_chain &c = chains[i];
+            const int64_t n = traces[c.trace_idx].n;
+            if ((c.mode == GL_MODE_DPD || c.mode == GL_MODE_DSD) && c.batch_cap <= gl::RX_MAXCAP &&
+                n >= (rx_force ? 1 : gl::RX_MIN_M)) {
+                ++rx_elig;
+                rx_ncap = std::max(rx_ncap, n);
+            }
+        }
+    const int64_t rx_lcap = std::min<int64_t>((int64_t)gl::RX_LFACTOR * rx_ncap + 64, ((int64_t)1 << 31) - 64);
+    const int32_t rx_nsegcap = (int32_t)((rx_ncap + gl::RX_SEG - 1) / gl::RX_SEG);
+    const size_t rx_b_j = align256(sizeof(int32_t) * (size_t)rx_ncap);
+    const size_t rx_b_seg = align256(sizeof(int32_t) * 2 * (size_t)rx_nsegcap);
+    const size_t rx_b_l = align256(sizeof(int64_t) * (size_t)(rx_lcap + 1));
+    const size_t rx_b_blk = align256(sizeof(gl::RxBlk) * (size_t)n_sm);
+    int32_t rx_slots = 0;
+    if (rx_elig > 0) {
+        const size_t per = 2 * rx_b_j + rx_b_seg + 3 * rx_b_l + rx_b_blk;
+        rx_slots = (int32_t)std::min<int64_t>(std::min<int64_t>(rx_elig, rx_force ? 16 : gl::RX_DEF_SLOTS),
+                                              (int64_t)(((size_t)4 << 30) / per));
+    }
+    const size_t off_rx_blk = total;
+    total += rx_b_blk * rx_slots;
     const size_t zero_bytes = total - off_zero;
+    // (not zeroed) slot descriptors, load factors, iterates and iteration arrays
+    const size_t off_rx_slots = total;
+    total += align256(sizeof(gl::DRelax) * (size_t)rx_slots);
+    const size_t off_rx_rho = total;
+    total += rx_slots ? align256(sizeof(double) * (size_t)n_chains) : 0;
+    const size_t off_rx_buf = total;
+    total += (2 * rx_b_j + rx_b_seg + 3 * rx_b_l) * rx_slots;
     unsigned char *scratch = nullptr;
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
         return st;
@@ -626,6 +673,26 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         e = cudaMemcpyAsync(d_prim_ids, idv.data(), sizeof(int32_t) * idv.size(),
                             cudaMemcpyHostToDevice, stream);
     }
+    std::vector<gl::DRelax> rxv(rx_slots);
+    for (int32_t k = 0; k < rx_slots; ++k) {
+        gl::DRelax &R = rxv[k];
+        std::memset(&R, 0, sizeof R);
+        unsigned char *b = scratch + off_rx_buf + (2 * rx_b_j + rx_b_seg + 3 * rx_b_l) * k;
+        R.J = reinterpret_cast<int32_t *>(b);
+        R.A = reinterpret_cast<int32_t *>(b + rx_b_j);
+        R.seg = reinterpret_cast<int32_t *>(b + 2 * rx_b_j);
+        R.h = reinterpret_cast<unsigned long long *>(b + 2 * rx_b_j + rx_b_seg);
+        R.P = reinterpret_cast<unsigned long long *>(b + 2 * rx_b_j + rx_b_seg + rx_b_l);
+        R.tau = reinterpret_cast<int64_t *>(b + 2 * rx_b_j + rx_b_seg + 2 * rx_b_l);
+        R.blk = reinterpret_cast<gl::RxBlk *>(scratch + off_rx_blk + rx_b_blk * k);
+        R.lcap = rx_lcap;
+        R.ncap = (int32_t)rx_ncap;
+        R.nsegcap = rx_nsegcap;
+        R.chain = -1;
+    }
+    if (e == cudaSuccess && rx_slots)
+        e = cudaMemcpyAsync(scratch + off_rx_slots, rxv.data(), sizeof(gl::DRelax) * rx_slots,
+                            cudaMemcpyHostToDevice, stream);
     if (e == cudaSuccess && lk)  // log sentinels: every byte 0xFF -> (T, b) = (-1, -1)
         e = cudaMemsetAsync(scratch + off_ev, 0xFF, sizeof(longlong2) * (size_t)ev_total, stream);
     int launches = 0;
@@ -737,7 +804,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     };
     // decode launches over chains [c0, c1) on `dstream`: disaggregated chains, then
     // co-located ones (each launch skips the other family's chains)
-    auto launch_decode = [&](int32_t c0, int32_t c1, cudaStream_t dstream, cudaStream_t colo_stream) {
+    auto launch_decode = [&](int32_t c0, int32_t c1, cudaStream_t dstream, cudaStream_t colo_stream,
+                             int32_t rxpass = -1) {
         if (e != cudaSuccess || c1 <= c0) return;
         const int32_t nc = c1 - c0;
         const unsigned blocks = (unsigned)(nc * (1 + extra));
@@ -747,7 +815,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                                                  (int)smem_dec);
             if (r != cudaSuccess) return r;
             prof_begin(name, ds);
-            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, ds>>>(dc + c0, stats_out + c0, rows, nc);
+            kern<<<blocks, 32 * gl::DEC_WARPS, smem_dec, ds>>>(dc + c0, stats_out + c0, rows, nc, rxpass);
             r = cudaGetLastError();
             prof_end(ds);
             ++launches;
@@ -794,6 +862,61 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         prologue(0, (int32_t)fams.size(), 0, (int32_t)solo_groups.size(), 0, n_prim, 0, n_fill,
                  0, n_sec, 0);
         launch_segments(0, n_chains);
+        // k_relax: pick the heavily loaded chains, then (side stream) guess and relax
+        // them while k_decode walks every chain on `stream`; each chain goes to
+        // whichever finishes it first (k_relax.cuh)
+        cudaStream_t rxs = nullptr;
+        cudaEvent_t rxj = nullptr;
+        const bool relax = rx_slots > 0 && e == cudaSuccess;
+        if (relax) {
+            gl::DRelax *d_slots = reinterpret_cast<gl::DRelax *>(scratch + off_rx_slots);
+            double *d_rho = reinterpret_cast<double *>(scratch + off_rx_rho);
+            prof_begin("k_relax_pick", stream);
+            gl::k_relax_rho<<<(unsigned)n_chains, 256, 0, stream>>>(dc, stats_out, d_rho,
+                                                                   rx_force ? 1 : gl::RX_MIN_M);
+            double rlo = rx_force ? 0.0 : gl::RX_RHO_LO, rhi = rx_force ? 1e300 : gl::RX_RHO_HI;
+            if (const char *rr = std::getenv("GL_RELAX_RHO")) std::sscanf(rr, "%lf,%lf", &rlo, &rhi);
+            gl::k_relax_pick<<<1, 32, 0, stream>>>(dc, n_chains, d_rho, d_slots, rx_slots, rlo, rhi);
+            e = cudaGetLastError();
+            prof_end(stream);
+            launches += 2;
+            if (e == cudaSuccess && !rx_solo && !side_fork(1, stream, rxs, rxj)) rxs = nullptr;
+        }
+        auto launch_relax = [&]() {
+            if (!relax) return;
+            gl::DRelax *d_slots = reinterpret_cast<gl::DRelax *>(scratch + off_rx_slots);
+            cudaStream_t xs = rxs ? rxs : stream;
+            const int32_t segs = rx_nsegcap;
+            const int64_t warps = (int64_t)rx_slots * segs;
+            if (e == cudaSuccess) {
+                prof_begin("k_relax_guess", xs);
+                gl::k_relax_guess<<<(unsigned)((warps + gl::RX_GWARPS - 1) / gl::RX_GWARPS),
+                                    32 * gl::RX_GWARPS, 0, xs>>>(d_slots, rx_slots, segs, dc);
+                e = cudaGetLastError();
+                prof_end(xs);
+                ++launches;
+            }
+            if (e == cudaSuccess) {
+                // one block per SM: room beside k_decode's warps (registers), all resident
+                int per_sm = 0;
+                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl::k_relax, gl::RX_THREADS, 0);
+                if (e == cudaSuccess && per_sm < 1) e = cudaErrorCooperativeLaunchTooLarge;
+                if (e == cudaSuccess) {
+                    int32_t ns = rx_slots;
+                    int64_t *rows_p = rows;
+                    gl_chain_stats *st_p = stats_out;
+                    const char *dbg_env = std::getenv("GL_RELAX_DEBUG");
+                    int32_t dbg = dbg_env ? std::atoi(dbg_env) : 0;
+                    void *args[] = {&d_slots, &ns, (void *)&dc, &st_p, &rows_p, &dbg};
+                    prof_begin("k_relax", xs);
+                    e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(gl::k_relax),
+                                                    dim3((unsigned)n_sm), dim3(gl::RX_THREADS), args, 0, xs);
+                    prof_end(xs);
+                    ++launches;
+                }
+            }
+        };
+        if (rx_solo) launch_relax();
         // Both families present (configurations 6 and 7): the co-located launch goes
         // to a side stream forked from `stream` and joined back, so the two launches
         // (disjoint chains) overlap; the call stays stream-ordered on `stream`.
@@ -801,8 +924,19 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         cudaEvent_t ev_join = nullptr;
         if (e == cudaSuccess && has_disg && has_colo && !lk && !side_fork(0, stream, side, ev_join))
             side = nullptr;  // no fork: both launches stay on `stream` (serialised)
-        launch_decode(0, n_chains, stream, side ? side : stream);
+        launch_decode(0, n_chains, stream, side ? side : stream, relax ? 1 : -1);
+        // (enqueued after k_decode, so that k_decode's blocks are placed first)
+        if (!rx_solo) launch_relax();
         join(side, ev_join);
+        join(rxs, rxj);
+        if (relax && e == cudaSuccess) {  // the chains k_relax solved first
+            prof_begin("k_relax_out", stream);
+            gl::k_relax_out<<<dim3(32, (unsigned)rx_slots), 256, 0, stream>>>(
+                reinterpret_cast<gl::DRelax *>(scratch + off_rx_slots), dc, stats_out, rows);
+            e = cudaGetLastError();
+            prof_end(stream);
+            ++launches;
+        }
     } else {
         // Phase A (the hinted chains and the primaries they copy from): DSD demand,
         // stage scans, clones, segments, then its decode on a side stream; phase B's

@@ -139,6 +139,7 @@ struct RunCtx {
     int32_t nseg;
     int32_t hid;  // helper index (buffer), -1 for the leader
     longlong2 *ev;  // LOG: the chain's batch-size log (T, b after the change)
+    int32_t rx;     // the leader races k_relax on this chain (polls x->pad for RX_RELAXED)
 };
 
 // kept out of line so the decode loops stay free of memory-ordering operations
@@ -249,6 +250,11 @@ __device__ RunOut decode_run(const RunCtx &cx, RingW &ring, int32_t q0, int32_t 
                 while (kb < nseg_r && nb < nxt) nb = ch.seg_start[++kb];
                 if (ROWS) {  // publish the leader's progress
                     publish_pos(pub && lane == 0, &xx->leader_pos, kb - 1);
+                    // k_relax solved the chain: end the input at the next half
+                    if (cx.rx && !aborted && (__shfl_sync(FULL, poll_pos(&xx->pad), 0) & RX_RELAXED)) {
+                        aborted = true;
+                        ring.q_end = min(ring.q_end, ring.ready_to);
+                    }
                 } else if (!aborted && __shfl_sync(FULL, poll_pos(&xx->leader_pos), 0) > k0) {
                     // the leader is past this run's start: end the input at the next
                     // half (its sentinels are written when that half is waited for)
@@ -711,7 +717,7 @@ __device__ __noinline__ void helper_loop(const RunCtx cx, RingW ring)
 template <int SPL, bool COLO, bool LOG = false>
 __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     k_decode(const DChain *__restrict__ chains, gl_chain_stats *__restrict__ stats,
-             int64_t *__restrict__ perreq, int32_t n_chains)
+             int64_t *__restrict__ perreq, int32_t n_chains, int32_t rxpass)
 {
     static_assert(!(LOG && COLO), "the co-located modes have no link");
     extern __shared__ __align__(16) unsigned char smem[];
@@ -748,9 +754,12 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
 
     const int32_t nseg = ch.x->nseg;
     const int32_t hid = leader ? -1 : (int32_t)(blockIdx.x / n_chains) - 1;
+    // racing k_relax (rxpass 1): a chain with a relaxation slot is walked too; the
+    // first to finish owns the statistics (x->pad bits), both write identical rows
+    const int32_t rx = (rxpass > 0 && leader) ? (ld_relaxed_gpu(&ch.x->pad) & RX_SLOT_MASK) : 0;
     RunCtx cx{&ch, steps, magic, perreq + 2 * ch.out_off + 1,
               ch.spec_fin + (int64_t)max(hid, 0) * ch.spec_stride, cap, lane, nseg, hid,
-              leader ? ch.ev : ch.ev_spec + (int64_t)max(hid, 0) * ch.ev_stride};
+              leader ? ch.ev : ch.ev_spec + (int64_t)max(hid, 0) * ch.ev_stride, rx};
     RingW ring;
     ring.r = ring_r;
     ring.dj = ring_dj;
@@ -770,7 +779,12 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     int64_t mk = 0;
     int32_t k = 0;
     const int32_t M = ch.x->M;
+    bool lost = false;  // k_relax solved the chain first
     while (k < nseg) {
+        if (rx && (__shfl_sync(FULL, ld_relaxed_gpu(&ch.x->pad), 0) & RX_RELAXED)) {
+            lost = true;
+            break;
+        }
         if (lane == 0) st_relaxed_gpu(&ch.x->leader_pos, k);
         int32_t st = 0;
         if (lane == 0) {
@@ -785,6 +799,10 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
             ring.q_end = M;
             const RunOut ro = decode_run<SPL, true, COLO, LOG>(cx, ring, ch.seg_start[k], k, true,
                                                               2 * ch.seg_start[k]);
+            if (ro.stop_seg < 0) {  // aborted: k_relax solved the chain
+                lost = true;
+                break;
+            }
             for (int i = 0; i < 4; ++i) acc[i] += ro.sums[i];
             mk = max(mk, ro.mk);
             k = ro.stop_seg;
@@ -845,6 +863,16 @@ __global__ void __launch_bounds__(32 * DEC_WARPS, 1)
     }
     if (lane == 0) {
         st_release_gpu(&ch.x->leader_pos, nseg);
+        if (rx && !lost) lost = (atomicOr(&ch.x->pad, RX_SERIAL) & RX_RELAXED) != 0;
+#ifdef GL_RX_TRACE
+        if (rx) {
+            uint64_t t;
+            asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+            printf("leader chain %d done lost %d k %d nseg %d t %llu\n", c, (int)lost, k, nseg, t);
+        }
+#endif
+    }
+    if (lane == 0 && !lost) {
         gl_chain_stats &s = stats[c];
         s.busy_new_us += acc[0];
         s.busy_old_us += acc[1];

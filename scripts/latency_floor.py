@@ -37,7 +37,7 @@ import sys
 import tempfile
 
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
-KDEC = "_ZN2gl8k_decodeILi1ELb0ELb0EEEvPKNS_6DChainEP14gl_chain_statsPli"
+KDEC = "_ZN2gl8k_decodeILi1ELb0ELb0EEEvPKNS_6DChainEP14gl_chain_statsPlii"
 
 
 def sass_lines(binary, fun=None):
