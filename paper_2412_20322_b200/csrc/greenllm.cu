@@ -189,7 +189,7 @@ struct SideStream {
 };
 bool side_fork(int slot, cudaStream_t from, cudaStream_t &side, cudaEvent_t &join)
 {
-    thread_local SideStream tl[16][5];  // [device][slot]
+    thread_local SideStream tl[16][6];  // [device][slot]
     int dev = 0;
     if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 16) {
         cudaGetLastError();
@@ -557,15 +557,16 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                 rx_ncap = std::max(rx_ncap, n);
             }
         }
-    const int64_t rx_lcap = std::min<int64_t>((int64_t)gl::RX_LFACTOR * rx_ncap + 64, ((int64_t)1 << 31) - 64);
+    const int64_t rx_lcap = std::min<int64_t>((int64_t)gl::RX_LFACTOR * rx_ncap + 64, ((int64_t)1 << 31) - 64) & ~(int64_t)7;
     const int32_t rx_nsegcap = (int32_t)((rx_ncap + gl::RX_SEG - 1) / gl::RX_SEG);
     const size_t rx_b_j = align256(sizeof(int32_t) * (size_t)rx_ncap);
     const size_t rx_b_seg = align256(sizeof(int32_t) * 2 * (size_t)rx_nsegcap);
-    const size_t rx_b_l = align256(sizeof(int64_t) * (size_t)(rx_lcap + 1));
+    const size_t rx_b_l = align256(sizeof(int64_t) * (size_t)(rx_lcap + 1));   // tau
+    const size_t rx_b_h = align256(sizeof(uint32_t) * (size_t)rx_lcap);        // histogram
     const size_t rx_b_blk = align256(sizeof(gl::RxBlk) * (size_t)n_sm);
     int32_t rx_slots = 0;
     if (rx_elig > 0) {
-        const size_t per = 2 * rx_b_j + rx_b_seg + 3 * rx_b_l + rx_b_blk;
+        const size_t per = 3 * rx_b_j + rx_b_seg + rx_b_l + rx_b_h + rx_b_blk;
         rx_slots = (int32_t)std::min<int64_t>(std::min<int64_t>(rx_elig, rx_force ? 16 : gl::RX_DEF_SLOTS),
                                               (int64_t)(((size_t)4 << 30) / per));
     }
@@ -578,7 +579,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     const size_t off_rx_rho = total;
     total += rx_slots ? align256(sizeof(double) * (size_t)n_chains) : 0;
     const size_t off_rx_buf = total;
-    total += (2 * rx_b_j + rx_b_seg + 3 * rx_b_l) * rx_slots;
+    total += (3 * rx_b_j + rx_b_seg + rx_b_l + rx_b_h) * rx_slots;
     unsigned char *scratch = nullptr;
     if ((st = cuda_status(cudaMallocAsync(reinterpret_cast<void **>(&scratch), total, stream))))
         return st;
@@ -677,13 +678,13 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     for (int32_t k = 0; k < rx_slots; ++k) {
         gl::DRelax &R = rxv[k];
         std::memset(&R, 0, sizeof R);
-        unsigned char *b = scratch + off_rx_buf + (2 * rx_b_j + rx_b_seg + 3 * rx_b_l) * k;
+        unsigned char *b = scratch + off_rx_buf + (3 * rx_b_j + rx_b_seg + rx_b_l + rx_b_h) * k;
         R.J = reinterpret_cast<int32_t *>(b);
         R.A = reinterpret_cast<int32_t *>(b + rx_b_j);
-        R.seg = reinterpret_cast<int32_t *>(b + 2 * rx_b_j);
-        R.h = reinterpret_cast<unsigned long long *>(b + 2 * rx_b_j + rx_b_seg);
-        R.P = reinterpret_cast<unsigned long long *>(b + 2 * rx_b_j + rx_b_seg + rx_b_l);
-        R.tau = reinterpret_cast<int64_t *>(b + 2 * rx_b_j + rx_b_seg + 2 * rx_b_l);
+        R.Sq = reinterpret_cast<int32_t *>(b + 2 * rx_b_j);
+        R.seg = reinterpret_cast<int32_t *>(b + 3 * rx_b_j);
+        R.tau = reinterpret_cast<int64_t *>(b + 3 * rx_b_j + rx_b_seg);
+        R.h = reinterpret_cast<uint32_t *>(b + 3 * rx_b_j + rx_b_seg + rx_b_l);
         R.blk = reinterpret_cast<gl::RxBlk *>(scratch + off_rx_blk + rx_b_blk * k);
         R.lcap = rx_lcap;
         R.ncap = (int32_t)rx_ncap;
@@ -880,7 +881,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             e = cudaGetLastError();
             prof_end(stream);
             launches += 2;
-            if (e == cudaSuccess && !rx_solo && !side_fork(1, stream, rxs, rxj)) rxs = nullptr;
+            if (e == cudaSuccess && !rx_solo && !side_fork(5, stream, rxs, rxj)) rxs = nullptr;
         }
         auto launch_relax = [&]() {
             if (!relax) return;
@@ -903,11 +904,9 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                 if (e == cudaSuccess && per_sm < 1) e = cudaErrorCooperativeLaunchTooLarge;
                 if (e == cudaSuccess) {
                     int32_t ns = rx_slots;
-                    int64_t *rows_p = rows;
-                    gl_chain_stats *st_p = stats_out;
                     const char *dbg_env = std::getenv("GL_RELAX_DEBUG");
                     int32_t dbg = dbg_env ? std::atoi(dbg_env) : 0;
-                    void *args[] = {&d_slots, &ns, (void *)&dc, &st_p, &rows_p, &dbg};
+                    void *args[] = {&d_slots, &ns, (void *)&dc, &dbg};
                     prof_begin("k_relax", xs);
                     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(gl::k_relax),
                                                     dim3((unsigned)n_sm), dim3(gl::RX_THREADS), args, 0, xs);

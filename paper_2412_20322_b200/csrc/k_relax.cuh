@@ -60,7 +60,7 @@ constexpr int RX_LFACTOR = 40;    // iteration capacity per request
 constexpr int RX_MAXCAP = 31;     // one member per lane in the guess
 constexpr int32_t RX_MIN_M = 8192;
 constexpr double RX_RHO_LO = 0.73, RX_RHO_HI = 0.82;
-constexpr int RX_DEF_SLOTS = 4;   // slots per call (GL_RELAX=force: up to 16)
+constexpr int RX_DEF_SLOTS = 8;   // slots per call (GL_RELAX=force: up to 16)
 
 // one block's share of a slot's scans in the current sweep (zeroed per call; flags =
 // sweep + 1 once the value is published)
@@ -69,16 +69,17 @@ struct RxBlk {
     unsigned long long s1;   // packed (joins << 32 | leaves) count of the block's iterations
     int64_t a2, b2;          // max-plus map x -> max(x + a2, b2) of the block's iterations
     int32_t mc, pad2;        // max of the block's requests' max(A_q, S_q)
+    int32_t qa[8];           // per warp: its first request in the A merge (warm start)
     int64_t pad3;
 };
 
 // one relaxation slot: buffers (host), chain and state (device)
 struct DRelax {
     int32_t *J;                 // [ncap] join boundary per decode request (the iterate)
-    int32_t *A;                 // [ncap] per request: prefix max of max(A_q, S_q) within its block
+    int32_t *A;                 // [ncap] A_q of the sweep, then the prefix max of max(A_q, S_q) per block
+    int32_t *Sq;                // [ncap] S_q of the sweep
     int32_t *seg;               // [2 nsegcap] guess: local J of a segment's first request / of the next one
-    unsigned long long *h;      // [lcap] packed histogram: joins << 32 | leaves per boundary
-    unsigned long long *P;      // [lcap] its inclusive prefix (GJ << 32 | G)
+    uint32_t *h;                // [lcap] histogram per boundary: joins << 16 | leaves
     int64_t *tau;               // [lcap + 1]
     RxBlk *blk;                 // [grid blocks]
     int64_t lcap;
@@ -92,7 +93,8 @@ struct DRelax {
     int32_t sweeps;
     int32_t Lf;                 // Lc of the converged iterate
     int32_t quit;               // k_decode's leader finished the chain first
-    unsigned long long cnt[RX_MAXCAP + 1];  // iterations per batch size (last sweep)
+    int64_t tend;               // tau(Lc + 1) of the sweep
+    unsigned long long cnt[2][RX_MAXCAP + 1];  // iterations per batch size (by sweep parity)
 };
 
 // ---- selection: load factor of every eligible chain, slots to the heaviest ones
@@ -381,15 +383,16 @@ __device__ __forceinline__ RxMap rx_shfl(RxMap m, int l)
 }
 
 // The relaxation of every slot, one cooperative grid of G blocks (one per SM).
-// Per sweep: A scatter (J, F) -> grid barrier -> B1 block sums of the histogram,
-// B2 prefix P and the iterations' maps (block map), B3 tau -> grid barrier -> C1
-// A_q, S_q and their prefix max per block, C2 J' -> grid barrier -> convergence.
-// Each block owns a contiguous chunk of every slot's iterations (and requests);
-// its warps stream contiguous sub-chunks 256 iterations at a time with warp scans,
-// and a block's carries come from its predecessors' published aggregates.
-__global__ void __launch_bounds__(RX_THREADS, 1)
-    k_relax(DRelax *__restrict__ slots, int32_t nslots, const DChain *__restrict__ chains,
-            gl_chain_stats *__restrict__ stats, int64_t *__restrict__ perreq, int32_t dbg)
+// Per sweep: A scatter (J, F) -> grid barrier -> B1 block sums of the histogram;
+// B2 the iterations' maps (block map) and S_q (one writer per request: the boundary
+// where the leaves count G reaches q - cap + 1); B3 tau, and A_q by merging the
+// sorted ready times into the tau of each 256-iteration tile -> grid barrier -> C1
+// max(A_q, S_q) and its prefix max per block, C2 J' -> grid barrier -> convergence.
+// Each block owns a contiguous chunk of every slot's iterations (and requests); its
+// warps stream contiguous sub-chunks 256 iterations at a time with warp scans, and
+// a block's carries come from its predecessors' published aggregates.
+__global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room beside k_decode
+    k_relax(DRelax *__restrict__ slots, int32_t nslots, const DChain *__restrict__ chains, int32_t dbg)
 {
     namespace cg = cooperative_groups;
     cg::grid_group grid = cg::this_grid();
@@ -400,10 +403,10 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
     __shared__ unsigned long long s_wsum[RX_MAX_SLOTS][RX_WARPS];
     __shared__ int64_t s_wa[RX_MAX_SLOTS][RX_WARPS], s_wb[RX_MAX_SLOTS][RX_WARPS];
     __shared__ unsigned long long s_c1[RX_MAX_SLOTS];
-    __shared__ int64_t s_c2[RX_MAX_SLOTS];
+    __shared__ int64_t s_c2[RX_MAX_SLOTS], s_tend[RX_MAX_SLOTS];
     __shared__ int32_t s_cq[RX_MAX_SLOTS];
-    __shared__ unsigned long long s_hist[RX_MAXCAP + 2];
-    __shared__ uint32_t s_chg;
+    __shared__ uint32_t s_hist[RX_MAXCAP + 2];
+    __shared__ int64_t s_tile[RX_WARPS][257];  // one 256-iteration tile's tau (+ the next)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t G = (int32_t)gridDim.x, blk = (int32_t)blockIdx.x;
     const int64_t gthreads = (int64_t)G * RX_THREADS;
@@ -422,6 +425,7 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
         s_cap[tid] = c >= 0 ? chains[c].cap : 0;
         s_M[tid] = c >= 0 ? slots[tid].M : 0;
     }
+    if (tid < RX_MAXCAP + 2) s_hist[tid] = 0u;
     // phase 0: stitch the guess segments (block s: slot s) and zero the histograms
     if (blk < nslots && ((active >> blk) & 1)) {
         DRelax &S = slots[blk];
@@ -440,14 +444,12 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
     }
     for (int s = 0; s < nslots; ++s) {
         if (!((active >> s) & 1)) continue;
-        unsigned long long *h = slots[s].h;
-        const int64_t L = slots[s].lcap;
-        for (int64_t i = gtid; i < L; i += gthreads) h[i] = 0ull;
+        uint4 *h4 = reinterpret_cast<uint4 *>(slots[s].h);
+        const int64_t L4 = slots[s].lcap / 4;
+        for (int64_t i = gtid; i < L4; i += gthreads) h4[i] = make_uint4(0u, 0u, 0u, 0u);
     }
     __syncthreads();
-    if (dbg && blk == 0 && tid == 0) printf("k_relax phase 0 start %llu\n", (unsigned long long)rx_now());
     grid.sync();
-    if (dbg && blk == 0 && tid == 0) printf("k_relax phase 0 done %llu\n", (unsigned long long)rx_now());
 
     uint64_t tph[4] = {0, 0, 0, 0}, pv[4] = {0, 0, 0, 0}, t_last = rx_now();
     auto lap = [&](int k) {
@@ -455,12 +457,45 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
         tph[k] += t - t_last;
         t_last = t;
     };
-    // a warp's super-tiles (256 iterations) of slot s: [*w0, *w1)
-    auto warp_tiles = [&](int64_t n, int64_t &w0, int64_t &w1) {
+    // a warp's super-tiles (256 iterations) of n iterations: [w0, w1)
+    auto warp_tiles = [&](int64_t n, int w, int64_t &w0, int64_t &w1) {
         const int64_t nst = (n + 255) / 256;
         const int64_t b0 = nst * blk / G, b1 = nst * (blk + 1) / G;
-        w0 = b0 + (b1 - b0) * warp / RX_WARPS;
-        w1 = b0 + (b1 - b0) * (warp + 1) / RX_WARPS;
+        w0 = b0 + (b1 - b0) * w / RX_WARPS;
+        w1 = b0 + (b1 - b0) * (w + 1) / RX_WARPS;
+    };
+    // one lane's 8 boundaries of a super-tile: packed (joins << 32 | leaves) counts
+    auto load8 = [&](const uint32_t *h, int64_t e0, int64_t n, unsigned long long (&v)[RX_EPT]) {
+        if (e0 + RX_EPT <= n) {
+            const uint4 *src = reinterpret_cast<const uint4 *>(h + e0);
+            const uint4 x0 = __ldcg(src), x1 = __ldcg(src + 1);
+            const uint32_t w[8] = {x0.x, x0.y, x0.z, x0.w, x1.x, x1.y, x1.z, x1.w};
+#pragma unroll
+            for (int k = 0; k < RX_EPT; ++k)
+                v[k] = ((unsigned long long)(w[k] >> 16) << 32) | (w[k] & 0xFFFFu);
+        } else {
+#pragma unroll
+            for (int k = 0; k < RX_EPT; ++k) {
+                const uint32_t w = e0 + k < n ? __ldcg(h + e0 + k) : 0u;
+                v[k] = ((unsigned long long)(w >> 16) << 32) | (w & 0xFFFFu);
+            }
+        }
+    };
+    // inclusive prefix of the lane's 8 plus the warp's carry; returns the lane's
+    // exclusive base and advances carry past the super-tile
+    auto prefix8 = [&](unsigned long long (&v)[RX_EPT], unsigned long long &carry) {
+#pragma unroll
+        for (int k = 1; k < RX_EPT; ++k) v[k] += v[k - 1];
+        unsigned long long inc = v[RX_EPT - 1];
+        for (int o = 1; o < 32; o <<= 1) {
+            const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+            if (lane >= o) inc += y;
+        }
+        const unsigned long long base = carry + inc - v[RX_EPT - 1];
+        carry += __shfl_sync(FULL, inc, 31);
+#pragma unroll
+        for (int k = 0; k < RX_EPT; ++k) v[k] += base;
+        return base;
     };
     int sw = 0;
     for (; active; ++sw) {
@@ -473,6 +508,12 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
             // the race: drop the chain once k_decode's leader has finished it
             if (ld_relaxed_gpu(&chains[slots[tid].chain].x->pad) & RX_SERIAL) slots[tid].quit = 1;
         }
+        if (blk == 1 % G) {
+            for (int i = tid; i < nslots * (RX_MAXCAP + 1); i += RX_THREADS) {
+                const int s = i / (RX_MAXCAP + 1);
+                if ((active >> s) & 1) slots[s].cnt[par][i % (RX_MAXCAP + 1)] = 0ull;
+            }
+        }
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
             DRelax &S = slots[s];
@@ -483,13 +524,13 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
                 int64_t j = __ldcg(S.J + q);
                 if (sw == 0) {  // first sweep: the stitched guess
                     j += __ldcg(S.seg + 2 * (q / RX_SEG));
-                    j = min(max(j, (int64_t)0), S.lcap - 4);
+                    j = min(max(j, (int64_t)0), S.lcap - 8);
                     S.J[q] = (int32_t)j;
                 }
                 const int64_t F = j + __ldg(&ch.dec_dj[q].x);
-                if (F + 2 < S.lcap) {
-                    atomicAdd(S.h + j, 1ull << 32);
-                    atomicAdd(S.h + F, 1ull);
+                if (F + 4 < S.lcap) {
+                    atomicAdd(S.h + j, 1u << 16);
+                    atomicAdd(S.h + F, 1u);
                 }
                 fv = max(fv, (int32_t)min(F, (int64_t)INT32_MAX));
             }
@@ -507,7 +548,7 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
         __syncthreads();
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
-            if ((int64_t)s_Lc[s] + 2 >= slots[s].lcap || s_cq[s]) {
+            if ((int64_t)s_Lc[s] + 4 >= slots[s].lcap || s_cq[s]) {
                 active &= ~(1u << s);
                 if (blk == 0 && tid == 0) {
                     slots[s].state = 2;
@@ -519,18 +560,19 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
         // ---- B1: the block's share of each slot's histogram sum
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
-            const unsigned long long *h = slots[s].h;
+            const uint32_t *h = slots[s].h;
             const int64_t n = (int64_t)s_Lc[s] + 1;
             int64_t w0, w1;
-            warp_tiles(n, w0, w1);
+            warp_tiles(n, warp, w0, w1);
             const int64_t e1 = min(w1 * 256, n);
             unsigned long long sum = 0;
-            for (int64_t i = w0 * 256 + lane; i < e1; i += 128) {
-                const unsigned long long x0 = __ldcg(h + i);
-                const unsigned long long x1 = i + 32 < e1 ? __ldcg(h + i + 32) : 0ull;
-                const unsigned long long x2 = i + 64 < e1 ? __ldcg(h + i + 64) : 0ull;
-                const unsigned long long x3 = i + 96 < e1 ? __ldcg(h + i + 96) : 0ull;
-                sum += x0 + x1 + x2 + x3;
+            for (int64_t i = w0 * 256 + lane; i < e1; i += 256) {
+                uint32_t x[8];
+#pragma unroll
+                for (int u = 0; u < 8; ++u) x[u] = i + 32 * u < e1 ? __ldcg(h + i + 32 * u) : 0u;
+#pragma unroll
+                for (int u = 0; u < 8; ++u)
+                    sum += ((unsigned long long)(x[u] >> 16) << 32) | (x[u] & 0xFFFFu);
             }
             for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
             if (lane == 0) s_wsum[s][warp] = sum;
@@ -559,7 +601,7 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
             if (lane == 0) s_c1[s] = c;
         }
         __syncthreads();
-        // ---- B2: prefix P (written; h zeroed), the warp's composed map
+        // ---- B2: the warp's composed map; S_q at the boundary where G reaches q - cap + 1
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
             DRelax &S = slots[s];
@@ -567,55 +609,28 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
             const int32_t M = s_M[s], cap = s_cap[s];
             const int64_t n = (int64_t)s_Lc[s] + 1;
             int64_t w0, w1;
-            warp_tiles(n, w0, w1);
+            warp_tiles(n, warp, w0, w1);
             unsigned long long carry = s_c1[s];
             for (int w = 0; w < warp; ++w) carry += s_wsum[s][w];
             RxMap acc{0, NEG_INF};
             for (int64_t st = w0; st < w1; ++st) {
                 const int64_t e0 = st * 256 + RX_EPT * lane;
                 unsigned long long v[RX_EPT];
-                if (e0 + RX_EPT <= n) {
-                    const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(S.h + e0);
-#pragma unroll
-                    for (int k = 0; k < RX_EPT / 2; ++k) {
-                        const ulonglong2 x = __ldcg(src + k);
-                        v[2 * k] = x.x;
-                        v[2 * k + 1] = x.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < RX_EPT; ++k) v[k] = e0 + k < n ? __ldcg(S.h + e0 + k) : 0ull;
-                }
-#pragma unroll
-                for (int k = 1; k < RX_EPT; ++k) v[k] += v[k - 1];
-                unsigned long long inc = v[RX_EPT - 1];
-                for (int o = 1; o < 32; o <<= 1) {
-                    const unsigned long long y = __shfl_up_sync(FULL, inc, o);
-                    if (lane >= o) inc += y;
-                }
-                const unsigned long long base = carry + inc - v[RX_EPT - 1];
-                carry += __shfl_sync(FULL, inc, 31);
+                load8(S.h, e0, n, v);
+                const unsigned long long base = prefix8(v, carry);
+                int64_t gprev = (int64_t)(base & 0xFFFFFFFFull);
                 RxMap cm{0, NEG_INF};
 #pragma unroll
                 for (int k = 0; k < RX_EPT; ++k) {
-                    v[k] += base;
-                    if (e0 + k < n) cm = rx_then(cm, rx_iter_map(v[k], s_step[s], cap, M, dec_r));
-                }
-                if (e0 + RX_EPT <= n) {
-                    ulonglong2 *dp = reinterpret_cast<ulonglong2 *>(S.P + e0);
-                    ulonglong2 *dh = reinterpret_cast<ulonglong2 *>(S.h + e0);
-#pragma unroll
-                    for (int k = 0; k < RX_EPT / 2; ++k) {
-                        dp[k] = make_ulonglong2(v[2 * k], v[2 * k + 1]);
-                        dh[k] = make_ulonglong2(0ull, 0ull);
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < RX_EPT; ++k)
-                        if (e0 + k < n) {
-                            S.P[e0 + k] = v[k];
-                            S.h[e0 + k] = 0ull;
+                    if (e0 + k < n) {
+                        cm = rx_then(cm, rx_iter_map(v[k], s_step[s], cap, M, dec_r));
+                        const int64_t gk = (int64_t)(v[k] & 0xFFFFFFFFull);
+                        for (int64_t need = gprev + 1; need <= gk; ++need) {
+                            const int64_t q = need + cap - 1;
+                            if (q < M) S.Sq[q] = (int32_t)(e0 + k);
                         }
+                        gprev = gk;
+                    }
                 }
                 for (int o = 1; o < 32; o <<= 1) {
                     const RxMap y = rx_shfl_up(cm, o);
@@ -658,7 +673,24 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
             if (lane == 0) s_c2[s] = rx_apply(acc, __ldg(chains[slots[s].chain].dec_r));
         }
         __syncthreads();
-        // ---- B3: tau
+        // ---- B3: tau; A_q by merging the ready times into each tile's tau
+        // lane s: tau at this warp's first boundary and its first request in the merge
+        int64_t x_l = 0;
+        int32_t qa_l = 0;
+        if (lane < nslots && ((active >> lane) & 1)) {
+            const int s = lane;
+            int64_t w0, w1;
+            warp_tiles((int64_t)s_Lc[s] + 1, warp, w0, w1);
+            x_l = s_c2[s];
+            for (int w = 0; w < warp; ++w) x_l = rx_apply(RxMap{s_wa[s][w], s_wb[s][w]}, x_l);
+            if (w0 > 0 && w1 > w0) {  // first request with r > tau(i0) (warm start: last sweep's)
+                const int64_t *dr = chains[slots[s].chain].dec_r;
+                const int32_t M = s_M[s];
+                qa_l = rx_search([&](int32_t i) { return __ldg(dr + i); }, x_l + 1,
+                                 min(max(__ldcg(&slots[s].blk[blk].qa[warp]), 0), M - 1), 0, M - 1);
+                slots[s].blk[blk].qa[warp] = qa_l;
+            }
+        }
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
             DRelax &S = slots[s];
@@ -666,29 +698,34 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
             const int32_t M = s_M[s], cap = s_cap[s], Lc = s_Lc[s];
             const int64_t n = (int64_t)Lc + 1;
             int64_t w0, w1;
-            warp_tiles(n, w0, w1);
-            int64_t x = s_c2[s];
-            for (int w = 0; w < warp; ++w) x = rx_apply(RxMap{s_wa[s][w], s_wb[s][w]}, x);
+            warp_tiles(n, warp, w0, w1);
+            unsigned long long carry = s_c1[s];
+            for (int w = 0; w < warp; ++w) carry += s_wsum[s][w];
+            int64_t x = __shfl_sync(FULL, x_l, s);
+            int32_t qp = __shfl_sync(FULL, qa_l, s);
+            int64_t pb = -1;  // run-length histogram of b over the lane's boundaries
+            uint32_t run = 0;
+            int64_t rn = qp + lane < M ? __ldg(dec_r + qp + lane) : INT64_MAX;  // next merge candidates
             for (int64_t st = w0; st < w1; ++st) {
                 const int64_t e0 = st * 256 + RX_EPT * lane;
                 unsigned long long v[RX_EPT];
-                if (e0 + RX_EPT <= n) {
-                    const ulonglong2 *src = reinterpret_cast<const ulonglong2 *>(S.P + e0);
-#pragma unroll
-                    for (int k = 0; k < RX_EPT / 2; ++k) {
-                        const ulonglong2 y = __ldcg(src + k);
-                        v[2 * k] = y.x;
-                        v[2 * k + 1] = y.y;
-                    }
-                } else {
-#pragma unroll
-                    for (int k = 0; k < RX_EPT; ++k) v[k] = e0 + k < n ? __ldcg(S.P + e0 + k) : 0ull;
-                }
+                load8(S.h, e0, n, v);
+                prefix8(v, carry);
                 RxMap mk[RX_EPT];
                 RxMap cm{0, NEG_INF};
 #pragma unroll
                 for (int k = 0; k < RX_EPT; ++k) {
-                    mk[k] = e0 + k < n ? rx_iter_map(v[k], s_step[s], cap, M, dec_r) : RxMap{0, NEG_INF};
+                    mk[k] = RxMap{0, NEG_INF};
+                    if (e0 + k < n) {
+                        mk[k] = rx_iter_map(v[k], s_step[s], cap, M, dec_r);
+                        const int64_t b = (int64_t)(v[k] >> 32) - (int64_t)(v[k] & 0xFFFFFFFFull);
+                        if (b != pb) {
+                            if (run && pb >= 0 && pb <= RX_MAXCAP) atomicAdd(&s_hist[pb], run);
+                            pb = b;
+                            run = 0;
+                        }
+                        ++run;
+                    }
                     cm = rx_then(cm, mk[k]);
                 }
                 RxMap in = cm;
@@ -704,96 +741,89 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
                 for (int k = 0; k < RX_EPT; ++k) {
                     tv[k] = y;
                     y = rx_apply(mk[k], y);
-                    if (e0 + k == Lc) S.tau[Lc + 1] = y;
+                    if (e0 + k == Lc) {
+                        S.tau[Lc + 1] = y;
+                        S.tend = y;
+                    }
                 }
                 if (e0 + RX_EPT <= n) {
                     longlong2 *dt = reinterpret_cast<longlong2 *>(S.tau + e0);
 #pragma unroll
                     for (int k = 0; k < RX_EPT / 2; ++k) dt[k] = make_longlong2(tv[2 * k], tv[2 * k + 1]);
+                    uint4 *dh = reinterpret_cast<uint4 *>(S.h + e0);
+                    dh[0] = make_uint4(0u, 0u, 0u, 0u);
+                    dh[1] = make_uint4(0u, 0u, 0u, 0u);
                 } else {
 #pragma unroll
                     for (int k = 0; k < RX_EPT; ++k)
-                        if (e0 + k < n) S.tau[e0 + k] = tv[k];
+                        if (e0 + k < n) {
+                            S.tau[e0 + k] = tv[k];
+                            S.h[e0 + k] = 0u;
+                        }
                 }
-                x = rx_apply(rx_shfl(in, 31), x);
+                const int64_t xn = rx_apply(rx_shfl(in, 31), x);  // tau at the next tile's start
+                // A_q for r_q in (tau(base), tau(base + 256)] (and r_q <= tau(0) at base 0)
+#pragma unroll
+                for (int k = 0; k < RX_EPT; ++k) s_tile[warp][RX_EPT * lane + k] = tv[k];
+                if (lane == 0) s_tile[warp][256] = xn;
+                __syncwarp();
+                const int lo0 = st == 0 ? 0 : 1;
+                for (;;) {
+                    const int32_t q = qp + lane;
+                    const int64_t rq = rn;
+                    const bool ok = rq <= xn;
+                    const unsigned bal = __ballot_sync(FULL, ok);
+                    {  // the candidates after this round's consumed ones
+                        const int c = __popc(bal);
+                        const int32_t qn = qp + c + lane;
+                        const int64_t sh = __shfl_sync(FULL, rq, (lane + c) & 31);
+                        rn = lane + c < 32 ? sh : (qn < M ? __ldg(dec_r + qn) : INT64_MAX);
+                    }
+                    if (ok) {
+                        int a = lo0 - 1, bnd = 256;  // first index in [lo0, 256] with tau >= rq
+                        while (bnd - a > 1) {
+                            const int m = (a + bnd) >> 1;
+                            if (s_tile[warp][m] >= rq) bnd = m;
+                            else a = m;
+                        }
+                        S.A[q] = (int32_t)(st * 256 + bnd);
+                    }
+                    qp += __popc(bal);
+                    if (bal != FULL) break;
+                }
+                __syncwarp();
+                x = xn;
             }
+            if (run && pb >= 0 && pb <= RX_MAXCAP) atomicAdd(&s_hist[pb], run);
+            __syncthreads();
+            if (tid <= RX_MAXCAP && s_hist[tid]) {
+                atomicAdd(&S.cnt[par][tid], (unsigned long long)s_hist[tid]);
+                s_hist[tid] = 0u;
+            }
+            if (tid == RX_MAXCAP + 1) s_hist[tid] = 0u;
+            __syncthreads();
         }
         grid.sync();
         lap(1);
-        // ---- C1: per request A_q, S_q; prefix max within the block's chunk
+        if (tid < nslots) s_tend[tid] = ((active >> tid) & 1) ? __ldcg(&slots[tid].tend) : 0;
+        __syncthreads();
+        // ---- C1: m_q = max(A_q, S_q); prefix max within the block's chunk
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
             DRelax &S = slots[s];
             const int64_t *dec_r = chains[S.chain].dec_r;
             const int32_t M = s_M[s], cap = s_cap[s], Lc = s_Lc[s];
-            const int64_t *tau = S.tau;
-            const unsigned long long *Pp = S.P;
+            const int64_t tend = s_tend[s];
             const int32_t c0 = (int32_t)((int64_t)M * blk / G), c1 = (int32_t)((int64_t)M * (blk + 1) / G);
             const int32_t t0 = c0 + (int32_t)((int64_t)(c1 - c0) * tid / RX_THREADS);
             const int32_t t1 = c0 + (int32_t)((int64_t)(c1 - c0) * (tid + 1) / RX_THREADS);
             int32_t run = INT32_MIN;
-            for (int32_t q0 = t0; q0 < t1; q0 += 4) {
-                int32_t jv[4];
-                int64_t rv[4], ta[4], tb[4];
-                unsigned long long pa[4], pb[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int32_t q = min(q0 + u, t1 - 1);
-                    jv[u] = __ldcg(S.J + q);
-                    rv[u] = __ldg(dec_r + q);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int32_t j = jv[u];
-                    ta[u] = j > 0 ? __ldcg(tau + j - 1) : INT64_MIN;
-                    tb[u] = __ldcg(tau + j);
-                    pa[u] = j > 0 ? __ldcg(Pp + j - 1) : 0ull;
-                    pb[u] = __ldcg(Pp + j);
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int32_t q = q0 + u;
-                    if (q >= t1) break;
-                    const int32_t j = jv[u];
-                    const int64_t r = rv[u];
-                    // m = max(A_q, S_q) needs only the binding constraint exactly: at a
-                    // converged request both are <= j and one of them equals j
-                    const int64_t need = (int64_t)q - cap + 1;
-                    const int64_t ga = j > 0 ? (int64_t)(pa[u] & 0xFFFFFFFFull) : -1;
-                    const int64_t gb = (int64_t)(pb[u] & 0xFFFFFFFFull);
-                    auto fa = [&](int32_t i) { return __ldcg(tau + i); };
-                    auto fg = [&](int32_t i) { return (int64_t)(__ldcg(Pp + i) & 0xFFFFFFFFull); };
-                    const bool cA = tb[u] >= r, cS = need <= 0 || gb >= need;
-                    int32_t m;
-                    // searches start at an interpolated boundary: the local step
-                    // tau(j) - tau(j-1) for A, the mean iterations per leave for S
-                    const int64_t lst = j > 0 ? max(tb[u] - ta[u], (int64_t)1) : (int64_t)s_step[s][cap];
-                    const int64_t ipl = max((int64_t)1, (int64_t)Lc / max(M, 1));
-                    if (cA && cS) {
-                        if (ta[u] < r || (need > 0 && ga < need)) {
-                            m = j;
-                        } else {  // both strictly below j
-                            const int64_t ea = j - 1 - (ta[u] - r) / lst;
-                            m = rx_search(fa, r, (int32_t)max(ea, (int64_t)0), 0, j - 1);
-                            if (need > 0) {
-                                const int64_t es = j - 1 - (ga - need) * ipl;
-                                m = max(m, rx_search(fg, need, (int32_t)max(es, (int64_t)0), 0, j - 1));
-                            }
-                        }
-                    } else {  // the failing ones are above j
-                        m = INT32_MIN;
-                        if (!cA) {
-                            const int64_t ea = j + (r - tb[u] + lst - 1) / lst;
-                            m = rx_search(fa, r, (int32_t)min(ea, (int64_t)Lc + 1), j + 1, Lc + 1);
-                        }
-                        if (!cS) {
-                            const int64_t es = j + (need - gb) * ipl;
-                            m = max(m, rx_search(fg, need, (int32_t)min(es, (int64_t)Lc), j + 1, Lc));
-                        }
-                    }
-                    run = max(run, m);
-                    S.A[q] = run;
-                }
+            for (int32_t q = t0; q < t1; ++q) {
+                // unwritten A: ready after tau(Lc + 1), so not before boundary Lc + 2
+                const int32_t a = __ldg(dec_r + q) > tend ? Lc + 2 : __ldcg(S.A + q);
+                const int32_t sq = (int64_t)q - cap + 1 > 0 ? __ldcg(S.Sq + q) : 0;
+                run = max(run, max(a, sq));
+                S.A[q] = run;
             }
             int32_t tot;
             const int32_t exq = rx_block_excl_max(run, s_i32, tot);
@@ -820,7 +850,6 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
             for (int o = 16; o; o >>= 1) c = max(c, __shfl_xor_sync(FULL, c, o));
             if (lane == 0) s_cq[s] = c;
         }
-        if (tid == 0) s_chg = 0;
         __syncthreads();
         lap(2);
         // ---- C2: J' = max(carry, block prefix); changed?
@@ -843,8 +872,7 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
         grid.sync();
         lap(3);
         if (dbg == 2 && blk == 0 && tid == 0)
-            printf("sweep %d active %x: searches %llu probes %llu  A %.1f B %.1f C1 %.1f C2 %.1f us (total %.3f ms)\n", sw, active,
-                   atomicExch(&g_rx_probes[0], 0ull), atomicExch(&g_rx_probes[1], 0ull),
+            printf("sweep %d active %x: A %.1f B %.1f C1 %.1f C2 %.1f us (total %.3f ms)\n", sw, active,
                    (tph[0] - pv[0]) * 1e-3, (tph[1] - pv[1]) * 1e-3, (tph[2] - pv[2]) * 1e-3,
                    (tph[3] - pv[3]) * 1e-3, (tph[0] + tph[1] + tph[2] + tph[3]) * 1e-6);
         for (int k = 0; k < 4; ++k) pv[k] = tph[k];
@@ -867,41 +895,17 @@ __global__ void __launch_bounds__(RX_THREADS, 1)
         }
         __syncthreads();
     }
-    grid.sync();
-    if (dbg && blk == 0 && tid == 0)
-        printf("k_relax %d sweeps: scatter %.3f ms, iterations %.3f ms, requests %.3f + %.3f ms\n", sw,
-               tph[0] * 1e-6, tph[1] * 1e-6, tph[2] * 1e-6, tph[3] * 1e-6);
-    // ---- owned slots: iterations per batch size over [0, Lf] (run-length per lane);
-    // k_relax_out writes the finish times and statistics after k_decode has finished
-    for (int s = 0; s < nslots; ++s) {
-        DRelax &S = slots[s];
-        const int32_t c = S.chain;
-        if (c < 0) continue;
-        const int32_t state = ld_relaxed_gpu(&S.state);
-        if (dbg && blk == 0 && tid == 0)
-            printf("k_relax slot %d chain %d M %d state %d sweeps %d Lf %d pad %x\n", s, c, S.M, state,
-                   S.sweeps, S.Lf, ld_relaxed_gpu(&chains[c].x->pad));
-        if (state != 3) continue;
-        // iterations per batch size over [0, Lf] (run-length per lane)
-        if (tid < RX_MAXCAP + 2) s_hist[tid] = 0ull;
-        __syncthreads();
-        const int32_t Lf = ld_relaxed_gpu(&S.Lf);
-        int64_t pb = -1, run = 0;
-        const int64_t i0 = ((int64_t)Lf + 1) * gtid / gthreads, i1 = ((int64_t)Lf + 1) * (gtid + 1) / gthreads;
-        for (int64_t i = i0; i < i1; ++i) {
-            const unsigned long long P = __ldcg(S.P + i);
-            const int64_t b = (int64_t)(P >> 32) - (int64_t)(P & 0xFFFFFFFFull);
-            if (b != pb) {
-                if (run && pb >= 0 && pb <= RX_MAXCAP) atomicAdd(&s_hist[pb], (unsigned long long)run);
-                pb = b;
-                run = 0;
-            }
-            ++run;
+    if (dbg) {
+        grid.sync();
+        if (blk == 0 && tid == 0) {
+            printf("k_relax %d sweeps: scatter %.3f ms, iterations %.3f ms, requests %.3f + %.3f ms\n", sw,
+                   tph[0] * 1e-6, tph[1] * 1e-6, tph[2] * 1e-6, tph[3] * 1e-6);
+            for (int s = 0; s < nslots; ++s)
+                if (slots[s].chain >= 0)
+                    printf("k_relax slot %d chain %d M %d state %d sweeps %d Lf %d pad %x\n", s,
+                           slots[s].chain, slots[s].M, ld_relaxed_gpu(&slots[s].state), slots[s].sweeps,
+                           slots[s].Lf, ld_relaxed_gpu(&chains[slots[s].chain].x->pad));
         }
-        if (run && pb >= 0 && pb <= RX_MAXCAP) atomicAdd(&s_hist[pb], (unsigned long long)run);
-        __syncthreads();
-        if (tid <= RX_MAXCAP && s_hist[tid]) atomicAdd(&S.cnt[tid], s_hist[tid]);
-        __syncthreads();
     }
 }
 
@@ -924,7 +928,7 @@ __global__ void __launch_bounds__(256)
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         int64_t a0 = 0, a1 = 0, a2 = 0, a3 = 0;
         for (int bb = 1; bb <= ch.cap; ++bb) {
-            const int64_t it = (int64_t)S.cnt[bb];
+            const int64_t it = (int64_t)S.cnt[(S.sweeps - 1) & 1][bb];
             if (!it) continue;
             a0 += it * __ldg(ch.sbn + bb);
             a1 += it * __ldg(ch.sbo + bb);
