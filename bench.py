@@ -495,9 +495,10 @@ def run_ours(args):
                      "latency": latency,
                      "alu_view": alu_view(winst, kdec_ms, sm_mhz, grid, lo, hi),
                      "note": "bound = latency: k_decode runs one serial event loop per timing "
-                             "chain (a busy period cannot be split exactly), so the step lasts as "
-                             "long as the slowest chain's dependent chain of events; HBM and the "
-                             "issue rate are both far from saturated (DESIGN.md §4)"},
+                             "chain, so the step lasts as long as the slowest chain it walks; "
+                             "k_relax (the decode stage as an exact parallel fixed point) races it "
+                             "on the heavily loaded chains and takes those it solves first; HBM "
+                             "and the issue rate are both far from saturated (DESIGN.md §4)"},
         "cpu_baseline": cpu,
         "e2e": e2e,
         "gpu_launches": launches,

@@ -535,12 +535,13 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     total += align256(sizeof(int32_t) * ((size_t)n_chains * 3 + 2));
     // k_relax (exact parallel decode of heavily loaded chains, k_relax.cuh): slots for
     // the chains k_relax_pick selects on the device by load factor.  Not with the link
-    // analysis (it needs the batch-size log) or a launch-order hint.  Opt-in: it races
-    // k_decode for SM issue slots and measured no net gain on the five configurations
-    // (DESIGN.md §10).  GL_RELAX=1 turns it on; GL_RELAX=force (tests) makes every
-    // one-row chain eligible at any load.
+    // analysis (it needs the batch-size log) or a launch-order hint, and by default not
+    // beside co-located chains (their decode shares the SMs' issue slots with it:
+    // config 6 +5%, config 7 +1.6%; config 4 -5.8%).  GL_RELAX=0 turns
+    // it off, GL_RELAX=1 on; GL_RELAX=force (tests) makes every one-row chain eligible
+    // at any load.
     const char *rx_env = std::getenv("GL_RELAX");
-    const bool rx_off = !rx_env || (rx_env[0] != '1' && rx_env[0] != 'f' && rx_env[0] != 's');
+    const bool rx_off = rx_env ? (rx_env[0] != '1' && rx_env[0] != 'f' && rx_env[0] != 's') : has_colo;
     const bool rx_force = rx_env && (rx_env[0] == 'f' || rx_env[0] == 's');
     // GL_RELAX=solo (tests): k_relax runs first on `stream`, so it wins every chain it
     // solves and k_decode walks only the rest
@@ -567,7 +568,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     int32_t rx_slots = 0;
     if (rx_elig > 0) {
         const size_t per = 3 * rx_b_j + rx_b_seg + rx_b_l + rx_b_h + rx_b_blk;
-        rx_slots = (int32_t)std::min<int64_t>(std::min<int64_t>(rx_elig, rx_force ? 16 : gl::RX_DEF_SLOTS),
+        rx_slots = (int32_t)std::min<int64_t>(std::min<int64_t>(rx_elig, rx_force ? gl::RX_MAX_SLOTS : gl::RX_DEF_SLOTS),
                                               (int64_t)(((size_t)4 << 30) / per));
     }
     const size_t off_rx_blk = total;
@@ -900,7 +901,10 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             if (e == cudaSuccess) {
                 // one block per SM: room beside k_decode's warps (registers), all resident
                 int per_sm = 0;
-                e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl::k_relax, gl::RX_THREADS, 0);
+                const size_t rx_smem = (size_t)rx_slots * gl::RX_THREADS * 24;  // lane carries and maps
+                e = cudaFuncSetAttribute(gl::k_relax, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)rx_smem);
+                if (e == cudaSuccess)
+                    e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, gl::k_relax, gl::RX_THREADS, rx_smem);
                 if (e == cudaSuccess && per_sm < 1) e = cudaErrorCooperativeLaunchTooLarge;
                 if (e == cudaSuccess) {
                     int32_t ns = rx_slots;
@@ -909,9 +913,15 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                     void *args[] = {&d_slots, &ns, (void *)&dc, &dbg};
                     prof_begin("k_relax", xs);
                     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(gl::k_relax),
-                                                    dim3((unsigned)n_sm), dim3(gl::RX_THREADS), args, 0, xs);
+                                                    dim3((unsigned)n_sm), dim3(gl::RX_THREADS), args, rx_smem, xs);
                     prof_end(xs);
                     ++launches;
+                }
+                // k_relax is an accelerator: without it k_decode walks every chain (no slot
+                // is ever marked solved, k_relax_out writes nothing)
+                if (e != cudaSuccess) {
+                    cudaGetLastError();
+                    e = cudaSuccess;
                 }
             }
         };

@@ -54,7 +54,7 @@ constexpr int RX_GWARPS = 4;      // guess warps per block
 constexpr int RX_THREADS = 256;   // k_relax block
 constexpr int RX_EPT = 8;         // iterations per lane per warp step
 constexpr int RX_WARPS = RX_THREADS / 32;
-constexpr int RX_MAX_SLOTS = 32;
+constexpr int RX_MAX_SLOTS = 16;
 constexpr int RX_MAX_SWEEPS = 160;
 constexpr int RX_LFACTOR = 40;    // iteration capacity per request
 constexpr int RX_MAXCAP = 31;     // one member per lane in the guess
@@ -69,7 +69,7 @@ struct RxBlk {
     unsigned long long s1;   // packed (joins << 32 | leaves) count of the block's iterations
     int64_t a2, b2;          // max-plus map x -> max(x + a2, b2) of the block's iterations
     int32_t mc, pad2;        // max of the block's requests' max(A_q, S_q)
-    int32_t qa[8];           // per warp: its first request in the A merge (warm start)
+    int32_t qa[256];         // per thread: its first request in the A merge (warm start)
     int64_t pad3;
 };
 
@@ -406,7 +406,11 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
     __shared__ int64_t s_c2[RX_MAX_SLOTS], s_tend[RX_MAX_SLOTS];
     __shared__ int32_t s_cq[RX_MAX_SLOTS];
     __shared__ uint32_t s_hist[RX_MAXCAP + 2];
-    __shared__ int64_t s_tile[RX_WARPS][257];  // one 256-iteration tile's tau (+ the next)
+    // per slot and thread: lane carry (exclusive within the warp) and lane map prefix
+    extern __shared__ __align__(16) unsigned char rx_dyn[];
+    unsigned long long *s_lc = reinterpret_cast<unsigned long long *>(rx_dyn);          // [nslots][256]
+    int64_t *s_la = reinterpret_cast<int64_t *>(rx_dyn) + (size_t)nslots * RX_THREADS;  // [nslots][256]
+    int64_t *s_lb = s_la + (size_t)nslots * RX_THREADS;                                  // [nslots][256]
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int32_t G = (int32_t)gridDim.x, blk = (int32_t)blockIdx.x;
     const int64_t gthreads = (int64_t)G * RX_THREADS;
@@ -464,6 +468,16 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
         w0 = b0 + (b1 - b0) * w / RX_WARPS;
         w1 = b0 + (b1 - b0) * (w + 1) / RX_WARPS;
     };
+    // this lane's boundaries [a_l, b_l) of n: the warp's sub-chunk of the block's chunk,
+    // split into lane-contiguous runs of whole 8-boundary units
+    auto lane_range = [&](int64_t n, int64_t &a_l, int64_t &b_l) {
+        int64_t w0, w1;
+        warp_tiles(n, warp, w0, w1);
+        const int64_t E0 = w0 * 256, E1 = min(w1 * 256, n);
+        const int64_t nu = (E1 - E0 + RX_EPT - 1) / RX_EPT;
+        a_l = min(E0 + RX_EPT * (nu * lane / 32), E1);
+        b_l = min(E0 + RX_EPT * (nu * (lane + 1) / 32), E1);
+    };
     // one lane's 8 boundaries of a super-tile: packed (joins << 32 | leaves) counts
     auto load8 = [&](const uint32_t *h, int64_t e0, int64_t n, unsigned long long (&v)[RX_EPT]) {
         if (e0 + RX_EPT <= n) {
@@ -480,22 +494,6 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
                 v[k] = ((unsigned long long)(w >> 16) << 32) | (w & 0xFFFFu);
             }
         }
-    };
-    // inclusive prefix of the lane's 8 plus the warp's carry; returns the lane's
-    // exclusive base and advances carry past the super-tile
-    auto prefix8 = [&](unsigned long long (&v)[RX_EPT], unsigned long long &carry) {
-#pragma unroll
-        for (int k = 1; k < RX_EPT; ++k) v[k] += v[k - 1];
-        unsigned long long inc = v[RX_EPT - 1];
-        for (int o = 1; o < 32; o <<= 1) {
-            const unsigned long long y = __shfl_up_sync(FULL, inc, o);
-            if (lane >= o) inc += y;
-        }
-        const unsigned long long base = carry + inc - v[RX_EPT - 1];
-        carry += __shfl_sync(FULL, inc, 31);
-#pragma unroll
-        for (int k = 0; k < RX_EPT; ++k) v[k] += base;
-        return base;
     };
     int sw = 0;
     for (; active; ++sw) {
@@ -557,25 +555,29 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
             }
         }
         if (!active) break;
-        // ---- B1: the block's share of each slot's histogram sum
+        // ---- B1: lane sums over lane-contiguous ranges (8-boundary units) of the
+        // warp's sub-chunk; lane carries (exclusive in the warp) and the block's sum
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
             const uint32_t *h = slots[s].h;
             const int64_t n = (int64_t)s_Lc[s] + 1;
-            int64_t w0, w1;
-            warp_tiles(n, warp, w0, w1);
-            const int64_t e1 = min(w1 * 256, n);
+            int64_t a_l, b_l;
+            lane_range(n, a_l, b_l);
             unsigned long long sum = 0;
-            for (int64_t i = w0 * 256 + lane; i < e1; i += 256) {
-                uint32_t x[8];
+            for (int64_t e0 = a_l; e0 < b_l; e0 += 2 * RX_EPT) {  // two units in flight
+                unsigned long long v[RX_EPT], w[RX_EPT];
+                load8(h, e0, b_l, v);
+                load8(h, e0 + RX_EPT, b_l, w);
 #pragma unroll
-                for (int u = 0; u < 8; ++u) x[u] = i + 32 * u < e1 ? __ldcg(h + i + 32 * u) : 0u;
-#pragma unroll
-                for (int u = 0; u < 8; ++u)
-                    sum += ((unsigned long long)(x[u] >> 16) << 32) | (x[u] & 0xFFFFu);
+                for (int k = 0; k < RX_EPT; ++k) sum += v[k] + w[k];
             }
-            for (int o = 16; o; o >>= 1) sum += __shfl_xor_sync(FULL, sum, o);
-            if (lane == 0) s_wsum[s][warp] = sum;
+            unsigned long long inc = sum;
+            for (int o = 1; o < 32; o <<= 1) {
+                const unsigned long long y = __shfl_up_sync(FULL, inc, o);
+                if (lane >= o) inc += y;
+            }
+            s_lc[s * RX_THREADS + tid] = inc - sum;
+            if (lane == 31) s_wsum[s][warp] = inc;
         }
         __syncthreads();
         if (tid < nslots && ((active >> tid) & 1)) {
@@ -601,30 +603,33 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
             if (lane == 0) s_c1[s] = c;
         }
         __syncthreads();
-        // ---- B2: the warp's composed map; S_q at the boundary where G reaches q - cap + 1
+        // ---- B2: each lane walks its range: prefix P, the iterations' maps (lane map),
+        // S_q at the boundary where the leave count G reaches q - cap + 1
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
             DRelax &S = slots[s];
             const int64_t *dec_r = chains[S.chain].dec_r;
             const int32_t M = s_M[s], cap = s_cap[s];
             const int64_t n = (int64_t)s_Lc[s] + 1;
-            int64_t w0, w1;
-            warp_tiles(n, warp, w0, w1);
-            unsigned long long carry = s_c1[s];
-            for (int w = 0; w < warp; ++w) carry += s_wsum[s][w];
-            RxMap acc{0, NEG_INF};
-            for (int64_t st = w0; st < w1; ++st) {
-                const int64_t e0 = st * 256 + RX_EPT * lane;
+            int64_t a_l, b_l;
+            lane_range(n, a_l, b_l);
+            unsigned long long P = s_c1[s] + s_lc[s * RX_THREADS + tid];
+            for (int w = 0; w < warp; ++w) P += s_wsum[s][w];
+            int64_t gprev = (int64_t)(P & 0xFFFFFFFFull);
+            RxMap lm{0, NEG_INF};
+            unsigned long long vn[RX_EPT];  // the next unit, loaded ahead
+            if (a_l < b_l) load8(S.h, a_l, b_l, vn);
+            for (int64_t e0 = a_l; e0 < b_l; e0 += RX_EPT) {
                 unsigned long long v[RX_EPT];
-                load8(S.h, e0, n, v);
-                const unsigned long long base = prefix8(v, carry);
-                int64_t gprev = (int64_t)(base & 0xFFFFFFFFull);
-                RxMap cm{0, NEG_INF};
+#pragma unroll
+                for (int k = 0; k < RX_EPT; ++k) v[k] = vn[k];
+                if (e0 + RX_EPT < b_l) load8(S.h, e0 + RX_EPT, b_l, vn);
 #pragma unroll
                 for (int k = 0; k < RX_EPT; ++k) {
-                    if (e0 + k < n) {
-                        cm = rx_then(cm, rx_iter_map(v[k], s_step[s], cap, M, dec_r));
-                        const int64_t gk = (int64_t)(v[k] & 0xFFFFFFFFull);
+                    if (e0 + k < b_l) {
+                        P += v[k];
+                        lm = rx_then(lm, rx_iter_map(P, s_step[s], cap, M, dec_r));
+                        const int64_t gk = (int64_t)(P & 0xFFFFFFFFull);
                         for (int64_t need = gprev + 1; need <= gk; ++need) {
                             const int64_t q = need + cap - 1;
                             if (q < M) S.Sq[q] = (int32_t)(e0 + k);
@@ -632,15 +637,19 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
                         gprev = gk;
                     }
                 }
-                for (int o = 1; o < 32; o <<= 1) {
-                    const RxMap y = rx_shfl_up(cm, o);
-                    if (lane >= o) cm = rx_then(y, cm);
-                }
-                acc = rx_then(acc, rx_shfl(cm, 31));
             }
-            if (lane == 0) {
-                s_wa[s][warp] = acc.a;
-                s_wb[s][warp] = acc.b;
+            RxMap in = lm;
+            for (int o = 1; o < 32; o <<= 1) {
+                const RxMap y = rx_shfl_up(in, o);
+                if (lane >= o) in = rx_then(y, in);
+            }
+            RxMap ex = rx_shfl_up(in, 1);
+            if (lane == 0) ex = RxMap{0, NEG_INF};
+            s_la[s * RX_THREADS + tid] = ex.a;
+            s_lb[s * RX_THREADS + tid] = ex.b;
+            if (lane == 31) {
+                s_wa[s][warp] = in.a;
+                s_wb[s][warp] = in.b;
             }
         }
         __syncthreads();
@@ -673,80 +682,68 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
             if (lane == 0) s_c2[s] = rx_apply(acc, __ldg(chains[slots[s].chain].dec_r));
         }
         __syncthreads();
-        // ---- B3: tau; A_q by merging the ready times into each tile's tau
-        // lane s: tau at this warp's first boundary and its first request in the merge
-        int64_t x_l = 0;
-        int32_t qa_l = 0;
-        if (lane < nslots && ((active >> lane) & 1)) {
-            const int s = lane;
-            int64_t w0, w1;
-            warp_tiles((int64_t)s_Lc[s] + 1, warp, w0, w1);
-            x_l = s_c2[s];
-            for (int w = 0; w < warp; ++w) x_l = rx_apply(RxMap{s_wa[s][w], s_wb[s][w]}, x_l);
-            if (w0 > 0 && w1 > w0) {  // first request with r > tau(i0) (warm start: last sweep's)
-                const int64_t *dr = chains[slots[s].chain].dec_r;
-                const int32_t M = s_M[s];
-                qa_l = rx_search([&](int32_t i) { return __ldg(dr + i); }, x_l + 1,
-                                 min(max(__ldcg(&slots[s].blk[blk].qa[warp]), 0), M - 1), 0, M - 1);
-                slots[s].blk[blk].qa[warp] = qa_l;
-            }
-        }
+        // ---- B3: each lane walks its range again: tau (written), h zeroed, iterations
+        // per batch size, and A_q for the requests with tau(a_l) < r_q <= tau(b_l)
+        // (the first range also r_q <= tau(0)), merged in ready order
         for (int s = 0; s < nslots; ++s) {
             if (!((active >> s) & 1)) continue;
             DRelax &S = slots[s];
             const int64_t *dec_r = chains[S.chain].dec_r;
             const int32_t M = s_M[s], cap = s_cap[s], Lc = s_Lc[s];
             const int64_t n = (int64_t)Lc + 1;
-            int64_t w0, w1;
-            warp_tiles(n, warp, w0, w1);
-            unsigned long long carry = s_c1[s];
-            for (int w = 0; w < warp; ++w) carry += s_wsum[s][w];
-            int64_t x = __shfl_sync(FULL, x_l, s);
-            int32_t qp = __shfl_sync(FULL, qa_l, s);
-            int64_t pb = -1;  // run-length histogram of b over the lane's boundaries
+            int64_t a_l, b_l;
+            lane_range(n, a_l, b_l);
+            unsigned long long P = s_c1[s] + s_lc[s * RX_THREADS + tid];
+            int64_t x = s_c2[s];
+            for (int w = 0; w < warp; ++w) {
+                P += s_wsum[s][w];
+                x = rx_apply(RxMap{s_wa[s][w], s_wb[s][w]}, x);
+            }
+            x = rx_apply(RxMap{s_la[s * RX_THREADS + tid], s_lb[s * RX_THREADS + tid]}, x);  // tau(a_l)
+            int32_t qp = 0;
+            if (a_l < b_l && a_l > 0) {  // first request with r > tau(a_l) (warm start: last sweep's)
+                qp = rx_search([&](int32_t i) { return __ldg(dec_r + i); }, x + 1,
+                               min(max(__ldcg(&S.blk[blk].qa[tid]), 0), max(M - 1, 0)), 0, M - 1);
+                S.blk[blk].qa[tid] = qp;
+            }
+            int64_t rq = (a_l < b_l && qp < M) ? __ldg(dec_r + qp) : INT64_MAX;
+            int64_t rq2 = (a_l < b_l && qp + 1 < M) ? __ldg(dec_r + qp + 1) : INT64_MAX;
+            auto consume = [&](int64_t tau_at, int64_t I) {
+                while (rq <= tau_at) {
+                    S.A[qp] = (int32_t)I;
+                    ++qp;
+                    rq = rq2;
+                    rq2 = qp + 1 < M ? __ldg(dec_r + qp + 1) : INT64_MAX;
+                }
+            };
+            if (a_l == 0 && a_l < b_l) consume(x, 0);  // ready by tau(0): boundary 0
+            int64_t pb = -1;  // run-length histogram of b
             uint32_t run = 0;
-            int64_t rn = qp + lane < M ? __ldg(dec_r + qp + lane) : INT64_MAX;  // next merge candidates
-            for (int64_t st = w0; st < w1; ++st) {
-                const int64_t e0 = st * 256 + RX_EPT * lane;
+            unsigned long long vn[RX_EPT];  // the next unit, loaded ahead
+            if (a_l < b_l) load8(S.h, a_l, b_l, vn);
+            for (int64_t e0 = a_l; e0 < b_l; e0 += RX_EPT) {
                 unsigned long long v[RX_EPT];
-                load8(S.h, e0, n, v);
-                prefix8(v, carry);
-                RxMap mk[RX_EPT];
-                RxMap cm{0, NEG_INF};
+#pragma unroll
+                for (int k = 0; k < RX_EPT; ++k) v[k] = vn[k];
+                if (e0 + RX_EPT < b_l) load8(S.h, e0 + RX_EPT, b_l, vn);
+                int64_t tv[RX_EPT];
 #pragma unroll
                 for (int k = 0; k < RX_EPT; ++k) {
-                    mk[k] = RxMap{0, NEG_INF};
-                    if (e0 + k < n) {
-                        mk[k] = rx_iter_map(v[k], s_step[s], cap, M, dec_r);
-                        const int64_t b = (int64_t)(v[k] >> 32) - (int64_t)(v[k] & 0xFFFFFFFFull);
+                    tv[k] = x;
+                    if (e0 + k < b_l) {
+                        P += v[k];
+                        const int64_t b = (int64_t)(P >> 32) - (int64_t)(P & 0xFFFFFFFFull);
                         if (b != pb) {
                             if (run && pb >= 0 && pb <= RX_MAXCAP) atomicAdd(&s_hist[pb], run);
                             pb = b;
                             run = 0;
                         }
                         ++run;
-                    }
-                    cm = rx_then(cm, mk[k]);
-                }
-                RxMap in = cm;
-                for (int o = 1; o < 32; o <<= 1) {
-                    const RxMap y = rx_shfl_up(in, o);
-                    if (lane >= o) in = rx_then(y, in);
-                }
-                RxMap ex = rx_shfl_up(in, 1);
-                if (lane == 0) ex = RxMap{0, NEG_INF};
-                int64_t y = rx_apply(ex, x);
-                int64_t tv[RX_EPT];
-#pragma unroll
-                for (int k = 0; k < RX_EPT; ++k) {
-                    tv[k] = y;
-                    y = rx_apply(mk[k], y);
-                    if (e0 + k == Lc) {
-                        S.tau[Lc + 1] = y;
-                        S.tend = y;
+                        x = rx_apply(rx_iter_map(P, s_step[s], cap, M, dec_r), x);  // tau(e + 1)
+                        consume(x, e0 + k + 1);
                     }
                 }
-                if (e0 + RX_EPT <= n) {
+                if (e0 + RX_EPT <= b_l) {
                     longlong2 *dt = reinterpret_cast<longlong2 *>(S.tau + e0);
 #pragma unroll
                     for (int k = 0; k < RX_EPT / 2; ++k) dt[k] = make_longlong2(tv[2 * k], tv[2 * k + 1]);
@@ -756,43 +753,15 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
                 } else {
 #pragma unroll
                     for (int k = 0; k < RX_EPT; ++k)
-                        if (e0 + k < n) {
+                        if (e0 + k < b_l) {
                             S.tau[e0 + k] = tv[k];
                             S.h[e0 + k] = 0u;
                         }
                 }
-                const int64_t xn = rx_apply(rx_shfl(in, 31), x);  // tau at the next tile's start
-                // A_q for r_q in (tau(base), tau(base + 256)] (and r_q <= tau(0) at base 0)
-#pragma unroll
-                for (int k = 0; k < RX_EPT; ++k) s_tile[warp][RX_EPT * lane + k] = tv[k];
-                if (lane == 0) s_tile[warp][256] = xn;
-                __syncwarp();
-                const int lo0 = st == 0 ? 0 : 1;
-                for (;;) {
-                    const int32_t q = qp + lane;
-                    const int64_t rq = rn;
-                    const bool ok = rq <= xn;
-                    const unsigned bal = __ballot_sync(FULL, ok);
-                    {  // the candidates after this round's consumed ones
-                        const int c = __popc(bal);
-                        const int32_t qn = qp + c + lane;
-                        const int64_t sh = __shfl_sync(FULL, rq, (lane + c) & 31);
-                        rn = lane + c < 32 ? sh : (qn < M ? __ldg(dec_r + qn) : INT64_MAX);
-                    }
-                    if (ok) {
-                        int a = lo0 - 1, bnd = 256;  // first index in [lo0, 256] with tau >= rq
-                        while (bnd - a > 1) {
-                            const int m = (a + bnd) >> 1;
-                            if (s_tile[warp][m] >= rq) bnd = m;
-                            else a = m;
-                        }
-                        S.A[q] = (int32_t)(st * 256 + bnd);
-                    }
-                    qp += __popc(bal);
-                    if (bal != FULL) break;
-                }
-                __syncwarp();
-                x = xn;
+            }
+            if (a_l < b_l && b_l == n) {  // the slot's last boundary: tau(Lc + 1)
+                S.tau[n] = x;
+                S.tend = x;
             }
             if (run && pb >= 0 && pb <= RX_MAXCAP) atomicAdd(&s_hist[pb], run);
             __syncthreads();
