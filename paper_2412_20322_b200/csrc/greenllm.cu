@@ -912,8 +912,10 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                     int32_t dbg = dbg_env ? std::atoi(dbg_env) : 0;
                     void *args[] = {&d_slots, &ns, (void *)&dc, &dbg};
                     prof_begin("k_relax", xs);
+                    int rx_blocks = n_sm;  // GL_RELAX_BLOCKS (experiments): fewer SMs
+                    if (const char *rb = std::getenv("GL_RELAX_BLOCKS")) rx_blocks = std::max(1, std::min(n_sm, std::atoi(rb)));
                     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(gl::k_relax),
-                                                    dim3((unsigned)n_sm), dim3(gl::RX_THREADS), args, rx_smem, xs);
+                                                    dim3((unsigned)rx_blocks), dim3(gl::RX_THREADS), args, rx_smem, xs);
                     prof_end(xs);
                     ++launches;
                 }
