@@ -588,16 +588,14 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
             __threadfence();
             st_release_gpu(&B.f1, ep);
         }
+        grid.sync();  // every block's aggregate is published
         for (int s = warp; s < nslots; s += RX_WARPS) {  // carry: predecessors' sums
             if (!((active >> s) & 1)) continue;
             const RxBlk *bl = slots[s].blk;
             unsigned long long c = 0;
             for (int32_t j0 = 0; j0 < blk; j0 += 32) {
                 const int32_t j = j0 + lane;
-                if (j < blk) {
-                    while (ld_acquire_gpu(&bl[j].f1) < ep) rx_spin();
-                    c += __ldcg(&bl[j].s1);
-                }
+                if (j < blk) c += __ldcg(&bl[j].s1);
             }
             for (int o = 16; o; o >>= 1) c += __shfl_xor_sync(FULL, c, o);
             if (lane == 0) s_c1[s] = c;
@@ -662,6 +660,7 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
             __threadfence();
             st_release_gpu(&B.f2, ep);
         }
+        grid.sync();  // every block's aggregate is published
         for (int s = warp; s < nslots; s += RX_WARPS) {  // carry: tau at the block's start
             if (!((active >> s) & 1)) continue;
             const RxBlk *bl = slots[s].blk;
@@ -669,10 +668,7 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
             for (int32_t j0 = 0; j0 < blk; j0 += 32) {
                 const int32_t j = j0 + lane;
                 RxMap m{0, NEG_INF};
-                if (j < blk) {
-                    while (ld_acquire_gpu(&bl[j].f2) < ep) rx_spin();
-                    m = RxMap{__ldcg(&bl[j].a2), __ldcg(&bl[j].b2)};
-                }
+                if (j < blk) m = RxMap{__ldcg(&bl[j].a2), __ldcg(&bl[j].b2)};
                 for (int o = 1; o < 32; o <<= 1) {  // in lane order: lane 0's map first
                     const RxMap y = RxMap{__shfl_down_sync(FULL, m.a, o), __shfl_down_sync(FULL, m.b, o)};
                     if ((lane & (2 * o - 1)) == 0 && lane + o < 32) m = rx_then(m, y);
@@ -805,16 +801,14 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
                 st_release_gpu(&B.fc, ep);
             }
         }
+        grid.sync();  // every block's aggregate is published
         for (int s = warp; s < nslots; s += RX_WARPS) {  // carry: predecessors' maxima
             if (!((active >> s) & 1)) continue;
             const RxBlk *bl = slots[s].blk;
             int32_t c = INT32_MIN;
             for (int32_t j0 = 0; j0 < blk; j0 += 32) {
                 const int32_t j = j0 + lane;
-                if (j < blk) {
-                    while (ld_acquire_gpu(&bl[j].fc) < ep) rx_spin();
-                    c = max(c, __ldcg(&bl[j].mc));
-                }
+                if (j < blk) c = max(c, __ldcg(&bl[j].mc));
             }
             for (int o = 16; o; o >>= 1) c = max(c, __shfl_xor_sync(FULL, c, o));
             if (lane == 0) s_cq[s] = c;
