@@ -7,7 +7,7 @@ Exercises: gl_eval_grid (DPD, DSD, Standalone, co-located SpecDecode chains; cap
 k_stages on a side stream and the fill pass; DSD families; the two-phase launch
 order of gl_eval_grid_sched / gl_evaluate_host_sched), gl_argmin_feasible,
 gl_link_demand, gl_savings_surface, gl_complete_matrices (cooperative and
-one-CTA paths), gl_argmin_matrices, gl_evaluate_host.
+one-CTA paths), gl_argmin_matrices, gl_evaluate_host, and k_relax alone and racing k_decode.
 """
 import sys
 
@@ -59,6 +59,19 @@ def main():
         choice, fb = api.argmin_matrices(out[0], out[0].clamp(0, 1))
         torch.cuda.synchronize()
         print("als", (B, R, C, k), "status", status.cpu().tolist()[:3], flush=True)
+    # k_relax: alone (solo: it owns what it solves, k_decode walks the rest) and racing
+    import os
+    for mode, g in (("solo", build_config(4, n=1500)), ("solo", build_config(2, n=800)),
+                    ("1", build_config(4, n=9000))):
+        os.environ["GL_RELAX"] = mode
+        if mode == "1":
+            os.environ["GL_RELAX_RHO"] = "0.0,10.0"
+        dg = api.DeviceGrid(g)
+        stats, rows = api.eval_grid(dg, per_request=True)
+        torch.cuda.synchronize()
+        print("relax", mode, g.name, "ok", flush=True)
+    os.environ.pop("GL_RELAX", None)
+    os.environ.pop("GL_RELAX_RHO", None)
     print("sanitize_run done")
 
 
