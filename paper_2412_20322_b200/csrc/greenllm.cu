@@ -564,7 +564,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     const size_t rx_b_seg = align256(sizeof(int32_t) * 2 * (size_t)rx_nsegcap);
     const size_t rx_b_l = align256(sizeof(int64_t) * (size_t)(rx_lcap + 1));   // tau
     const size_t rx_b_h = align256(sizeof(uint32_t) * (size_t)rx_lcap);        // histogram
-    const size_t rx_b_blk = align256(sizeof(gl::RxBlk) * (size_t)n_sm);
+    const size_t rx_b_blk = align256(sizeof(gl::RxBlk) * (size_t)n_sm * gl::RX_BPS);
     int32_t rx_slots = 0;
     if (rx_elig > 0) {
         const size_t per = 3 * rx_b_j + rx_b_seg + rx_b_l + rx_b_h + rx_b_blk;
@@ -912,8 +912,9 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
                     int32_t dbg = dbg_env ? std::atoi(dbg_env) : 0;
                     void *args[] = {&d_slots, &ns, (void *)&dc, &dbg};
                     prof_begin("k_relax", xs);
-                    int rx_blocks = n_sm;  // GL_RELAX_BLOCKS (experiments): fewer SMs
-                    if (const char *rb = std::getenv("GL_RELAX_BLOCKS")) rx_blocks = std::max(1, std::min(n_sm, std::atoi(rb)));
+                    int rx_blocks = n_sm * std::min(gl::RX_BPS, per_sm);  // GL_RELAX_BLOCKS: experiments
+                    if (const char *rb = std::getenv("GL_RELAX_BLOCKS"))
+                        rx_blocks = std::max(1, std::min(n_sm * std::min(gl::RX_BPS, per_sm), std::atoi(rb)));
                     e = cudaLaunchCooperativeKernel(reinterpret_cast<const void *>(gl::k_relax),
                                                     dim3((unsigned)rx_blocks), dim3(gl::RX_THREADS), args, rx_smem, xs);
                     prof_end(xs);

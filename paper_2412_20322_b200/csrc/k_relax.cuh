@@ -52,6 +52,7 @@ constexpr int RX_SEG = 1024;      // decode requests per guess segment
 constexpr int RX_WU = 128;        // warm-up requests simulated before a segment
 constexpr int RX_GWARPS = 4;      // guess warps per block
 constexpr int RX_THREADS = 256;   // k_relax block
+constexpr int RX_BPS = 2;         // k_relax blocks per SM
 constexpr int RX_EPT = 8;         // iterations per lane per warp step
 constexpr int RX_WARPS = RX_THREADS / 32;
 constexpr int RX_MAX_SLOTS = 16;
@@ -391,7 +392,7 @@ __device__ __forceinline__ RxMap rx_shfl(RxMap m, int l)
 // Each block owns a contiguous chunk of every slot's iterations (and requests); its
 // warps stream contiguous sub-chunks 256 iterations at a time with warp scans, and
 // a block's carries come from its predecessors' published aggregates.
-__global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room beside k_decode
+__global__ void __launch_bounds__(RX_THREADS, RX_BPS + 1)  // registers: room beside k_decode
     k_relax(DRelax *__restrict__ slots, int32_t nslots, const DChain *__restrict__ chains, int32_t dbg)
 {
     namespace cg = cooperative_groups;
@@ -455,7 +456,7 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
     __syncthreads();
     grid.sync();
 
-    uint64_t tph[4] = {0, 0, 0, 0}, pv[4] = {0, 0, 0, 0}, t_last = rx_now();
+    uint64_t tph[8] = {0, 0, 0, 0, 0, 0, 0, 0}, pv[4] = {0, 0, 0, 0}, t_last = rx_now();
     auto lap = [&](int k) {
         const uint64_t t = rx_now();
         tph[k] += t - t_last;
@@ -601,6 +602,7 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
             if (lane == 0) s_c1[s] = c;
         }
         __syncthreads();
+        lap(4);
         // ---- B2: each lane walks its range: prefix P, the iterations' maps (lane map),
         // S_q at the boundary where the leave count G reaches q - cap + 1
         for (int s = 0; s < nslots; ++s) {
@@ -678,6 +680,7 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
             if (lane == 0) s_c2[s] = rx_apply(acc, __ldg(chains[slots[s].chain].dec_r));
         }
         __syncthreads();
+        lap(5);
         // ---- B3: each lane walks its range again: tau (written), h zeroed, iterations
         // per batch size, and A_q for the requests with tau(a_l) < r_q <= tau(b_l)
         // (the first range also r_q <= tau(0)), merged in ready order
@@ -861,8 +864,9 @@ __global__ void __launch_bounds__(RX_THREADS, 2)  // <= 128 registers: room besi
     if (dbg) {
         grid.sync();
         if (blk == 0 && tid == 0) {
-            printf("k_relax %d sweeps: scatter %.3f ms, iterations %.3f ms, requests %.3f + %.3f ms\n", sw,
-                   tph[0] * 1e-6, tph[1] * 1e-6, tph[2] * 1e-6, tph[3] * 1e-6);
+            printf("k_relax %d sweeps: scatter %.3f ms, iterations %.3f ms (B1 %.3f, B2 %.3f, B3 %.3f), requests %.3f + %.3f ms\n", sw,
+                   tph[0] * 1e-6, (tph[4] + tph[5] + tph[1]) * 1e-6, tph[4] * 1e-6, tph[5] * 1e-6, tph[1] * 1e-6,
+                   tph[2] * 1e-6, tph[3] * 1e-6);
             for (int s = 0; s < nslots; ++s)
                 if (slots[s].chain >= 0)
                     printf("k_relax slot %d chain %d M %d state %d sweeps %d Lf %d pad %x\n", s,
