@@ -552,8 +552,10 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         for (int32_t i = 0; i < n_chains; ++i) {
             const gl_chain &c = chains[i];
             const int64_t n = traces[c.trace_idx].n;
+            // (by default not on 1M-request traces: their heavy chains are saturated ones
+            // that do not relax in time, and the slots would take ~4 GiB of scratch)
             if ((c.mode == GL_MODE_DPD || c.mode == GL_MODE_DSD) && c.batch_cap <= gl::RX_MAXCAP &&
-                n >= (rx_force ? 1 : gl::RX_MIN_M)) {
+                n >= (rx_force ? 1 : gl::RX_MIN_M) && (rx_force || n <= gl::RX_MAX_N)) {
                 ++rx_elig;
                 rx_ncap = std::max(rx_ncap, n);
             }

@@ -60,6 +60,7 @@ constexpr int RX_MAX_SWEEPS = 160;
 constexpr int RX_LFACTOR = 40;    // iteration capacity per request
 constexpr int RX_MAXCAP = 31;     // one member per lane in the guess
 constexpr int32_t RX_MIN_M = 8192;
+constexpr int64_t RX_MAX_N = 262144;  // default eligibility: traces up to this many requests
 constexpr double RX_RHO_LO = 0.73, RX_RHO_HI = 0.82;
 constexpr int RX_DEF_SLOTS = 8;   // slots per call (GL_RELAX=force: up to 16)
 
