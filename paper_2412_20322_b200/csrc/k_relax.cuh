@@ -2,9 +2,9 @@
 // parallel-in-time fixed point (DESIGN.md §4 "k_relax").
 //
 // k_decode walks a chain's decode stage serially and parallelises it only at idle
-// points.  A chain loaded to 0.6-0.9 of its decode capacity runs one busy period of
+// points.  A chain loaded to ~0.75 of its decode capacity runs one busy period of
 // ~10^5 requests without an idle point, so its serial walk is the step's critical
-// path.  Here the same stage is solved for all requests at once.
+// path.  Here the same stage is solved for all requests at once (R57).
 //
 // Iteration domain.  Boundary I (= 0, 1, ...) of a chain's decode stage has a time
 // tau(I); iteration I runs from tau(I) to tau(I + 1) with b(I) members.  Decode
@@ -22,19 +22,22 @@
 // causal, so the system has exactly one solution, the serial simulation's.
 //
 // Relaxation.  Start from a guess of J and apply the rules as a map
-//   J -> b, tau (two scans over iterations) -> A, S (searches) -> J' (prefix max)
+//   J -> b, tau (scans over the boundaries) -> A, S (scattered / merged while the
+//   boundaries are walked) -> J' (prefix max)
 // until J' = J; the fixed point is the unique solution (bit-exact, integer).  The
 // prefix before the first wrong J_q is exact after every sweep, so it converges;
-// from a good guess it takes ~30 sweeps on config 4's heavy chains (prototype,
-// DESIGN.md §10).  The guess: k_relax_guess simulates every 1,024-request segment
+// from a good guess it takes ~30 sweeps on config 4's chains 33 and 51, 88 on 63
+// and 133 on 46, whose long saturated stretches fix joins by earlier leaves only
+// (DESIGN.md §10).  The guess: k_relax_guess simulates every 1,024-request segment
 // serially (one warp each, all segments at once) from an empty batch 128 requests
 // earlier; the segments' local iteration numbers are stitched by a prefix sum.
 // For convergence only, b > cap (possible in an iterate, never in the solution)
 // extrapolates the step table linearly.
 //
 // k_relax is one cooperative kernel (grid barriers between phases) over all
-// selected chains (slots); the iteration and request scans are single-pass
-// block-contiguous streaming scans.  It races k_decode, which walks the same chains:
+// selected chains (slots); every block owns a contiguous chunk of each slot's
+// boundaries and requests, every lane a contiguous run, and block carries come from
+// the predecessors' aggregates after a grid barrier.  It races k_decode, which walks the same chains:
 // whichever finishes a chain first owns its statistics (DChainX::pad bits); both
 // write identical finish times, and the loser stops early (k_decode's leader polls
 // the flag every 128 requests, k_relax every sweep).  A chain that outgrows its
@@ -263,7 +266,7 @@ __device__ __forceinline__ void st_release_u64(unsigned long long *p, unsigned l
 }
 
 // first I in [lo, hi] with v(I) >= x (v nondecreasing), hi + 1 if none; galloping from s
-__device__ unsigned long long g_rx_probes[4];  // debug: searches, probes
+__device__ unsigned long long g_rx_probes[4];  // GL_RX_TRACE builds: searches, probes
 template <typename V>
 __device__ __forceinline__ int32_t rx_search(V v, int64_t x, int32_t s, int32_t lo, int32_t hi)
 {
