@@ -63,7 +63,8 @@ constexpr int RX_MAX_SWEEPS = 160;
 constexpr int RX_LFACTOR = 40;    // iteration capacity per request
 constexpr int RX_MAXCAP = 31;     // one member per lane in the guess
 constexpr int32_t RX_MIN_M = 8192;
-constexpr int64_t RX_MAX_N = 262144;  // default eligibility: traces up to this many requests
+constexpr int64_t RX_MAX_N = 262144;
+constexpr int32_t RX_MAX_NSEG = 4;   // k_segments' idle-point candidates: more = k_decode's helpers parallelise it  // default eligibility: traces up to this many requests
 constexpr double RX_RHO_LO = 0.73, RX_RHO_HI = 0.82;
 constexpr int RX_DEF_SLOTS = 8;   // slots per call (GL_RELAX=force: up to 16)
 
@@ -142,7 +143,10 @@ __global__ void k_relax_pick(const DChain *__restrict__ chains, int32_t n_chains
         int32_t bc = -1;
         for (int32_t c = lane; c < n_chains; c += 32) {
             const double v = rho[c];
-            if (v >= rho_lo && v < rho_hi && chains[c].x->M <= slots[s].ncap && v > best) {
+            // long busy periods only: a chain with many idle-point candidates is walked in
+            // parallel by k_decode's helpers already (config 4's chain 21: 3 ms)
+            if (v >= rho_lo && v < rho_hi && chains[c].x->M <= slots[s].ncap && v > best &&
+                (rho_hi > 1e200 || chains[c].x->nseg <= RX_MAX_NSEG)) {
                 best = v;
                 bc = c;
             }
