@@ -877,7 +877,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             double *d_rho = reinterpret_cast<double *>(scratch + off_rx_rho);
             prof_begin("k_relax_pick", stream);
             gl::k_relax_rho<<<(unsigned)n_chains, 256, 0, stream>>>(dc, stats_out, d_rho,
-                                                                   rx_force ? 1 : gl::RX_MIN_M);
+                                                                   rx_force ? 1 : gl::RX_MIN_M,
+                                                                   rx_force ? 1e300 : gl::RX_MAX_IPR);
             double rlo = rx_force ? 0.0 : gl::RX_RHO_LO, rhi = rx_force ? 1e300 : gl::RX_RHO_HI;
             if (const char *rr = std::getenv("GL_RELAX_RHO")) std::sscanf(rr, "%lf,%lf", &rlo, &rhi);
             gl::k_relax_pick<<<1, 32, 0, stream>>>(dc, n_chains, d_rho, d_slots, rx_slots, rlo, rhi);

@@ -64,7 +64,8 @@ constexpr int RX_LFACTOR = 40;    // iteration capacity per request
 constexpr int RX_MAXCAP = 31;     // one member per lane in the guess
 constexpr int32_t RX_MIN_M = 8192;
 constexpr int64_t RX_MAX_N = 262144;
-constexpr int32_t RX_MAX_NSEG = 4;   // k_segments' idle-point candidates: more = k_decode's helpers parallelise it  // default eligibility: traces up to this many requests
+constexpr int32_t RX_MAX_NSEG = 4;
+constexpr double RX_MAX_IPR = 10.0;  // iterations per request (estimated): a sweep costs O(iterations)   // k_segments' idle-point candidates: more = k_decode's helpers parallelise it  // default eligibility: traces up to this many requests
 constexpr double RX_RHO_LO = 0.73, RX_RHO_HI = 0.82;
 constexpr int RX_DEF_SLOTS = 8;   // slots per call (GL_RELAX=force: up to 16)
 
@@ -108,7 +109,7 @@ struct DRelax {
 // per us over the stage's capacity at a full batch.
 __global__ void __launch_bounds__(256)
     k_relax_rho(const DChain *__restrict__ chains, const gl_chain_stats *__restrict__ stats,
-                double *__restrict__ rho, int32_t min_m)
+                double *__restrict__ rho, int32_t min_m, double ipr_max)
 {
     __shared__ unsigned long long s_sum[8];
     const int c = blockIdx.x;
@@ -128,7 +129,12 @@ __global__ void __launch_bounds__(256)
     if (threadIdx.x == 0) {
         for (int w = 1; w < 8; ++w) s += s_sum[w];
         const int64_t span = max((int64_t)1, ch.dec_r[M - 1] - ch.dec_r[0]);
-        rho[c] = (double)s * (double)__ldg(ch.step + ch.cap) / (double)ch.cap / (double)span;
+        const double r_ = (double)s * (double)__ldg(ch.step + ch.cap) / (double)ch.cap / (double)span;
+        // a sweep costs O(boundaries) ~ sum K / mean batch ~ sum K / (rho cap), the serial
+        // walk O(requests): chains with many iterations per request (DPD chat chains,
+        // ~20) are cheaper to walk than to relax (ipr_max: GL_RELAX=force passes 1e300)
+        const double ipr = (double)s / (max(r_, 1e-9) * (double)ch.cap) / (double)M;
+        rho[c] = ipr <= ipr_max ? r_ : -1.0;
     }
 }
 
