@@ -548,6 +548,8 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
     const bool rx_solo = rx_env && rx_env[0] == 's';
     int64_t rx_ncap = 0;
     int32_t rx_elig = 0;
+    int64_t rx_max_n = gl::RX_MAX_N;  // GL_RELAX_MAXN: experiments
+    if (const char *mn = std::getenv("GL_RELAX_MAXN")) rx_max_n = std::atoll(mn);
     if (!lk && !phased && !rx_off)
         for (int32_t i = 0; i < n_chains; ++i) {
             const gl_chain &c = chains[i];
@@ -555,7 +557,7 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
             // (by default not on 1M-request traces: their heavy chains are saturated ones
             // that do not relax in time, and the slots would take ~4 GiB of scratch)
             if ((c.mode == GL_MODE_DPD || c.mode == GL_MODE_DSD) && c.batch_cap <= gl::RX_MAXCAP &&
-                n >= (rx_force ? 1 : gl::RX_MIN_M) && (rx_force || n <= gl::RX_MAX_N)) {
+                n >= (rx_force ? 1 : gl::RX_MIN_M) && (rx_force || n <= rx_max_n)) {
                 ++rx_elig;
                 rx_ncap = std::max(rx_ncap, n);
             }
