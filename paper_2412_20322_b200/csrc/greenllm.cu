@@ -877,10 +877,12 @@ gl_status eval_impl(const gl_trace *traces, int32_t n_traces, const gl_chain *ch
         if (relax) {
             gl::DRelax *d_slots = reinterpret_cast<gl::DRelax *>(scratch + off_rx_slots);
             double *d_rho = reinterpret_cast<double *>(scratch + off_rx_rho);
+            double rx_ipr = gl::RX_MAX_IPR;  // GL_RELAX_IPR: experiments
+            if (const char *ip = std::getenv("GL_RELAX_IPR")) rx_ipr = std::atof(ip);
             prof_begin("k_relax_pick", stream);
             gl::k_relax_rho<<<(unsigned)n_chains, 256, 0, stream>>>(dc, stats_out, d_rho,
                                                                    rx_force ? 1 : gl::RX_MIN_M,
-                                                                   rx_force ? 1e300 : gl::RX_MAX_IPR);
+                                                                   rx_force ? 1e300 : rx_ipr);
             double rlo = rx_force ? 0.0 : gl::RX_RHO_LO, rhi = rx_force ? 1e300 : gl::RX_RHO_HI;
             if (const char *rr = std::getenv("GL_RELAX_RHO")) std::sscanf(rr, "%lf,%lf", &rlo, &rhi);
             gl::k_relax_pick<<<1, 32, 0, stream>>>(dc, n_chains, d_rho, d_slots, rx_slots, rlo, rhi);
