@@ -69,3 +69,10 @@ def test_relax_race_config4_full_heavy_chains(monkeypatch):
     monkeypatch.setenv("GL_RELAX", "1")
     g = build_config(4)
     assert_parity(g, chain_ids=[33, 51, 63, 46, 26, 21])
+
+
+def test_relax_solo_stage_group_secondaries(solo):
+    """Config 5's stage groups: secondary chains share their primary's ready times and
+    bring their own DSD demand (k_stage_clone, a DSD family) -- relaxed all the same."""
+    g = build_config(5, n=3000)
+    assert_parity(subset_chains(g, list(range(0, 80))), per_request=True)
